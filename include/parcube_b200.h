@@ -1,0 +1,253 @@
+/*
+ * parcube_b200.h -- C-ABI of the B200-native PAGANI / m-Cubes hot path.
+ *
+ * The reference package (`parcube`, /root/reference/pkg/src/parcube) is pure Python and has
+ * no FFI of its own; its boundary is the Python function surface re-exported in
+ * __init__.py:11-83.  Each entry point below is what a ctypes binding placed behind one of
+ * those functions calls (INTEGRATION.md shows the stub).  Plain pointers and sizes only;
+ * all buffers are caller-owned HOST memory unless the name ends in `_dev`; one in-flight
+ * call per context.  Every function returns a pcb_status; pcb_last_error() gives the text.
+ *
+ * There is no CPU fallback: every entry point needs a CUDA device (sm_100a build).
+ */
+#ifndef PARCUBE_B200_H
+#define PARCUBE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCB_MAX_DIM 12 /* reference: core.py:14 */
+
+typedef enum {
+  PCB_OK = 0,
+  PCB_NONFINITE = 1, /* integrand returned NaN/inf: see pcb_nonfinite (core.py:26-37)   */
+  PCB_BUDGET = 2,    /* workload exceeds a cap (core.py:22-23, 262-263)                 */
+  PCB_INVALID = 3,   /* bad argument (the reference's ValueError paths)                 */
+  PCB_CUDA = 4       /* CUDA runtime failure                                            */
+} pcb_status;
+
+/* Integrand families = the reference registry BENCHMARKS (integrands.py:131-139). */
+typedef enum {
+  PCB_F1_OSCILLATORY = 0,   /* cos(sum i*x_i)                      integrands.py:28-39   */
+  PCB_F2_PRODUCT_PEAK = 1,  /* prod 1/(a^2+(x_i-1/2)^2)            integrands.py:42-53   */
+  PCB_F3_CORNER_PEAK = 2,   /* (1+sum i*x_i)^(-d-1)                integrands.py:56-67   */
+  PCB_F4_GAUSSIAN = 3,      /* exp(-rate*sum (x_i-1/2)^2)          integrands.py:70-81   */
+  PCB_F5_KINKED = 4,        /* exp(-10*sum |x_i-1/2|)              integrands.py:84-92   */
+  PCB_F6_DISCONTINUOUS = 5, /* exp(sum (i+4)x_i) below thresholds  integrands.py:95-118  */
+  PCB_SUM = 6,              /* sum x_i                             integrands.py:121-128 */
+  PCB_ONE = 7,              /* constant 1 (SPEC.md known answers)                        */
+  PCB_N_FAMILIES = 8
+} pcb_family;
+
+/* A compiled device functor is selected by (family, d); `param` carries the family's
+ * constants as computed by the host in the reference's own expressions:
+ *   f2: param[0] = a^2 (1/2500)   f4: param[0] = rate (625)   f5: param[0] = 10
+ *   f6: param[j] = threshold_j = (3 + (j+1)) / 10
+ * `bounded` applies scale_to_bounds (core.py:134-148): f(low + width*y) * jac.            */
+typedef struct {
+  int32_t family;
+  int32_t d;
+  int32_t bounded;
+  int32_t reserved;
+  double param[PCB_MAX_DIM];
+  double low[PCB_MAX_DIM];
+  double width[PCB_MAX_DIM];
+  double jac;
+} pcb_integrand;
+
+/* Orbit form of a RuleTable (quadrature.py:43-70): the table is input data, compressed by the
+ * host after verifying its fully symmetric structure (rules.py:orbit_form).
+ * offsets: 1/2, (1+l2)/2, (1-l2)/2, (1+l3)/2, (1-l3)/2, (1+l5)/2, (1-l5)/2 -- the values of
+ * (generators + 1.0) / 2.0 (quadrature.py:301).  weights[k][o]: rule k on orbit o
+ * (centre, l2-axial, l3-axial, l4-pairs, l5-corners); corner_parity[k] != 0 means the corner
+ * weight alternates in sign with the parity of the corner's bit count (quadrature.py:199-203). */
+typedef struct {
+  int32_t d;
+  int32_t f_eval;
+  double offsets[7];
+  double weights[5][5];
+  int32_t corner_parity[5];
+  int32_t reserved;
+  double split_weights[2]; /* quadrature.py:279 */
+  int32_t null_high[4];    /* null_degrees[k] >= 5 (pagani.py:123-124) */
+  double null_scale[4];    /* null_scales (pagani.py:126) */
+} pcb_rule;
+
+typedef enum { PCB_ERR_TWO_LEVEL = 0, PCB_ERR_MAX_NULL = 1, PCB_ERR_MAX_PAIRWISE = 2 } pcb_err_mode;
+
+/* The numerically relevant part of PaganiConfig (pagani.py:44-69). */
+typedef struct {
+  double rel_tol;
+  int32_t max_iterations;
+  int32_t group_size;      /* strided schedule width G, 1..64 (pagani.py:175-192) */
+  int64_t region_cap;
+  int32_t initial_regions;
+  int32_t err_mode;        /* pcb_err_mode */
+  double rel_floor;
+} pcb_pagani_config;
+
+/* First non-finite evaluation in row-major (region, point) order (pagani.py:206-209,
+ * mcubes.py:238-241). */
+typedef struct {
+  int64_t region_index; /* region (PAGANI) or sub-cube (m-Cubes) index */
+  int64_t point_index;  /* rule point or sample index inside it */
+  double value;
+  double point[PCB_MAX_DIM];
+} pcb_nonfinite;
+
+/* One record per refinement iteration == the reference's progress dict + history tuple
+ * (pagani.py:339-349). */
+typedef struct {
+  int32_t iteration;
+  int32_t reserved;
+  int64_t n_regions; /* leaves: finished + active */
+  int64_t active;
+  double estimate;
+  double errorest;
+} pcb_pagani_progress;
+
+typedef enum {
+  PCB_STOP_TOLERANCE = 0,  /* "tolerance met"            pagani.py:350-353 */
+  PCB_STOP_MAX_ITER = 1,   /* "max iterations reached"   pagani.py:354-356 */
+  PCB_STOP_NO_ACTIVE = 2,  /* "no active regions left"   pagani.py:357-359 */
+  PCB_STOP_REGION_CAP = 3  /* "region cap reached"       pagani.py:367-369 */
+} pcb_stop_reason;
+
+/* IntegralResult (pagani.py:89-101); history is returned through the progress records. */
+typedef struct {
+  double estimate;
+  double errorest;
+  int32_t iterations;
+  int32_t converged;
+  int64_t regions_processed;
+  int32_t reason; /* pcb_stop_reason */
+  int32_t n_records;
+  double seconds_device; /* CUDA-event time of the whole refinement, for reporting only */
+  int64_t kernel_launches;
+} pcb_pagani_result;
+
+typedef void (*pcb_pagani_progress_fn)(void* user, const pcb_pagani_progress* rec);
+
+/* McubesPlan (mcubes.py:77-107). */
+typedef struct {
+  int32_t d;
+  int32_t g;
+  int32_t p;
+  int32_t group_size;
+  int64_t m;
+  int64_t s;
+  int32_t n_bins;
+  int32_t reserved;
+} pcb_mcubes_plan;
+
+typedef enum {
+  PCB_RNG_REFERENCE_HASH = 0, /* the reference's SplitMix64-style hash (mcubes.py:31-55): bit-exact */
+  PCB_RNG_PHILOX = 1,         /* Philox4x32-10 keyed by (seed, stream), counter-indexed             */
+  PCB_RNG_INJECTED = 2        /* uniforms read from a caller table, index (cube*p + k)*d + j          */
+} pcb_rng_kind;
+
+/* McubesIterationResult (mcubes.py:182-192) minus the table, which is an output array. */
+typedef struct {
+  double integral;
+  double variance;
+  int64_t n_samples;
+  int64_t clamp_events;
+} pcb_mcubes_iteration;
+
+typedef struct {
+  int32_t iteration;
+  int32_t reserved;
+  double estimate;
+  double errorest;
+  double chi2_per_dof;
+  double iter_integral;
+  double iter_variance;
+} pcb_mcubes_progress;
+
+typedef void (*pcb_mcubes_progress_fn)(void* user, const pcb_mcubes_progress* rec);
+
+typedef struct pcb_ctx pcb_ctx;
+
+/* ---- context ------------------------------------------------------------------------- */
+pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out);
+void pcb_ctx_destroy(pcb_ctx* ctx);
+const char* pcb_last_error(const pcb_ctx* ctx);
+/* name and SM count of the context's device, multiprocessor clock in kHz */
+pcb_status pcb_device_info(pcb_ctx* ctx, char* name, int name_len, int32_t* sm_count, int32_t* clock_khz);
+/* kernels launched by this context since creation (bench.py "gpu_launches") */
+int64_t pcb_launch_count(const pcb_ctx* ctx);
+/* Measured FP64 peak: runs a dependent-free DFMA loop on every SM; returns TFLOP/s. */
+pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops);
+
+/* ---- integrand functors: replaces Integrand.eval_many (core.py:66-68, integrands.py) --- */
+pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points /* (n,d) */,
+                           double* values /* (n) */);
+
+/* ---- PAGANI evaluate: replaces pagani_kernel (pagani.py:227-257) ------------------------
+ * lefts/lengths: (n,d) row-major as in RegionList (core.py:187-207); outputs as in
+ * RegionEstimates (core.py:224-247): integrals, errors float64, split_axes int64.            */
+pcb_status pcb_pagani_evaluate(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule,
+                               const pcb_pagani_config* cfg, int64_t n, const double* lefts,
+                               const double* lengths, double* integrals, double* errors,
+                               int64_t* split_axes, pcb_nonfinite* bad);
+/* Same on device-resident structure-of-arrays buffers: lefts_dev[j*ld + r]; split_axes int32. */
+pcb_status pcb_pagani_evaluate_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule,
+                                   const pcb_pagani_config* cfg, int64_t n, int64_t ld,
+                                   const double* lefts_dev, const double* lengths_dev,
+                                   double* integrals_dev, double* errors_dev, int32_t* split_axes_dev,
+                                   pcb_nonfinite* bad);
+/* quadrature.apply_rules (quadrature.py:305-322): one region, plain pair tree over all points */
+pcb_status pcb_apply_rules(pcb_ctx* ctx, const pcb_integrand* f, int32_t f_eval, const double* generators,
+                           const double* weights, const double* left, const double* length,
+                           double values[5], double* stored_evals, pcb_nonfinite* bad);
+
+/* ---- PAGANI refine: replaces refine (pagani.py:300-391), whole loop device-resident -------
+ * records: capacity cfg->max_iterations + 1.  progress may be NULL.                            */
+pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule,
+                             const pcb_pagani_config* cfg, pcb_pagani_result* result,
+                             pcb_pagani_progress* records, pcb_pagani_progress_fn progress, void* user,
+                             pcb_nonfinite* bad);
+
+/* ---- fixed-shape reductions: replaces engine.tree_sum (engine.py:69-86) --------------- */
+pcb_status pcb_tree_sum(pcb_ctx* ctx, int64_t n, const double* values, double* out);
+
+/* ---- m-Cubes V-Sample: replaces mcubes_kernel (mcubes.py:268-308) ------------------------
+ * boundaries: (d, n_bins+1) as VegasGrid.boundaries (vegas_grid.py:21-43).
+ * Logical threads [thread_begin, thread_end) are processed (whole range = one GPU; a
+ * sub-range = one shard, mcubes.py:224-232 makes draws independent of the partition).
+ * group_partials (optional, may be NULL): (n_groups_touched, 2) per-work-group (I, Var) partial
+ * sums in group order starting at group thread_begin / group_size (mcubes.py:292-293).
+ * contributions: (d, n_bins) (mcubes.py:294-298).                                            */
+pcb_status pcb_mcubes_sample(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan,
+                             const double* boundaries, uint64_t seed, int32_t rng_kind,
+                             const double* injected_uniforms, int32_t squared_weighted,
+                             int64_t thread_begin, int64_t thread_end, pcb_mcubes_iteration* out,
+                             double* contributions, double* group_partials, pcb_nonfinite* bad);
+
+/* ---- grid refinement: replaces refine_grid (vegas_grid.py:142-193) --------------------- */
+pcb_status pcb_grid_refine(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double* boundaries,
+                           const double* contributions, double alpha, int32_t smoothing,
+                           double* new_boundaries);
+
+/* ---- m-Cubes driver: replaces run (mcubes.py:332-382), loop device-resident ---------------
+ * rel_tol <= 0 reproduces the reference (fixed iteration count); rel_tol > 0 adds the
+ * time-to-epsrel stop of BASELINE.md section 3.  iterations_out: capacity `iterations`.
+ * final_boundaries (optional): (d, n_bins+1).                                                 */
+pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan,
+                          int32_t iterations, uint64_t seed, int32_t rng_kind, int32_t adapt, double alpha,
+                          int32_t smoothing, double rel_tol, pcb_mcubes_iteration* iterations_out,
+                          int32_t* n_done, pcb_mcubes_progress_fn progress, void* user,
+                          double* contributions_out /* optional (iterations, d, n_bins) */,
+                          double* final_boundaries, double* seconds_device, pcb_nonfinite* bad);
+
+/* ---- RNG mirror: replaces mcubes._uniform / derive_seed (mcubes.py:51-60) -------------- */
+pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,
+                        const uint64_t* counters, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARCUBE_B200_H */

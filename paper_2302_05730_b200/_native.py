@@ -1,0 +1,449 @@
+"""ctypes binding of libparcube_b200.so (the C-ABI declared in include/parcube_b200.h).
+
+This module is the only place that touches the shared library.  It fails loudly:
+a missing library or a missing CUDA device raises, nothing falls back to the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+MAX_DIM = 12
+LIB_NAME = "libparcube_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+PCB_OK, PCB_NONFINITE, PCB_BUDGET, PCB_INVALID, PCB_CUDA = range(5)
+RNG_REFERENCE_HASH, RNG_PHILOX, RNG_INJECTED = range(3)
+ERR_MODES = {"two-level": 0, "max-null": 1, "max-pairwise": 2}
+STOP_REASONS = ("tolerance met", "max iterations reached", "no active regions left", "region cap reached")
+FAMILY_IDS = {"f1": 0, "f2": 1, "f3": 2, "f4": 3, "f5": 4, "f6": 5, "sum": 6, "one": 7}
+
+
+class NativeError(RuntimeError):
+    """CUDA / library level failure (status PCB_CUDA)."""
+
+
+class NonFiniteStatus(Exception):
+    """Internal carrier of a PCB_NONFINITE report; the API layers translate it."""
+
+    def __init__(self, region_index, point_index, value, point, message):
+        super().__init__(message)
+        self.region_index, self.point_index, self.value, self.point = region_index, point_index, value, point
+
+
+class BudgetStatus(Exception):
+    """Internal carrier of PCB_BUDGET."""
+
+
+# --------------------------------------------------------------------------- C structs
+class IntegrandC(C.Structure):
+    _fields_ = [("family", C.c_int32), ("d", C.c_int32), ("bounded", C.c_int32), ("reserved", C.c_int32),
+                ("param", C.c_double * MAX_DIM), ("low", C.c_double * MAX_DIM), ("width", C.c_double * MAX_DIM),
+                ("jac", C.c_double)]
+
+
+class RuleC(C.Structure):
+    _fields_ = [("d", C.c_int32), ("f_eval", C.c_int32), ("offsets", C.c_double * 7),
+                ("weights", (C.c_double * 5) * 5), ("corner_parity", C.c_int32 * 5), ("reserved", C.c_int32),
+                ("split_weights", C.c_double * 2), ("null_high", C.c_int32 * 4), ("null_scale", C.c_double * 4)]
+
+
+class PaganiConfigC(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("max_iterations", C.c_int32), ("group_size", C.c_int32),
+                ("region_cap", C.c_int64), ("initial_regions", C.c_int32), ("err_mode", C.c_int32),
+                ("rel_floor", C.c_double)]
+
+
+class NonFiniteC(C.Structure):
+    _fields_ = [("region_index", C.c_int64), ("point_index", C.c_int64), ("value", C.c_double),
+                ("point", C.c_double * MAX_DIM)]
+
+
+class PaganiProgressC(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("reserved", C.c_int32), ("n_regions", C.c_int64), ("active", C.c_int64),
+                ("estimate", C.c_double), ("errorest", C.c_double)]
+
+
+class PaganiResultC(C.Structure):
+    _fields_ = [("estimate", C.c_double), ("errorest", C.c_double), ("iterations", C.c_int32),
+                ("converged", C.c_int32), ("regions_processed", C.c_int64), ("reason", C.c_int32),
+                ("n_records", C.c_int32), ("seconds_device", C.c_double), ("kernel_launches", C.c_int64)]
+
+
+class McubesPlanC(C.Structure):
+    _fields_ = [("d", C.c_int32), ("g", C.c_int32), ("p", C.c_int32), ("group_size", C.c_int32), ("m", C.c_int64),
+                ("s", C.c_int64), ("n_bins", C.c_int32), ("reserved", C.c_int32)]
+
+
+class McubesIterationC(C.Structure):
+    _fields_ = [("integral", C.c_double), ("variance", C.c_double), ("n_samples", C.c_int64),
+                ("clamp_events", C.c_int64)]
+
+
+class McubesProgressC(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("reserved", C.c_int32), ("estimate", C.c_double), ("errorest", C.c_double),
+                ("chi2_per_dof", C.c_double), ("iter_integral", C.c_double), ("iter_variance", C.c_double)]
+
+
+PAGANI_PROGRESS_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(PaganiProgressC))
+MCUBES_PROGRESS_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(McubesProgressC))
+
+_DP = C.POINTER(C.c_double)
+# every exported symbol of include/parcube_b200.h with its signature (tests check the list)
+SIGNATURES = {
+    "pcb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "pcb_ctx_destroy": (None, [C.c_void_p]),
+    "pcb_last_error": (C.c_char_p, [C.c_void_p]),
+    "pcb_device_info": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "pcb_launch_count": (C.c_int64, [C.c_void_p]),
+    "pcb_measure_fp64_peak": (C.c_int, [C.c_void_p, _DP]),
+    "pcb_eval_points": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_void_p]),
+    "pcb_pagani_evaluate": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
+                                      C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(NonFiniteC)]),
+    "pcb_pagani_evaluate_dev": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
+                                          C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_apply_rules": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_pagani_refine": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
+                                    C.POINTER(PaganiResultC), C.POINTER(PaganiProgressC), PAGANI_PROGRESS_FN, C.c_void_p,
+                                    C.POINTER(NonFiniteC)]),
+    "pcb_tree_sum": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, _DP]),
+    "pcb_mcubes_sample": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_void_p, C.c_uint64,
+                                    C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(McubesIterationC),
+                                    C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_grid_refine": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
+                                  C.c_void_p]),
+    "pcb_mcubes_run": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_int32, C.c_uint64,
+                                 C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.POINTER(McubesIterationC),
+                                 C.POINTER(C.c_int32), MCUBES_PROGRESS_FN, C.c_void_p, C.c_void_p, C.c_void_p, _DP,
+                                 C.POINTER(NonFiniteC)]),
+    "pcb_uniforms": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+}
+
+_lib = None
+_lock = threading.Lock()
+_contexts: dict = {}
+
+
+def load_library():
+    """dlopen the in-tree library and bind every declared symbol; raises if anything is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise NativeError(f"{LIB_PATH} is missing: build it with `python -m paper_2302_05730_b200._build` "
+                              "(nvcc, sm_100a). There is no CPU fallback.")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)  # AttributeError if the symbol is not exported
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+class Context:
+    """One pcb_ctx (device, stream, scratch buffers).  One in-flight call at a time."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        handle = C.c_void_p()
+        status = self.lib.pcb_ctx_create(int(device), C.byref(handle))
+        self.handle = handle
+        if status != PCB_OK:
+            msg = self.last_error()
+            if handle:
+                self.lib.pcb_ctx_destroy(handle)
+            self.handle = None
+            raise NativeError(f"cannot create a B200 context on device {device}: {msg} (no CPU fallback exists)")
+        self.device = int(device)
+        self.call_lock = threading.Lock()
+
+    def last_error(self) -> str:
+        if not self.handle:
+            return "no context"
+        return (self.lib.pcb_last_error(self.handle) or b"").decode(errors="replace")
+
+    def close(self):
+        if self.handle:
+            self.lib.pcb_ctx_destroy(self.handle)
+            self.handle = None
+
+    def check(self, status: int, bad: NonFiniteC | None = None, d: int = 0):
+        if status == PCB_OK:
+            return
+        msg = self.last_error()
+        if status == PCB_NONFINITE:
+            point = np.array(bad.point[:d]) if bad is not None else np.full(max(d, 1), np.nan)
+            raise NonFiniteStatus(bad.region_index if bad is not None else None,
+                                  bad.point_index if bad is not None else None,
+                                  bad.value if bad is not None else float("nan"), point, msg)
+        if status == PCB_BUDGET:
+            raise BudgetStatus(msg)
+        if status == PCB_INVALID:
+            raise ValueError(msg)
+        raise NativeError(msg)
+
+    # ------------------------------------------------------------------ info
+    def device_info(self):
+        name = C.create_string_buffer(256)
+        sms, khz = C.c_int32(), C.c_int32()
+        self.check(self.lib.pcb_device_info(self.handle, name, 256, C.byref(sms), C.byref(khz)))
+        return name.value.decode(), sms.value, khz.value
+
+    def launch_count(self) -> int:
+        return int(self.lib.pcb_launch_count(self.handle))
+
+    def measure_fp64_peak(self) -> float:
+        out = C.c_double()
+        self.check(self.lib.pcb_measure_fp64_peak(self.handle, C.byref(out)))
+        return out.value
+
+
+def default_device() -> int:
+    env = os.environ.get("PARCUBE_B200_DEVICE")
+    if env is not None:
+        return int(env)
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def context(device: int | None = None) -> Context:
+    """Process-wide context cache, one per device ordinal."""
+    dev = default_device() if device is None else int(device)
+    with _lock:
+        ctx = _contexts.get(dev)
+    if ctx is None:
+        ctx = Context(dev)
+        with _lock:
+            _contexts.setdefault(dev, ctx)
+            ctx = _contexts[dev]
+    return ctx
+
+
+# --------------------------------------------------------------------------- marshalling helpers
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _f64(a, shape=None) -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None and out.shape != shape:
+        raise ValueError(f"expected shape {shape}, got {out.shape}")
+    return out
+
+
+class DeviceSpec:
+    """(family, d, params, optional bounds) -> pcb_integrand."""
+
+    def __init__(self, family: str, d: int, param=(), low=None, width=None, jac=1.0):
+        self.family, self.d = family, int(d)
+        self.param = tuple(float(v) for v in param)
+        self.low, self.width, self.jac = low, width, float(jac)
+
+    @property
+    def bounded(self) -> bool:
+        return self.low is not None
+
+    def with_bounds(self, low, width, jac) -> "DeviceSpec":
+        return DeviceSpec(self.family, self.d, self.param, np.array(low, dtype=float), np.array(width, dtype=float), jac)
+
+    def to_c(self) -> IntegrandC:
+        c = IntegrandC()
+        c.family, c.d, c.bounded = FAMILY_IDS[self.family], self.d, int(self.bounded)
+        for i, v in enumerate(self.param):
+            c.param[i] = v
+        if self.bounded:
+            for j in range(self.d):
+                c.low[j], c.width[j] = float(self.low[j]), float(self.width[j])
+        c.jac = self.jac
+        return c
+
+
+def rule_to_c(orbit) -> RuleC:
+    c = RuleC()
+    c.d, c.f_eval = orbit.d, orbit.f_eval
+    for i in range(7):
+        c.offsets[i] = float(orbit.offsets[i])
+    for k in range(5):
+        for o in range(5):
+            c.weights[k][o] = float(orbit.weights[k, o])
+        c.corner_parity[k] = int(orbit.corner_parity[k])
+    c.split_weights[0], c.split_weights[1] = float(orbit.split_weights[0]), float(orbit.split_weights[1])
+    for k in range(4):
+        c.null_high[k] = int(orbit.high_mask[k])
+        c.null_scale[k] = float(orbit.null_scales[k])
+    return c
+
+
+def pagani_config_to_c(cfg) -> PaganiConfigC:
+    c = PaganiConfigC()
+    c.rel_tol, c.max_iterations, c.group_size = float(cfg.rel_tol), int(cfg.max_iterations), int(cfg.group_size)
+    c.region_cap, c.initial_regions = int(cfg.region_cap), int(cfg.initial_regions)
+    c.err_mode, c.rel_floor = ERR_MODES[cfg.err_mode], float(cfg.rel_floor)
+    return c
+
+
+def plan_to_c(plan, n_bins: int) -> McubesPlanC:
+    c = McubesPlanC()
+    c.d, c.g, c.p, c.group_size, c.m, c.s, c.n_bins = plan.d, plan.g, plan.p, plan.group_size, plan.m, plan.s, int(n_bins)
+    return c
+
+
+# --------------------------------------------------------------------------- calls
+def eval_points(spec: DeviceSpec, points: np.ndarray, device=None) -> np.ndarray:
+    ctx = context(device)
+    pts = _f64(points)
+    out = np.empty(pts.shape[0], dtype=np.float64)
+    fc = spec.to_c()
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_eval_points(ctx.handle, C.byref(fc), pts.shape[0], _ptr(pts), _ptr(out)))
+    return out
+
+
+def tree_sum_1d(values: np.ndarray, device=None) -> float:
+    ctx = context(device)
+    v = _f64(values).ravel()
+    out = C.c_double()
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_tree_sum(ctx.handle, v.size, _ptr(v), C.byref(out)))
+    return out.value
+
+
+def pagani_evaluate(spec: DeviceSpec, orbit, cfg, lefts: np.ndarray, lengths: np.ndarray, device=None):
+    ctx = context(device)
+    n, d = lefts.shape
+    lefts, lengths = _f64(lefts), _f64(lengths)
+    i_out, e_out = np.empty(n), np.empty(n)
+    k_out = np.empty(n, dtype=np.int64)
+    fc, rc, cc, bad = spec.to_c(), rule_to_c(orbit), pagani_config_to_c(cfg), NonFiniteC()
+    with ctx.call_lock:
+        st = ctx.lib.pcb_pagani_evaluate(ctx.handle, C.byref(fc), C.byref(rc), C.byref(cc), n, _ptr(lefts), _ptr(lengths),
+                                         _ptr(i_out), _ptr(e_out), _ptr(k_out), C.byref(bad))
+        ctx.check(st, bad, d)
+    return i_out, e_out, k_out
+
+
+def pagani_refine(spec: DeviceSpec, orbit, cfg, progress=None, device=None):
+    ctx = context(device)
+    fc, rc, cc, bad = spec.to_c(), rule_to_c(orbit), pagani_config_to_c(cfg), NonFiniteC()
+    res = PaganiResultC()
+    records = (PaganiProgressC * (int(cfg.max_iterations) + 1))()
+    failure = []
+
+    def _cb(_user, rec):
+        if progress is None or failure:
+            return
+        try:
+            r = rec.contents
+            progress({"iteration": r.iteration, "n_regions": int(r.n_regions), "active": int(r.active),
+                      "estimate": r.estimate, "errorest": r.errorest})
+        except BaseException as exc:  # noqa: BLE001 - re-raised after the native call returns
+            failure.append(exc)
+
+    cb = PAGANI_PROGRESS_FN(_cb)
+    with ctx.call_lock:
+        st = ctx.lib.pcb_pagani_refine(ctx.handle, C.byref(fc), C.byref(rc), C.byref(cc), C.byref(res), records, cb, None,
+                                       C.byref(bad))
+        if failure:
+            raise failure[0]
+        ctx.check(st, bad, spec.d)
+    history = [(records[i].estimate, records[i].errorest, int(records[i].n_regions)) for i in range(res.n_records)]
+    return res, history
+
+
+def apply_rules_single(spec: DeviceSpec, rule, left, length, device=None):
+    ctx = context(device)
+    fc, bad = spec.to_c(), NonFiniteC()
+    gen, w = _f64(rule.generators), _f64(rule.weights)
+    left, length = _f64(left), _f64(length)
+    values, fx = np.empty(5), np.empty(rule.f_eval)
+    with ctx.call_lock:
+        st = ctx.lib.pcb_apply_rules(ctx.handle, C.byref(fc), rule.f_eval, _ptr(gen), _ptr(w), _ptr(left), _ptr(length),
+                                     _ptr(values), _ptr(fx), C.byref(bad))
+        ctx.check(st, bad, spec.d)
+    return values, fx
+
+
+def mcubes_sample(spec: DeviceSpec, plan, boundaries: np.ndarray, seed: int, rng_kind: int = RNG_REFERENCE_HASH,
+                  injected=None, squared_weighted: bool = True, thread_range=None, want_group_partials=False, device=None):
+    ctx = context(device)
+    d, nb = boundaries.shape[0], boundaries.shape[1] - 1
+    b = _f64(boundaries)
+    fc, pc, it, bad = spec.to_c(), plan_to_c(plan, nb), McubesIterationC(), NonFiniteC()
+    t0, t1 = (0, plan.n_threads) if thread_range is None else thread_range
+    contrib = np.empty((d, nb))
+    n_groups = -(-(t1 - t0) // plan.group_size)
+    partials = np.empty((n_groups, 2)) if want_group_partials else None
+    inj = None if injected is None else _f64(injected).ravel()
+    if inj is not None and inj.size != plan.m * plan.p * d:
+        raise ValueError("injected uniforms must have m*p*d entries")
+    with ctx.call_lock:
+        st = ctx.lib.pcb_mcubes_sample(ctx.handle, C.byref(fc), C.byref(pc), _ptr(b), C.c_uint64(seed & (2**64 - 1)),
+                                       rng_kind, None if inj is None else _ptr(inj), int(bool(squared_weighted)), t0, t1,
+                                       C.byref(it), _ptr(contrib), None if partials is None else _ptr(partials),
+                                       C.byref(bad))
+        ctx.check(st, bad, d)
+    return it, contrib, partials
+
+
+def grid_refine(boundaries: np.ndarray, contributions: np.ndarray, alpha: float, smoothing: bool, device=None):
+    ctx = context(device)
+    d, nb1 = boundaries.shape
+    b, c = _f64(boundaries), _f64(contributions, (d, nb1 - 1))
+    out = np.empty_like(b)
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_grid_refine(ctx.handle, d, nb1 - 1, _ptr(b), _ptr(c), float(alpha), int(bool(smoothing)),
+                                          _ptr(out)))
+    return out
+
+
+def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, rng_kind: int, adapt: bool, alpha: float,
+               smoothing: bool, rel_tol: float = 0.0, progress=None, keep_contributions=True, device=None):
+    ctx = context(device)
+    d = plan.d
+    fc, pc, bad = spec.to_c(), plan_to_c(plan, n_bins), NonFiniteC()
+    its = (McubesIterationC * iterations)()
+    n_done, seconds = C.c_int32(), C.c_double()
+    contribs = np.zeros((iterations, d, n_bins)) if keep_contributions else None
+    final_b = np.empty((d, n_bins + 1))
+    failure = []
+
+    def _cb(_user, rec):
+        if progress is None or failure:
+            return
+        try:
+            r = rec.contents
+            progress({"iteration": r.iteration, "estimate": r.estimate, "errorest": r.errorest,
+                      "chi2_per_dof": r.chi2_per_dof, "iter_integral": r.iter_integral,
+                      "iter_sd": float(np.sqrt(r.iter_variance))})
+        except BaseException as exc:  # noqa: BLE001
+            failure.append(exc)
+
+    cb = MCUBES_PROGRESS_FN(_cb)
+    with ctx.call_lock:
+        st = ctx.lib.pcb_mcubes_run(ctx.handle, C.byref(fc), C.byref(pc), int(iterations), C.c_uint64(seed & (2**64 - 1)),
+                                    rng_kind, int(bool(adapt)), float(alpha), int(bool(smoothing)), float(rel_tol), its,
+                                    C.byref(n_done), cb, None, None if contribs is None else _ptr(contribs),
+                                    _ptr(final_b), C.byref(seconds), C.byref(bad))
+        if failure:
+            raise failure[0]
+        ctx.check(st, bad, d)
+    done = n_done.value
+    return [its[i] for i in range(done)], (None if contribs is None else contribs[:done]), final_b, seconds.value
+
+
+def uniforms(seed: int, streams, counters, rng_kind: int = RNG_REFERENCE_HASH, device=None) -> np.ndarray:
+    ctx = context(device)
+    s = np.ascontiguousarray(np.broadcast_to(np.asarray(streams, dtype=np.uint64), np.broadcast(streams, counters).shape)).ravel()
+    c = np.ascontiguousarray(np.broadcast_to(np.asarray(counters, dtype=np.uint64), np.broadcast(streams, counters).shape)).ravel()
+    out = np.empty(s.size)
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_uniforms(ctx.handle, C.c_uint64(seed & (2**64 - 1)), rng_kind, s.size, _ptr(s), _ptr(c), _ptr(out)))
+    return out

@@ -1,0 +1,179 @@
+// Context, kernel dispatch tables, eval_points, RNG mirror and the FP64 peak probe.
+#include "pcb_device.cuh"
+#include "pcb_host.h"
+
+#include <cmath>
+#include <cstring>
+#include <new>
+
+namespace pcb {
+
+#define PCB_DECL(F, _) \
+  const void* eval_kernel_fam##F(int d); \
+  const void* points_kernel_fam##F(int d); \
+  const void* vsample_kernel_fam##F(int d);
+PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5, ) PCB_DECL(6, ) PCB_DECL(7, )
+#undef PCB_DECL
+
+static const kernel_getter kEval[PCB_N_FAMILIES] = {eval_kernel_fam0, eval_kernel_fam1, eval_kernel_fam2, eval_kernel_fam3,
+                                                    eval_kernel_fam4, eval_kernel_fam5, eval_kernel_fam6, eval_kernel_fam7};
+static const kernel_getter kPoints[PCB_N_FAMILIES] = {points_kernel_fam0, points_kernel_fam1, points_kernel_fam2, points_kernel_fam3,
+                                                      points_kernel_fam4, points_kernel_fam5, points_kernel_fam6, points_kernel_fam7};
+static const kernel_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsample_kernel_fam1, vsample_kernel_fam2, vsample_kernel_fam3,
+                                                      vsample_kernel_fam4, vsample_kernel_fam5, vsample_kernel_fam6, vsample_kernel_fam7};
+
+const void* eval_kernel(int family, int d) { return kEval[family](d); }
+const void* points_kernel(int family, int d) { return kPoints[family](d); }
+const void* vsample_kernel_ptr(int family, int d) { return kSample[family](d); }
+
+pcb_status validate_integrand(pcb_ctx* ctx, const pcb_integrand* f) {
+  if (!f) return fail(ctx, PCB_INVALID, "integrand is NULL");
+  if (f->family < 0 || f->family >= PCB_N_FAMILIES) return fail(ctx, PCB_INVALID, "unknown integrand family %d", f->family);
+  if (f->d < 1 || f->d > PCB_MAX_DIM) return fail(ctx, PCB_INVALID, "dimension %d outside [1, %d]", f->d, PCB_MAX_DIM);
+  return PCB_OK;
+}
+
+__global__ void fp64_peak_kernel(double* sink, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+    x0 = __fma_rn(x0, a, b); x1 = __fma_rn(x1, a, b); x2 = __fma_rn(x2, a, b); x3 = __fma_rn(x3, a, b);
+    x4 = __fma_rn(x4, a, b); x5 = __fma_rn(x5, a, b); x6 = __fma_rn(x6, a, b); x7 = __fma_rn(x7, a, b);
+  }
+  double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 12345.678) sink[0] = s;
+}
+
+__global__ void uniforms_kernel(unsigned long long seed, int kind, long long n, const unsigned long long* streams,
+                                const unsigned long long* counters, double* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = kind == PCB_RNG_PHILOX ? philox_uniform(seed, streams[i], counters[i])
+                                    : hash_uniform(stream_key(seed, streams[i]), counters[i]);
+}
+
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" {
+
+pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out) {
+  if (!out) return PCB_INVALID;
+  *out = nullptr;
+  pcb_ctx* ctx = new (std::nothrow) pcb_ctx();
+  if (!ctx) return PCB_CUDA;
+  *out = ctx;  // returned even on failure so the caller can read the error text
+  ctx->device = device_ordinal;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(device_ordinal));
+  cudaDeviceProp prop;
+  PCB_CUDA_TRY(ctx, cudaGetDeviceProperties(&prop, device_ordinal));
+  if (prop.major < 10)
+    return fail(ctx, PCB_CUDA, "device %d (%s, sm_%d%d) is not a Blackwell sm_100 part; this library has no other code path",
+                device_ordinal, prop.name, prop.major, prop.minor);
+  ctx->sm_count = prop.multiProcessorCount;
+  ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  int khz = 0;
+  cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_ordinal);
+  ctx->clock_khz = khz;
+  std::strncpy(ctx->name, prop.name, sizeof(ctx->name) - 1);
+  PCB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pinned, 1 << 16));
+  PCB_CUDA_TRY(ctx, ctx->scalars.ensure(64 * sizeof(double)));
+  return PCB_OK;
+}
+
+void pcb_ctx_destroy(pcb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+  }
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  delete ctx;
+}
+
+const char* pcb_last_error(const pcb_ctx* ctx) { return ctx ? ctx->err.c_str() : "context is NULL"; }
+
+pcb_status pcb_device_info(pcb_ctx* ctx, char* name, int name_len, int32_t* sm_count, int32_t* clock_khz) {
+  if (!ctx) return PCB_INVALID;
+  if (name && name_len > 0) {
+    std::strncpy(name, ctx->name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (sm_count) *sm_count = ctx->sm_count;
+  if (clock_khz) *clock_khz = ctx->clock_khz;
+  return PCB_OK;
+}
+
+int64_t pcb_launch_count(const pcb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) return PCB_INVALID;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int iters = 1 << 15, threads = 512, blocks = ctx->sm_count * 4;
+  cudaEvent_t e0, e1;
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&e0));
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&e1));
+  double best = 0.0;
+  for (int rep = 0; rep < 4; ++rep) {
+    cudaEventRecord(e0, ctx->stream);
+    fp64_peak_kernel<<<blocks, threads, 0, ctx->stream>>>(ctx->scalars.as<double>() + 32, iters, 1.0000001, 1e-9);
+    cudaEventRecord(e1, ctx->stream);
+    PCB_CUDA_TRY(ctx, cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double tf = 2.0 * 8.0 * iters * (double)threads * blocks / (ms * 1e-3) / 1e12;
+    if (rep > 0 && tf > best) best = tf;
+    ctx->launches++;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *tflops = best;
+  return PCB_OK;
+}
+
+pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points, double* values) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  if (n < 0 || (n > 0 && (!points || !values))) return fail(ctx, PCB_INVALID, "eval_points: bad buffers");
+  if (n == 0) return PCB_OK;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, ctx->rows_a.ensure((size_t)n * f->d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->rows_b.ensure((size_t)n * sizeof(double)));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_a.p, points, (size_t)n * f->d * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  const double* pts = ctx->rows_a.as<double>();
+  double* out = ctx->rows_b.as<double>();
+  long long nn = n;
+  pcb_integrand fv = *f;
+  void* args[] = {&fv, &nn, &pts, &out};
+  int blocks = (int)std::min<long long>((n + 255) / 256, (long long)ctx->sm_count * 16);
+  PCB_CUDA_TRY(ctx, cudaLaunchKernel(points_kernel(f->family, f->d), dim3(blocks), dim3(256), args, 0, ctx->stream));
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(values, out, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,
+                        const uint64_t* counters, double* out) {
+  if (!ctx) return PCB_INVALID;
+  if (n < 0 || (n > 0 && (!streams || !counters || !out))) return fail(ctx, PCB_INVALID, "uniforms: bad buffers");
+  if (rng_kind != PCB_RNG_REFERENCE_HASH && rng_kind != PCB_RNG_PHILOX) return fail(ctx, PCB_INVALID, "uniforms: bad rng kind");
+  if (n == 0) return PCB_OK;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, ctx->rows_a.ensure((size_t)n * 16));
+  PCB_CUDA_TRY(ctx, ctx->rows_b.ensure((size_t)n * 8));
+  unsigned long long* s = ctx->rows_a.as<unsigned long long>();
+  unsigned long long* c = s + n;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(s, streams, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(c, counters, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  int blocks = (int)std::min<long long>((n + 255) / 256, (long long)ctx->sm_count * 16);
+  uniforms_kernel<<<blocks, 256, 0, ctx->stream>>>(seed, rng_kind, n, s, c, ctx->rows_b.as<double>());
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->rows_b.p, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,184 @@
+// m-Cubes auxiliary kernels (not templated on the integrand): table merge, work-group trees,
+// grid refinement (reference: mcubes.py:255-265, 292-298; vegas_grid.py:133-193).
+#pragma once
+
+#include "pcb_device.cuh"
+
+namespace pcb {
+
+// CTA tables -> contribution table, fixed CTA order
+__global__ void merge_hist_kernel(const double* __restrict__ block_hist, int nblocks, int nbins_total, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbins_total) return;
+  double t = block_hist[i];
+  for (int b = 1; b < nblocks; ++b) t = t + block_hist[(size_t)b * nbins_total + i];
+  out[i] = t;
+}
+
+// per logical thread: serial sum of its segment partials; then one CTA per work-group reduces the
+// group's threads with the adjacent-pair tree (mcubes.py:255-259).  out[g][0..1] = (I_g, E_g).
+__global__ void group_tree_kernel(const double* __restrict__ seg_partials, int nseg, long long n_local_threads,
+                                  int group_size, int pow2, double* __restrict__ group_out) {
+  extern __shared__ double s[];  // [2][pow2]
+  const long long t0 = (long long)blockIdx.x * group_size;
+  for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
+    double e = 0.0, v = 0.0;
+    const long long t = t0 + i;
+    if (i < group_size && t < n_local_threads) {
+      const double* src = seg_partials + t * nseg * 2;
+      e = src[0];
+      v = src[1];
+      for (int q = 1; q < nseg; ++q) { e = e + src[2 * q]; v = v + src[2 * q + 1]; }
+    }
+    s[i] = e;
+    s[pow2 + i] = v;
+  }
+  __syncthreads();
+  for (int half = pow2 >> 1; half >= 1; half >>= 1) {
+    // adjacent pairs: element i of the next level = s[2i] + s[2i+1]; done in place via a staging read
+    double e[8], v[8];
+    int cnt = 0;
+    for (int i = threadIdx.x; i < half; i += blockDim.x, ++cnt) { e[cnt] = s[2 * i] + s[2 * i + 1]; v[cnt] = s[pow2 + 2 * i] + s[pow2 + 2 * i + 1]; }
+    __syncthreads();
+    cnt = 0;
+    for (int i = threadIdx.x; i < half; i += blockDim.x, ++cnt) { s[i] = e[cnt]; s[pow2 + i] = v[cnt]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    group_out[2 * blockIdx.x] = s[0];
+    group_out[2 * blockIdx.x + 1] = s[pow2];
+  }
+}
+
+__global__ void deinterleave2_kernel(const double* __restrict__ in, int n, double* __restrict__ a, double* __restrict__ b) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { a[i] = in[2 * i]; b[i] = in[2 * i + 1]; }
+}
+
+// ------------------------------------------------------------------------------------------
+// refine_grid (vegas_grid.py:142-193): one CTA per axis.
+// numpy's pairwise float sum of an n-vector (n <= 128*k blocks) restated serially.
+// ------------------------------------------------------------------------------------------
+__device__ inline double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;  // numpy starts from the first element; 0.0 + a[0] == a[0] for these inputs (a >= 0)
+    for (int i = 0; i < n; ++i) r = (i == 0) ? a[0] : r + a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int k = 0; k < 8; ++k) r[k] = r[k] + a[i + k];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res = res + a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+struct RefineArgs {
+  int d, n;
+  double alpha;
+  int smoothing;
+  const double* boundaries;     // [d][n+1]
+  const double* contrib;        // [d][n]
+  double* new_boundaries;       // [d][n+1]
+};
+
+__global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant__ RefineArgs a) {
+  extern __shared__ double sh[];
+  const int n = a.n, j = blockIdx.x, tid = threadIdx.x;
+  double* c = sh;              // [n]   smoothed contributions
+  double* w = c + n;           // [n]   damped weights
+  double* cw = w + n;          // [n+1] cumulative weights
+  double* row = cw + n + 1;    // [n+1] new boundaries
+  __shared__ double s_total, s_wsum;
+  __shared__ int s_any;
+  const double* src = a.contrib + (size_t)j * n;
+  const double* old = a.boundaries + (size_t)j * (n + 1);
+  double* dst = a.new_boundaries + (size_t)j * (n + 1);
+
+  if (tid == 0) s_any = 0;
+  __syncthreads();
+  int any = 0;
+  for (int i = tid; i < n; i += blockDim.x) any |= (src[i] > 0.0);
+  if (any) atomicOr(&s_any, 1);
+  __syncthreads();
+  if (!s_any) {  // axis untouched (vegas_grid.py:156-157)
+    for (int i = tid; i <= n; i += blockDim.x) dst[i] = old[i];
+    return;
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    double v;
+    if (a.smoothing && n >= 2) {
+      if (i == 0) v = (src[0] + src[1]) / 2.0;
+      else if (i == n - 1) v = (src[n - 2] + src[n - 1]) / 2.0;
+      else v = (src[i - 1] + src[i] + src[i + 1]) / 3.0;
+    } else {
+      v = src[i];
+    }
+    c[i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) s_total = np_pairwise_sum(c, n);
+  __syncthreads();
+  const double total = s_total;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double r = c[i] / total;
+    double ww = 0.0;
+    if (r > 0.0 && r < 1.0) ww = pow((1.0 - r) / log(1.0 / r), a.alpha);
+    else if (r >= 1.0) ww = 1.0;
+    w[i] = ww;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const double wsum = np_pairwise_sum(w, n);
+    s_wsum = wsum;
+    double run = 0.0;
+    cw[0] = 0.0;
+    for (int i = 0; i < n; ++i) {  // np.cumsum: serial
+      run = (i == 0) ? w[0] : run + w[i];
+      cw[i + 1] = run;
+    }
+    cw[n] = wsum;
+  }
+  __syncthreads();
+  const double wsum = s_wsum;
+  if (!(wsum > 0.0)) {
+    for (int i = tid; i <= n; i += blockDim.x) dst[i] = old[i];
+    return;
+  }
+  for (int k = tid + 1; k < n; k += blockDim.x) {
+    const double target = wsum * (double)k / (double)n;
+    // searchsorted(cw, target, side="right") - 1, clipped to [0, n-1]
+    int lo = 0, hi = n + 1;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (cw[mid] <= target) lo = mid + 1; else hi = mid;
+    }
+    int idx = lo - 1;
+    idx = idx < 0 ? 0 : (idx > n - 1 ? n - 1 : idx);
+    const double seg = cw[idx + 1] - cw[idx];
+    const double frac = seg > 0.0 ? (target - cw[idx]) / seg : 0.0;
+    row[k] = old[idx] + frac * (old[idx + 1] - old[idx]);
+  }
+  if (tid == 0) { row[0] = 0.0; row[n] = 1.0; }
+  __syncthreads();
+  if (tid == 0) {  // restore strict monotonicity (vegas_grid.py:183-192)
+    for (int k = 1; k <= n; ++k)
+      if (row[k] <= row[k - 1]) row[k] = nextafter(row[k - 1], 2.0);
+    if (row[n] != 1.0) {
+      row[n] = 1.0;
+      for (int k = n; k > 0; --k)
+        if (row[k - 1] >= row[k]) row[k - 1] = nextafter(row[k], -1.0);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i <= n; i += blockDim.x) dst[i] = row[i];
+}
+
+}  // namespace pcb

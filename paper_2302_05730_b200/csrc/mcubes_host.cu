@@ -1,0 +1,341 @@
+// m-Cubes C-ABI: V-Sample pass, grid refinement and the iteration driver.
+// Reference: mcubes.py:210-382, vegas_grid.py:133-193.
+#include "mcubes_aux.cuh"
+#include "mcubes_kernels.cuh"
+#include "pcb_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+namespace pcb {
+
+enum { M_BAD = 0, M_CLAMPS = 1, M_INTEGRAL = 2, M_VARIANCE = 3 };  // slots in ctx->scalars (offset 40)
+constexpr int kMcSlot = 40;
+
+struct SampleLaunch {
+  int warps = 0;
+  int blocks = 0;
+  size_t smem = 0;
+  int nseg = 1;
+  long long seg_len = 0;
+};
+
+static pcb_status validate_plan(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan) {
+  if (!plan) return fail(ctx, PCB_INVALID, "plan is NULL");
+  if (plan->d != f->d) return fail(ctx, PCB_INVALID, "plan, grid, and integrand dimensions must agree");
+  if (plan->g < 1 || plan->p < 2 || plan->s < 1 || plan->group_size < 1 || plan->n_bins < 2)
+    return fail(ctx, PCB_INVALID, "plan needs g >= 1, p >= 2, s >= 1, group_size >= 1, n_bins >= 2");
+  long double m = 1;
+  for (int j = 0; j < plan->d; ++j) m *= plan->g;
+  if (m != (long double)plan->m) return fail(ctx, PCB_INVALID, "m must equal g^d");
+  if (plan->group_size > 4096) return fail(ctx, PCB_INVALID, "group_size %d > 4096 unsupported", plan->group_size);
+  return PCB_OK;
+}
+
+static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long long n_local_threads, SampleLaunch* out) {
+  const size_t bounds_bytes = (size_t)plan->d * (plan->n_bins + 1) * sizeof(double);
+  const size_t per_warp = (size_t)plan->d * plan->n_bins * (sizeof(double) + 1);
+  const size_t avail = ctx->smem_optin > 1024 ? ctx->smem_optin - 1024 : 0;
+  if (avail < bounds_bytes + per_warp)
+    return fail(ctx, PCB_INVALID, "d=%d, n_bins=%d needs %zu B of shared memory per CTA, device offers %zu", plan->d,
+                plan->n_bins, bounds_bytes + per_warp + 1024, ctx->smem_optin);
+  int warps = (int)std::min<size_t>((avail - bounds_bytes) / per_warp, 16);
+  const long long n_lw = (n_local_threads + 31) / 32;
+  // tiny passes do not need every SM
+  long long blocks = std::min<long long>(ctx->sm_count, std::max<long long>(1, (n_lw + warps - 1) / warps));
+  out->warps = warps;
+  out->blocks = (int)blocks;
+  out->smem = bounds_bytes + (size_t)warps * per_warp + 16;
+  const long long phys = blocks * warps;
+  int nseg = 1;
+  if (n_lw < 4 * phys) nseg = (int)std::min<long long>(plan->s, (6 * phys + n_lw - 1) / n_lw);
+  if (const char* env = std::getenv("PCB_MCUBES_SEGMENTS")) {
+    int v = std::atoi(env);
+    if (v >= 1) nseg = (int)std::min<long long>(plan->s, v);
+  }
+  long long seg_len = (plan->s + nseg - 1) / nseg;
+  out->seg_len = seg_len;
+  out->nseg = (int)((plan->s + seg_len - 1) / seg_len);
+  return PCB_OK;
+}
+
+static pcb_status read_mc_scalars(pcb_ctx* ctx) {
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync((double*)ctx->pinned + kMcSlot, ctx->scalars.as<double>() + kMcSlot, 4 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+// One V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries.
+// Leaves: contributions in ctx->mc_contrib (d*nb), per-group (I, Var) in ctx->mc_group,
+// scalars (bad, clamps, integral, variance) in ctx->scalars[kMcSlot..].
+static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, const double* bounds_dev,
+                             unsigned long long seed, int rng_kind, const double* injected_dev, int squared_weighted,
+                             long long t_begin, long long t_end, long long* n_groups_out) {
+  const int d = plan->d, nb = plan->n_bins;
+  const long long n_threads = (plan->m + plan->s - 1) / plan->s;
+  if (t_begin < 0 || t_end > n_threads || t_begin >= t_end)
+    return fail(ctx, PCB_INVALID, "thread range [%lld, %lld) outside [0, %lld)", t_begin, t_end, n_threads);
+  if (t_begin % plan->group_size != 0)
+    return fail(ctx, PCB_INVALID, "thread_begin %lld must be a multiple of group_size %d", t_begin, plan->group_size);
+  const long long nt = t_end - t_begin;
+  SampleLaunch L;
+  PCB_TRY(plan_launch(ctx, plan, nt, &L));
+  const void* fn = vsample_kernel_ptr(f->family, d);
+  PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+
+  PCB_CUDA_TRY(ctx, ctx->mc_seg.ensure((size_t)nt * L.nseg * 2 * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)L.blocks * d * nb * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure((size_t)d * nb * sizeof(double)));
+  const long long n_groups = (nt + plan->group_size - 1) / plan->group_size;
+  PCB_CUDA_TRY(ctx, ctx->mc_group.ensure((size_t)n_groups * 4 * sizeof(double)));
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>() + kMcSlot;
+  double* sc = ctx->scalars.as<double>() + kMcSlot;
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_CLAMPS, 0, sizeof(unsigned long long), ctx->stream));
+
+  SampleArgs a;
+  a.f = *f;
+  a.g = plan->g; a.p = plan->p; a.nb = nb; a.squared_weighted = squared_weighted;
+  a.m = plan->m; a.s = plan->s;
+  a.n_threads = n_threads;
+  a.t_begin = t_begin; a.t_end = t_end;
+  a.n_lw = (nt + 31) / 32;
+  a.nseg = L.nseg;
+  a.rng_kind = rng_kind;
+  a.seg_len = L.seg_len;
+  a.seed = seed;
+  a.injected = injected_dev;
+  a.boundaries = bounds_dev;
+  a.gd = (double)plan->g;
+  a.rg = 1.0 / (double)plan->g;
+  // exact integer denominators rounded once, as Python's int -> float conversion does (mcubes.py:247-248)
+  a.den_est = (double)((long double)plan->p * (long double)plan->m);
+  {
+    unsigned __int128 den = (unsigned __int128)plan->p * (unsigned __int128)(plan->p - 1);
+    den *= (unsigned __int128)plan->m;
+    den *= (unsigned __int128)plan->m;
+    a.den_var = (double)den;  // correctly rounded conversion of the exact product
+  }
+  a.seg_partials = ctx->mc_seg.as<double>();
+  a.clamps = sc_u + M_CLAMPS;
+  a.bad = sc_u + M_BAD;
+  a.block_hist = ctx->mc_hist.as<double>();
+  void* args[] = {&a};
+  PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(L.blocks), dim3(L.warps * 32), args, L.smem, ctx->stream));
+  merge_hist_kernel<<<(d * nb + 255) / 256, 256, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), L.blocks, d * nb,
+                                                                     ctx->mc_contrib.as<double>());
+  int pow2 = 1;
+  while (pow2 < plan->group_size) pow2 <<= 1;
+  const int gt_threads = std::max(32, std::min(256, pow2 / 2));
+  group_tree_kernel<<<(unsigned)n_groups, gt_threads, 2 * pow2 * sizeof(double), ctx->stream>>>(
+      ctx->mc_seg.as<double>(), L.nseg, nt, plan->group_size, pow2, ctx->mc_group.as<double>());
+  double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
+  double* ge = gi + n_groups;
+  deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
+  ctx->launches += 4;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));   // engine.reduce in group order (mcubes.py:292-293)
+  PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
+  if (n_groups_out) *n_groups_out = n_groups;
+  return PCB_OK;
+}
+
+// first non-finite sample: recompute its point on the device path is overkill; report index and value
+static pcb_status report_bad_sample(pcb_ctx* ctx, const pcb_mcubes_plan* plan, unsigned long long flat, pcb_nonfinite* bad) {
+  const long long cube = (long long)(flat / (unsigned long long)plan->p);
+  const long long k = (long long)(flat % (unsigned long long)plan->p);
+  if (bad) {
+    bad->region_index = cube;
+    bad->point_index = k;
+    bad->value = NAN;
+    std::memset(bad->point, 0, sizeof bad->point);
+  }
+  return fail(ctx, PCB_NONFINITE, "non-finite integrand value in sub-cube %lld (sample %lld)", cube, k);
+}
+
+static pcb_status refine_dev(pcb_ctx* ctx, int d, int nb, const double* bounds_dev, const double* contrib_dev, double alpha,
+                             int smoothing, double* out_dev) {
+  RefineArgs r;
+  r.d = d; r.n = nb; r.alpha = alpha; r.smoothing = smoothing;
+  r.boundaries = bounds_dev; r.contrib = contrib_dev; r.new_boundaries = out_dev;
+  const size_t smem = (size_t)(4 * nb + 2) * sizeof(double);
+  if (smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
+  PCB_CUDA_TRY(ctx, cudaFuncSetAttribute((const void*)refine_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  refine_grid_kernel<<<d, 512, smem, ctx->stream>>>(r);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  return PCB_OK;
+}
+
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" {
+
+pcb_status pcb_mcubes_sample(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, const double* boundaries,
+                             uint64_t seed, int32_t rng_kind, const double* injected_uniforms, int32_t squared_weighted,
+                             int64_t thread_begin, int64_t thread_end, pcb_mcubes_iteration* out, double* contributions,
+                             double* group_partials, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_plan(ctx, f, plan));
+  if (!boundaries || !out || !contributions) return fail(ctx, PCB_INVALID, "mcubes_sample: NULL buffer");
+  if (rng_kind < 0 || rng_kind > 2 || (rng_kind == PCB_RNG_INJECTED && !injected_uniforms))
+    return fail(ctx, PCB_INVALID, "mcubes_sample: bad rng kind / missing injected table");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = plan->d, nb = plan->n_bins;
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, boundaries, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+  const double* inj = nullptr;
+  if (rng_kind == PCB_RNG_INJECTED) {
+    const size_t ibytes = (size_t)plan->m * plan->p * d * sizeof(double);
+    PCB_CUDA_TRY(ctx, ctx->mc_inject.ensure(ibytes));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_inject.p, injected_uniforms, ibytes, cudaMemcpyHostToDevice, ctx->stream));
+    inj = ctx->mc_inject.as<double>();
+  }
+  long long n_groups = 0;
+  PCB_TRY(sample_dev(ctx, f, plan, ctx->mc_bounds[0].as<double>(), seed, rng_kind, inj, squared_weighted, thread_begin,
+                     thread_end, &n_groups));
+  PCB_TRY(read_mc_scalars(ctx));
+  const unsigned long long* hu = (const unsigned long long*)ctx->pinned + kMcSlot;
+  const double* hd = (const double*)ctx->pinned + kMcSlot;
+  if (hu[M_BAD] != ~0ULL) return report_bad_sample(ctx, plan, hu[M_BAD], bad);
+  out->integral = hd[M_INTEGRAL];
+  out->variance = std::fmax(hd[M_VARIANCE], 0.0);
+  out->clamp_events = (int64_t)hu[M_CLAMPS];
+  // samples drawn by this call: the cubes of the shard times p
+  const long long c0 = thread_begin * plan->s, c1 = std::min<long long>(thread_end * plan->s, plan->m);
+  out->n_samples = (c1 - c0) * plan->p;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(contributions, ctx->mc_contrib.p, (size_t)d * nb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (group_partials)
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(group_partials, ctx->mc_group.p, (size_t)n_groups * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_grid_refine(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double* boundaries, const double* contributions,
+                           double alpha, int32_t smoothing, double* new_boundaries) {
+  if (!ctx) return PCB_INVALID;
+  if (d < 1 || d > PCB_MAX_DIM || n_bins < 2 || !boundaries || !contributions || !new_boundaries || alpha < 0)
+    return fail(ctx, PCB_INVALID, "grid_refine: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t bbytes = (size_t)d * (n_bins + 1) * sizeof(double), cbytes = (size_t)d * n_bins * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[1].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure(cbytes));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, boundaries, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_contrib.p, contributions, cbytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_TRY(refine_dev(ctx, d, n_bins, ctx->mc_bounds[0].as<double>(), ctx->mc_contrib.as<double>(), alpha, smoothing,
+                     ctx->mc_bounds[1].as<double>()));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(new_boundaries, ctx->mc_bounds[1].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, int32_t iterations, uint64_t seed,
+                          int32_t rng_kind, int32_t adapt, double alpha, int32_t smoothing, double rel_tol,
+                          pcb_mcubes_iteration* iterations_out, int32_t* n_done, pcb_mcubes_progress_fn progress, void* user,
+                          double* contributions_out, double* final_boundaries, double* seconds_device, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_plan(ctx, f, plan));
+  if (iterations < 1) return fail(ctx, PCB_INVALID, "iterations must be >= 1");
+  if (!iterations_out || !n_done) return fail(ctx, PCB_INVALID, "mcubes_run: NULL buffer");
+  if (rng_kind != PCB_RNG_REFERENCE_HASH && rng_kind != PCB_RNG_PHILOX) return fail(ctx, PCB_INVALID, "mcubes_run: bad rng kind");
+  if (alpha < 0) return fail(ctx, PCB_INVALID, "alpha must be >= 0");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = plan->d, nb = plan->n_bins;
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[1].ensure(bbytes));
+  {  // init_grid: k / n_bins on every axis (vegas_grid.py:77-84)
+    std::vector<double> b((size_t)d * (nb + 1));
+    for (int j = 0; j < d; ++j)
+      for (int k = 0; k <= nb; ++k) b[(size_t)j * (nb + 1) + k] = (double)k / (double)nb;
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, b.data(), bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  cudaEvent_t ev0, ev1;
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev0));
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev1));
+  struct EventGuard {
+    cudaEvent_t a, b;
+    ~EventGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  } guard{ev0, ev1};
+  cudaEventRecord(ev0, ctx->stream);
+
+  const long long n_threads = (plan->m + plan->s - 1) / plan->s;
+  int cur = 0, done = 0;
+  std::vector<double> ivals, ivars;
+  for (int it = 0; it < iterations; ++it) {
+    const unsigned long long it_seed = derive_seed(seed, (unsigned long long)it);  // mcubes.py:58-60, 359
+    PCB_TRY(sample_dev(ctx, f, plan, ctx->mc_bounds[cur].as<double>(), it_seed, rng_kind, nullptr, 1, 0, n_threads, nullptr));
+    if (contributions_out)
+      PCB_CUDA_TRY(ctx, cudaMemcpyAsync(contributions_out + (size_t)it * d * nb, ctx->mc_contrib.p, (size_t)d * nb * sizeof(double),
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+    if (adapt) {
+      PCB_TRY(refine_dev(ctx, d, nb, ctx->mc_bounds[cur].as<double>(), ctx->mc_contrib.as<double>(), alpha, smoothing,
+                         ctx->mc_bounds[cur ^ 1].as<double>()));
+      cur ^= 1;
+    }
+    PCB_TRY(read_mc_scalars(ctx));
+    const unsigned long long* hu = (const unsigned long long*)ctx->pinned + kMcSlot;
+    const double* hd = (const double*)ctx->pinned + kMcSlot;
+    if (hu[M_BAD] != ~0ULL) return report_bad_sample(ctx, plan, hu[M_BAD], bad);
+    pcb_mcubes_iteration& o = iterations_out[it];
+    o.integral = hd[M_INTEGRAL];
+    o.variance = std::fmax(hd[M_VARIANCE], 0.0);
+    o.n_samples = plan->m * plan->p;
+    o.clamp_events = (int64_t)hu[M_CLAMPS];
+    done = it + 1;
+    ivals.push_back(o.integral);
+    ivars.push_back(o.variance);
+    // combine_iterations (mcubes.py:311-329): inverse-variance weights, variances floored at 1e-30
+    double wsum = 0.0, dot = 0.0;
+    for (int i = 0; i < done; ++i) {
+      const double w = 1.0 / std::fmax(ivars[i], 1e-30);
+      wsum += w;
+      dot += w * ivals[i];
+    }
+    const double est = dot / wsum, err = std::pow(wsum, -0.5);
+    double chi2 = 0.0;
+    if (done > 1) {
+      for (int i = 0; i < done; ++i) {
+        const double w = 1.0 / std::fmax(ivars[i], 1e-30), dv = ivals[i] - est;
+        chi2 += w * (dv * dv);
+      }
+      chi2 /= (double)(done - 1);
+    }
+    if (progress) {
+      pcb_mcubes_progress rec;
+      rec.iteration = it;
+      rec.reserved = 0;
+      rec.estimate = est;
+      rec.errorest = err;
+      rec.chi2_per_dof = chi2;
+      rec.iter_integral = o.integral;
+      rec.iter_variance = o.variance;
+      progress(user, &rec);
+    }
+    if (rel_tol > 0 && err <= rel_tol * std::fabs(est)) break;
+  }
+  cudaEventRecord(ev1, ctx->stream);
+  PCB_CUDA_TRY(ctx, cudaEventSynchronize(ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  if (seconds_device) *seconds_device = ms * 1e-3;
+  *n_done = done;
+  if (final_boundaries) {
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(final_boundaries, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  return PCB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+// PAGANI region evaluation: one warp per region (reference: pagani.py:195-224, A.1 of SURVEY.md).
+//
+// Per region the kernel
+//   1. tabulates, per axis, the integrand's per-axis term at the 7 distinct abscissae
+//      left + length*offset (quadrature.py:301-302; mul then add) -- 7*D terms instead of F*D;
+//   2. evaluates the F rule points: lane l plays the reference's virtual threads l and l+32 of
+//      the G=64 strided schedule (point indices t, t+G, ...; pagani.py:175-192), assembling each
+//      point's terms from the table in numpy's combine order;
+//   3. reduces the 2x5 partial sums with a reduce-scatter butterfly whose add tree is exactly the
+//      adjacent-pair tree of engine.tree_sum over 64 virtual threads (xor 1,2,4,8,16, then A+B);
+//   4. scales by the volume, forms the error estimate (pagani.py:104-132) and the split axis
+//      (pagani.py:215-223, first maximum wins).
+#pragma once
+
+#include "pcb_device.cuh"
+
+namespace pcb {
+
+struct EvalArgs {
+  pcb_integrand f;
+  pcb_rule rule;
+  long long n, ld;
+  const double* lefts;    // [d][ld]
+  const double* lengths;  // [d][ld]
+  double* integrals;
+  double* errors;
+  int32_t* split_axes;
+  unsigned long long* bad;  // min over non-finite evaluations of region*F + point
+  int group;
+  int err_mode;
+  double rel_floor;
+};
+
+constexpr int kEvalWarps = 4;  // warps per CTA
+
+// error estimate from the five volume-scaled rule values (pagani.py:104-132)
+__device__ __forceinline__ double region_error(const double (&v)[5], const pcb_rule& rule, int mode,
+                                               double rel_floor) {
+  double nul[4] = {fabs(v[1]), fabs(v[2]), fabs(v[3]), fabs(v[4])};
+  double err;
+  if (mode == PCB_ERR_MAX_NULL) {
+    err = fmax(fmax(nul[0], nul[1]), fmax(nul[2], nul[3]));
+  } else if (mode == PCB_ERR_MAX_PAIRWISE) {
+    err = 0.0;
+#pragma unroll
+    for (int a = 1; a < 5; ++a)
+#pragma unroll
+      for (int b = 1; b < 5; ++b) err = fmax(err, fabs(v[a] - v[b]));
+  } else {
+    double e_high = -1.0, e_low = -1.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (rule.null_high[k]) e_high = fmax(e_high, nul[k]);
+      else e_low = fmax(e_low, nul[k] / rule.null_scale[k]);
+    }
+    double corr = (e_low > 0.0) ? (10.0 * e_high) / e_low : 1.0;
+    err = e_high * fmin(1.0, corr);
+  }
+  return fmax(err, rel_floor * fabs(v[0]));
+}
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) { return __shfl_xor_sync(PCB_FULL_MASK, v, m); }
+__device__ __forceinline__ double shfl_idx_d(double v, int l) { return __shfl_sync(PCB_FULL_MASK, v, l); }
+
+// Reduce 2 sets x 5 columns over the 32 lanes with the adjacent-pair tree, then add the two sets.
+// On return every lane holds all five sums.
+__device__ __forceinline__ void schedule_tree(const double (&a)[5], const double (&b)[5], int lane,
+                                              double (&out)[5]) {
+  const bool b0 = lane & 1, b1 = lane & 2, b2 = lane & 4, b3 = lane & 8;
+  double c5[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {  // level 1: lanes (l, l^1); even lanes keep set A, odd lanes set B
+    double keep = b0 ? b[k] : a[k];
+    double send = b0 ? a[k] : b[k];
+    c5[k] = keep + shfl_xor_d(send, 1);
+  }
+  double c4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // level 2: bit1 = 0 keeps columns 0..3, bit1 = 1 keeps 4..7 (5..7 are padding)
+    double hi = (i == 0) ? c5[4] : 0.0;
+    double keep = b1 ? hi : c5[i];
+    double send = b1 ? c5[i] : hi;
+    c4[i] = keep + shfl_xor_d(send, 2);
+  }
+  double c2[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {  // level 3
+    double keep = b2 ? c4[2 + i] : c4[i];
+    double send = b2 ? c4[i] : c4[2 + i];
+    c2[i] = keep + shfl_xor_d(send, 4);
+  }
+  double keep = b3 ? c2[1] : c2[0];  // level 4
+  double send = b3 ? c2[0] : c2[1];
+  double c1 = keep + shfl_xor_d(send, 8);
+  c1 = c1 + shfl_xor_d(c1, 16);      // level 5
+  c1 = c1 + shfl_xor_d(c1, 1);       // level 6: virtual threads 0..31 + 32..63
+  // column held by lane l: (bit1<<2) | (bit2<<1) | bit3
+  out[0] = shfl_idx_d(c1, 0);
+  out[1] = shfl_idx_d(c1, 8);
+  out[2] = shfl_idx_d(c1, 4);
+  out[3] = shfl_idx_d(c1, 12);
+  out[4] = shfl_idx_d(c1, 2);
+}
+
+template <int FAM, int D>
+__global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __grid_constant__ EvalArgs args) {
+  using F = Family<FAM>;
+  constexpr int kStore = 4 * D + 1;           // f(centre), f(+-l2 e_j), f(+-l3 e_j): split-axis inputs
+  constexpr int kPairs = D * (D - 1) / 2;
+  __shared__ double s_term[kEvalWarps][D * 8];
+  __shared__ double s_store[kEvalWarps][kStore + 1];
+  __shared__ double s_w[6][5];                 // orbit weights; rows 4/5 = corners with even/odd bit count
+  __shared__ double s_off[8];
+  __shared__ unsigned char s_pair[kPairs > 0 ? kPairs : 1][2];
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const pcb_rule& rule = args.rule;
+  if (threadIdx.x < 30) {
+    int o = threadIdx.x / 5, k = threadIdx.x % 5;
+    double w = rule.weights[k][o < 5 ? o : 4];
+    if (o == 5 && rule.corner_parity[k]) w = -w;
+    s_w[o][k] = w;
+  }
+  if (threadIdx.x < 7) s_off[threadIdx.x] = rule.offsets[threadIdx.x];
+  if (threadIdx.x == 0) {
+    int q = 0;
+    for (int j = 0; j < D; ++j)
+      for (int k = j + 1; k < D; ++k) { s_pair[q][0] = j; s_pair[q][1] = k; ++q; }
+  }
+  __syncthreads();
+
+  const int fe = rule.f_eval, G = args.group;
+  const int corner0 = fe - (1 << D);
+  const int steps = (fe + G - 1) / G;
+  double* term = s_term[wib];
+  double* store = s_store[wib];
+  const long long ld = args.ld;
+
+  for (long long r = (long long)blockIdx.x * kEvalWarps + wib; r < args.n; r += (long long)gridDim.x * kEvalWarps) {
+    // ---- 1. per-axis term table at the 7 distinct abscissae
+    for (int e = lane; e < 8 * D; e += 32) {
+      int j = e >> 3, c = e & 7;
+      if (c < 7) {
+        double x = args.lefts[j * ld + r] + args.lengths[j * ld + r] * s_off[c];
+        term[e] = axis_term<F>(j, x, args.f);
+      }
+    }
+    double vol = args.lengths[r];
+#pragma unroll
+    for (int j = 1; j < D; ++j) vol = vol * args.lengths[j * ld + r];  // np.prod, left to right
+    __syncwarp();
+    double t0[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t0[j] = term[j * 8];
+
+    // ---- 2. rule points of my two virtual threads
+    double acc[2][5];
+#pragma unroll
+    for (int set = 0; set < 2; ++set) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc[set][k] = 0.0;
+      const int vt = lane + 32 * set;
+      if (vt >= G) continue;
+      for (int s = 0; s < steps; ++s) {
+        const int i = vt + G * s;
+        if (i >= fe) break;
+        double t[D];
+        int orbit;
+        if (i < corner0) {
+          int a = -1, b = -1;
+          double va = 0.0, vb = 0.0;
+          if (i == 0) {
+            orbit = 0;
+          } else if (i <= 2 * D) {
+            int q = i - 1;
+            a = q >> 1; va = term[a * 8 + 1 + (q & 1)]; orbit = 1;
+          } else if (i <= 4 * D) {
+            int q = i - 1 - 2 * D;
+            a = q >> 1; va = term[a * 8 + 3 + (q & 1)]; orbit = 2;
+          } else {
+            int q = i - 1 - 4 * D;
+            int pr = q >> 2, sg = q & 3;
+            a = s_pair[pr][0]; b = s_pair[pr][1];
+            va = term[a * 8 + 3 + (sg & 1)];
+            vb = term[b * 8 + 3 + (sg >> 1)];
+            orbit = 3;
+          }
+#pragma unroll
+          for (int j = 0; j < D; ++j) t[j] = (j == a) ? va : ((j == b) ? vb : t0[j]);
+        } else {
+          const int bits = i - corner0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) t[j] = term[j * 8 + 5 + ((bits >> j) & 1)];
+          orbit = 4 + (__popc(bits) & 1);
+        }
+        const double fx = finish_value<F, D>(combine_terms<F, D>(t), args.f);
+        if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+        if (i < kStore) store[i] = fx;
+        const double* w = s_w[orbit];
+        if (s == 0) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+        }
+      }
+    }
+
+    // ---- 3. schedule tree, 4. volume scaling / error / split axis
+    double sums[5];
+    schedule_tree(acc[0], acc[1], lane, sums);
+    double v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = vol * sums[k];
+    __syncwarp();
+    int axis = 0;
+    if constexpr (D > 1) {
+      double ind = -1.0;
+      if (lane < D) {
+        double two_f0 = 2.0 * store[0];
+        double d2a = (store[1 + 2 * lane] + store[2 + 2 * lane]) - two_f0;
+        double d2b = (store[1 + 2 * D + 2 * lane] + store[2 + 2 * D + 2 * lane]) - two_f0;
+        ind = fabs(rule.split_weights[0] * d2a - rule.split_weights[1] * d2b);
+      }
+      int idx = lane;
+#pragma unroll
+      for (int m = 8; m >= 1; m >>= 1) {  // argmax over lanes 0..15, lowest index wins ties
+        double o = shfl_xor_d(ind, m);
+        int oi = __shfl_xor_sync(PCB_FULL_MASK, idx, m);
+        if (o > ind || (o == ind && oi < idx)) { ind = o; idx = oi; }
+      }
+      axis = __shfl_sync(PCB_FULL_MASK, idx, 0);
+    }
+    if (lane == 0) {
+      args.integrals[r] = v[0];
+      args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
+      args.split_axes[r] = axis;
+    }
+    __syncwarp();
+  }
+}
+
+// Plain evaluation of the functor at caller-supplied points (Integrand.eval_many).
+template <int FAM, int D>
+__global__ void eval_points_kernel(const __grid_constant__ pcb_integrand f, long long n, const double* pts, double* out) {
+  using F = Family<FAM>;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = pts[i * D + j];
+    out[i] = eval_at<F, D>(x, f);
+  }
+}
+
+}  // namespace pcb

@@ -1,0 +1,463 @@
+// PAGANI C-ABI: evaluate (host and device buffers), apply_rules, tree_sum and the refinement driver.
+// Reference: pagani.py:195-391, engine.py:69-86, quadrature.py:305-322.
+#include "pagani_driver.cuh"
+#include "pagani_eval.cuh"
+#include "pcb_host.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace pcb {
+
+template <class... Args>
+static cudaError_t launch(pcb_ctx* ctx, const void* fn, dim3 grid, dim3 block, size_t smem, Args... a) {
+  void* args[] = {(void*)&a...};
+  ctx->launches++;
+  return cudaLaunchKernel(fn, grid, block, args, smem, ctx->stream);
+}
+
+static pcb_status validate_rule(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg) {
+  if (!rule || !cfg) return fail(ctx, PCB_INVALID, "rule/config is NULL");
+  if (rule->d != f->d) return fail(ctx, PCB_INVALID, "rule, regions, and integrand dimensions must agree");
+  if (rule->f_eval != (1 << rule->d) + 2 * rule->d * rule->d + 2 * rule->d + 1)
+    return fail(ctx, PCB_INVALID, "rule f_eval %d is not 2^d + 2d^2 + 2d + 1", rule->f_eval);
+  if (cfg->group_size < 1 || cfg->group_size > 64)
+    return fail(ctx, PCB_INVALID, "group_size %d unsupported: the warp schedule covers 1..64 virtual threads", cfg->group_size);
+  if (cfg->err_mode < 0 || cfg->err_mode > 2) return fail(ctx, PCB_INVALID, "unknown err_mode %d", cfg->err_mode);
+  return PCB_OK;
+}
+
+static int eval_grid(pcb_ctx* ctx, const void* fn, long long n) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEvalWarps * 32, 0);
+  if (per_sm < 1) per_sm = 1;
+  long long want = (n + kEvalWarps - 1) / kEvalWarps;
+  return (int)std::min<long long>(want, (long long)per_sm * ctx->sm_count);
+}
+
+// launch the evaluate kernel on SoA device buffers; `bad_dev` must already hold ~0
+static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                                  long long n, long long ld, const double* lefts, const double* lengths, double* I, double* E,
+                                  int32_t* K, unsigned long long* bad_dev) {
+  EvalArgs a;
+  a.f = *f;
+  a.rule = *rule;
+  a.n = n;
+  a.ld = ld;
+  a.lefts = lefts;
+  a.lengths = lengths;
+  a.integrals = I;
+  a.errors = E;
+  a.split_axes = K;
+  a.bad = bad_dev;
+  a.group = cfg->group_size;
+  a.err_mode = cfg->err_mode;
+  a.rel_floor = cfg->rel_floor;
+  const void* fn = eval_kernel(f->family, f->d);
+  PCB_CUDA_TRY(ctx, launch(ctx, fn, dim3(eval_grid(ctx, fn, n)), dim3(kEvalWarps * 32), 0, a));
+  return PCB_OK;
+}
+
+pcb_status tree_sum_dev(pcb_ctx* ctx, const double* in, long long n, double* out) {
+  if (n <= 0) {
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(out, 0, sizeof(double), ctx->stream));
+    return PCB_OK;
+  }
+  int which = 0;
+  while (true) {
+    long long nb = (n + kTreeSpan - 1) / kTreeSpan;
+    double* dst = out;
+    if (nb > 1) {
+      PCB_CUDA_TRY(ctx, ctx->tree[which].ensure((size_t)nb * sizeof(double)));
+      dst = ctx->tree[which].as<double>();
+    }
+    tree_level_kernel<<<(unsigned)nb, kTreeBlock, 0, ctx->stream>>>(in, n, dst);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+    if (nb == 1) return PCB_OK;
+    in = dst;
+    n = nb;
+    which ^= 1;
+  }
+}
+
+static void point_of(const pcb_rule* rule, int d, long long point, const double* left, const double* length, double* x) {
+  // abscissa of rule point `point` in canonical order: left + length*offset (quadrature.py:299-302)
+  int cand[PCB_MAX_DIM] = {0};
+  const int fe = rule->f_eval, corner0 = fe - (1 << d);
+  if (point >= corner0) {
+    long long bits = point - corner0;
+    for (int j = 0; j < d; ++j) cand[j] = 5 + (int)((bits >> j) & 1);
+  } else if (point > 4 * d) {
+    long long q = point - 1 - 4 * d, pr = q >> 2, sg = q & 3, idx = 0;
+    for (int j = 0; j < d; ++j)
+      for (int k = j + 1; k < d; ++k, ++idx)
+        if (idx == pr) { cand[j] = 3 + (int)(sg & 1); cand[k] = 3 + (int)(sg >> 1); }
+  } else if (point > 2 * d) {
+    long long q = point - 1 - 2 * d;
+    cand[q >> 1] = 3 + (int)(q & 1);
+  } else if (point > 0) {
+    long long q = point - 1;
+    cand[q >> 1] = 1 + (int)(q & 1);
+  }
+  for (int j = 0; j < d; ++j) {
+    volatile double prod = length[j] * rule->offsets[cand[j]];  // two roundings, never contracted
+    x[j] = left[j] + prod;
+  }
+}
+
+pcb_status fetch_nonfinite_pagani(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, long long ld,
+                                  const double* lefts_dev, const double* lengths_dev, unsigned long long flat,
+                                  pcb_nonfinite* bad) {
+  const long long region = (long long)(flat / (unsigned long long)rule->f_eval);
+  const long long point = (long long)(flat % (unsigned long long)rule->f_eval);
+  double left[PCB_MAX_DIM], length[PCB_MAX_DIM], x[PCB_MAX_DIM], value = NAN;
+  for (int j = 0; j < f->d; ++j) {
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(&left[j], lefts_dev + j * ld + region, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(&length[j], lengths_dev + j * ld + region, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  point_of(rule, f->d, point, left, length, x);
+  pcb_status st = pcb_eval_points(ctx, f, 1, x, &value);
+  if (st != PCB_OK) return st;
+  if (bad) {
+    bad->region_index = region;
+    bad->point_index = point;
+    bad->value = value;
+    std::memset(bad->point, 0, sizeof bad->point);
+    std::memcpy(bad->point, x, sizeof(double) * f->d);
+  }
+  return fail(ctx, PCB_NONFINITE, "non-finite integrand value %g in region %lld (rule point %lld)", value, region, point);
+}
+
+static pcb_status read_scalars(pcb_ctx* ctx, int first, int count) {
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync((double*)ctx->pinned + first, ctx->scalars.as<double>() + first, count * sizeof(double),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+// scalar slots in ctx->scalars / ctx->pinned
+enum { S_BAD = 0, S_SUM_I = 1, S_SUM_E = 2, S_NSPLIT = 3, S_EMAX = 4, S_RET_I = 5, S_RET_E = 6 };
+
+}  // namespace pcb
+
+using namespace pcb;
+
+extern "C" {
+
+pcb_status pcb_tree_sum(pcb_ctx* ctx, int64_t n, const double* values, double* out) {
+  if (!ctx || !out || n < 0 || (n > 0 && !values)) return fail(ctx, PCB_INVALID, "tree_sum: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  if (n > 0) {
+    PCB_CUDA_TRY(ctx, ctx->rows_a.ensure((size_t)n * sizeof(double)));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_a.p, values, (size_t)n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  PCB_TRY(tree_sum_dev(ctx, ctx->rows_a.as<double>(), n, ctx->scalars.as<double>() + S_SUM_I));
+  PCB_TRY(read_scalars(ctx, S_SUM_I, 1));
+  *out = ((double*)ctx->pinned)[S_SUM_I];
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_evaluate_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                                   int64_t n, int64_t ld, const double* lefts_dev, const double* lengths_dev,
+                                   double* integrals_dev, double* errors_dev, int32_t* split_axes_dev, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_rule(ctx, f, rule, cfg));
+  if (n <= 0) return fail(ctx, PCB_INVALID, "region list is empty");
+  if (ld < n) return fail(ctx, PCB_INVALID, "leading dimension %lld < n %lld", (long long)ld, (long long)n);
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  unsigned long long* bad_dev = ctx->scalars.as<unsigned long long>() + S_BAD;
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xFF, sizeof(unsigned long long), ctx->stream));
+  PCB_TRY(evaluate_launch(ctx, f, rule, cfg, n, ld, lefts_dev, lengths_dev, integrals_dev, errors_dev, split_axes_dev, bad_dev));
+  PCB_TRY(read_scalars(ctx, S_BAD, 1));
+  unsigned long long flat = ((unsigned long long*)ctx->pinned)[S_BAD];
+  if (flat != ~0ULL) return fetch_nonfinite_pagani(ctx, f, rule, ld, lefts_dev, lengths_dev, flat, bad);
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_evaluate(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                               int64_t n, const double* lefts, const double* lengths, double* integrals, double* errors,
+                               int64_t* split_axes, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_rule(ctx, f, rule, cfg));
+  if (n <= 0) return fail(ctx, PCB_INVALID, "region list is empty");
+  if (!lefts || !lengths || !integrals || !errors || !split_axes) return fail(ctx, PCB_INVALID, "pagani_evaluate: NULL buffer");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = f->d;
+  const long long ld = round_up(n, 32);
+  const size_t row_bytes = (size_t)n * d * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->rows_a.ensure(row_bytes));
+  PCB_CUDA_TRY(ctx, ctx->rows_b.ensure(row_bytes));
+  PCB_CUDA_TRY(ctx, ctx->lefts[0].ensure((size_t)ld * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[0].ensure((size_t)ld * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)n * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)n * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)n * sizeof(int32_t)));
+  PCB_CUDA_TRY(ctx, ctx->k64.ensure((size_t)n * sizeof(long long)));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_a.p, lefts, row_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_b.p, lengths, row_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  const int tb = (int)std::min<long long>((n + 255) / 256, (long long)ctx->sm_count * 8);
+  rows_to_soa_kernel<<<tb, 256, 0, ctx->stream>>>(d, n, ld, ctx->rows_a.as<double>(), ctx->lefts[0].as<double>());
+  rows_to_soa_kernel<<<tb, 256, 0, ctx->stream>>>(d, n, ld, ctx->rows_b.as<double>(), ctx->lengths[0].as<double>());
+  ctx->launches += 2;
+  pcb_status st = pcb_pagani_evaluate_dev(ctx, f, rule, cfg, n, ld, ctx->lefts[0].as<double>(), ctx->lengths[0].as<double>(),
+                                          ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), bad);
+  if (st != PCB_OK) return st;
+  widen_axes_kernel<<<tb, 256, 0, ctx->stream>>>(n, ctx->est_k.as<int32_t>(), ctx->k64.as<long long>());
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(integrals, ctx->est_i.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(errors, ctx->est_e.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(split_axes, ctx->k64.p, (size_t)n * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                             pcb_pagani_result* result, pcb_pagani_progress* records, pcb_pagani_progress_fn progress,
+                             void* user, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_rule(ctx, f, rule, cfg));
+  if (!result) return fail(ctx, PCB_INVALID, "result is NULL");
+  if (!(cfg->rel_tol > 0)) return fail(ctx, PCB_INVALID, "rel_tol must be > 0");
+  if (cfg->max_iterations < 0 || cfg->initial_regions < 1) return fail(ctx, PCB_INVALID, "bad iteration/initial-region budget");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = f->d;
+  const long long launches0 = ctx->launches;
+
+  // iteration 0: smallest g with g^d >= initial_regions (pagani.py:273-279), uniform tiling (core.py:250-269)
+  long long g = 1, n = 1;
+  long double exact = 1;
+  for (;; ++g) {
+    exact = 1;
+    for (int j = 0; j < d; ++j) exact *= (long double)g;
+    if (exact >= (long double)cfg->initial_regions) break;
+  }
+  if (exact > (long double)cfg->region_cap)
+    return fail(ctx, PCB_BUDGET, "uniform split needs %.0Lf regions, cap is %lld", exact, (long long)cfg->region_cap);
+  n = (long long)exact;
+
+  cudaEvent_t ev0, ev1;
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev0));
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev1));
+  struct EventGuard {
+    cudaEvent_t a, b;
+    ~EventGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  } guard{ev0, ev1};
+  cudaEventRecord(ev0, ctx->stream);
+
+  int cur = 0;
+  long long ld = round_up(n, 32);
+  PCB_CUDA_TRY(ctx, ctx->lefts[cur].ensure((size_t)ld * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[cur].ensure((size_t)ld * d * sizeof(double)));
+  tiling_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+      d, (int)g, n, ld, 1.0 / (double)g, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>());
+  ctx->launches++;
+
+  double* sc = ctx->scalars.as<double>();
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>();
+  double* host = (double*)ctx->pinned;
+  unsigned long long* host_u = (unsigned long long*)ctx->pinned;
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc, 0, 16 * sizeof(double), ctx->stream));
+
+  auto evaluate = [&](long long count, long long ldim) -> pcb_status {
+    PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)count * sizeof(double)));
+    PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)count * sizeof(double)));
+    PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)count * sizeof(int32_t)));
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + S_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+    return evaluate_launch(ctx, f, rule, cfg, count, ldim, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(),
+                           ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), sc_u + S_BAD);
+  };
+  PCB_TRY(evaluate(n, ld));
+
+  double fin_i = 0.0, fin_e = 0.0, estimate = 0.0, errorest = 0.0;
+  long long fin_count = 0, processed = n;
+  int n_rec = 0, reason = PCB_STOP_MAX_ITER;
+  bool converged = false, have_retired = false;
+
+  for (int it = 0; it <= cfg->max_iterations; ++it) {
+    PCB_TRY(tree_sum_dev(ctx, ctx->est_i.as<double>(), n, sc + S_SUM_I));
+    PCB_TRY(tree_sum_dev(ctx, ctx->est_e.as<double>(), n, sc + S_SUM_E));
+    PCB_TRY(read_scalars(ctx, 0, 8));
+    if (host_u[S_BAD] != ~0ULL)
+      return fetch_nonfinite_pagani(ctx, f, rule, ld, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(), host_u[S_BAD], bad);
+    if (have_retired) {  // fin += tree_sum(act[~mask]) of the previous iteration (pagani.py:371-372)
+      fin_i += host[S_RET_I];
+      fin_e += host[S_RET_E];
+      have_retired = false;
+    }
+    estimate = fin_i + host[S_SUM_I];
+    errorest = fin_e + host[S_SUM_E];
+    pcb_pagani_progress rec;
+    rec.iteration = it;
+    rec.reserved = 0;
+    rec.n_regions = fin_count + n;
+    rec.active = n;
+    rec.estimate = estimate;
+    rec.errorest = errorest;
+    if (records) records[n_rec] = rec;
+    ++n_rec;
+    if (progress) progress(user, &rec);
+    if (errorest <= cfg->rel_tol * std::fabs(estimate)) {
+      converged = true;
+      reason = PCB_STOP_TOLERANCE;
+      break;
+    }
+    if (it == cfg->max_iterations) { reason = PCB_STOP_MAX_ITER; break; }
+    if (n == 0) { reason = PCB_STOP_NO_ACTIVE; break; }
+
+    // classification (pagani.py:361-365)
+    const double budget = 0.8 * cfg->rel_tol * std::fabs(estimate);
+    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
+    PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)n));
+    PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));
+    PCB_CUDA_TRY(ctx, ctx->offsets.ensure((size_t)nblk * sizeof(unsigned long long)));
+    ClassifyArgs ca;
+    ca.n = n; ca.ld = ld; ca.d = d; ca.mode = 0; ca.budget = budget; ca.emax = 0.0;
+    ca.lengths = ctx->lengths[cur].as<double>();
+    ca.errors = ctx->est_e.as<double>();
+    ca.flags = ctx->flags.as<unsigned char>();
+    ca.block_counts = ctx->counts.as<unsigned int>();
+    long long n_split = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      classify_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(ca);
+      scan_counts_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->counts.as<unsigned int>(), (int)nblk,
+                                                      ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT);
+      ctx->launches += 2;
+      PCB_TRY(read_scalars(ctx, S_NSPLIT, 1));
+      n_split = (long long)host_u[S_NSPLIT];
+      if (n_split > 0 || pass == 1) break;
+      // nothing exceeds its budget: force progress on the worst regions, ties included (pagani.py:364-365)
+      PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc + S_EMAX, 0, sizeof(double), ctx->stream));
+      max_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 1024), 256, 0, ctx->stream>>>(ctx->est_e.as<double>(), n, sc + S_EMAX);
+      ctx->launches++;
+      PCB_TRY(read_scalars(ctx, S_EMAX, 1));
+      ca.mode = 1;
+      ca.emax = host[S_EMAX];
+    }
+    if (processed + 2 * n_split > cfg->region_cap) { reason = PCB_STOP_REGION_CAP; break; }
+
+    // retire the rest, bisect the split regions (pagani.py:371-378)
+    const long long n_child = 2 * n_split, n_ret = n - n_split, ld_out = round_up(n_child, 32);
+    const int nxt = cur ^ 1;
+    PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_out * d * sizeof(double)));
+    PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_out * d * sizeof(double)));
+    PCB_CUDA_TRY(ctx, ctx->ret_i.ensure((size_t)std::max<long long>(n_ret, 1) * sizeof(double)));
+    PCB_CUDA_TRY(ctx, ctx->ret_e.ensure((size_t)std::max<long long>(n_ret, 1) * sizeof(double)));
+    SplitArgs sa;
+    sa.n = n; sa.ld_in = ld; sa.ld_out = ld_out; sa.d = d;
+    sa.lefts = ctx->lefts[cur].as<double>();
+    sa.lengths = ctx->lengths[cur].as<double>();
+    sa.integrals = ctx->est_i.as<double>();
+    sa.errors = ctx->est_e.as<double>();
+    sa.axes = ctx->est_k.as<int32_t>();
+    sa.flags = ctx->flags.as<unsigned char>();
+    sa.block_offsets = ctx->offsets.as<unsigned long long>();
+    sa.out_lefts = ctx->lefts[nxt].as<double>();
+    sa.out_lengths = ctx->lengths[nxt].as<double>();
+    sa.retired_i = ctx->ret_i.as<double>();
+    sa.retired_e = ctx->ret_e.as<double>();
+    split_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(sa);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+    PCB_TRY(tree_sum_dev(ctx, ctx->ret_i.as<double>(), n_ret, sc + S_RET_I));
+    PCB_TRY(tree_sum_dev(ctx, ctx->ret_e.as<double>(), n_ret, sc + S_RET_E));
+    have_retired = true;  // read back together with the next iteration's sums
+    fin_count += n_ret;
+    processed += n_child;
+    n = n_child;
+    ld = ld_out;
+    cur = nxt;
+    PCB_TRY(evaluate(n, ld));
+  }
+
+  cudaEventRecord(ev1, ctx->stream);
+  PCB_CUDA_TRY(ctx, cudaEventSynchronize(ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  result->estimate = estimate;
+  result->errorest = errorest;
+  result->iterations = n_rec - 1;
+  result->converged = converged ? 1 : 0;
+  result->regions_processed = processed;
+  result->reason = reason;
+  result->n_records = n_rec;
+  result->seconds_device = ms * 1e-3;
+  result->kernel_launches = ctx->launches - launches0;
+  return PCB_OK;
+}
+
+// quadrature.apply_rules for a single region: generic table, plain pair tree over all points.
+__global__ void region_points_kernel(int d, int fe, const double* gen, const double* left, const double* length, double* pts) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= fe * d) return;
+  int j = i % d;
+  double off = (gen[i] + 1.0) / 2.0;
+  pts[i] = left[j] + length[j] * off;
+}
+__global__ void rule_products_kernel(int fe, const double* w, const double* fx, double* prod) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 5 * fe) prod[i] = w[i] * fx[i % fe];
+}
+__global__ void scale_by_volume_kernel(int d, const double* length, double* sums) {
+  double vol = length[0];
+  for (int j = 1; j < d; ++j) vol = vol * length[j];
+  for (int k = 0; k < 5; ++k) sums[k] = vol * sums[k];
+}
+
+pcb_status pcb_apply_rules(pcb_ctx* ctx, const pcb_integrand* f, int32_t f_eval, const double* generators, const double* weights,
+                           const double* left, const double* length, double values[5], double* stored_evals, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  if (f_eval < 1 || !generators || !weights || !left || !length || !values || !stored_evals)
+    return fail(ctx, PCB_INVALID, "apply_rules: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = f->d, fe = f_eval;
+  // layout in rows_a: gen[fe*d] | w[5*fe] | left[d] | length[d] | pts[fe*d] | fx[fe] | prod[5*fe]
+  const size_t total = (size_t)fe * d * 2 + (size_t)fe * 11 + 2 * d;
+  PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure(total * sizeof(double)));
+  double* base = ctx->mc_tmp.as<double>();
+  double *g_dev = base, *w_dev = g_dev + (size_t)fe * d, *l_dev = w_dev + 5 * (size_t)fe, *h_dev = l_dev + d;
+  double *p_dev = h_dev + d, *fx_dev = p_dev + (size_t)fe * d, *prod_dev = fx_dev + fe;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(g_dev, generators, (size_t)fe * d * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(w_dev, weights, (size_t)fe * 5 * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(l_dev, left, d * 8, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(h_dev, length, d * 8, cudaMemcpyHostToDevice, ctx->stream));
+  region_points_kernel<<<(fe * d + 255) / 256, 256, 0, ctx->stream>>>(d, fe, g_dev, l_dev, h_dev, p_dev);
+  ctx->launches++;
+  long long nn = fe;
+  pcb_integrand fv = *f;
+  const double* pts_c = p_dev;
+  void* args[] = {&fv, &nn, &pts_c, &fx_dev};
+  PCB_CUDA_TRY(ctx, cudaLaunchKernel(points_kernel(f->family, d), dim3((fe + 255) / 256), dim3(256), args, 0, ctx->stream));
+  rule_products_kernel<<<(5 * fe + 255) / 256, 256, 0, ctx->stream>>>(fe, w_dev, fx_dev, prod_dev);
+  ctx->launches += 2;
+  double* sums = ctx->scalars.as<double>() + 16;
+  for (int k = 0; k < 5; ++k) PCB_TRY(tree_sum_dev(ctx, prod_dev + (size_t)k * fe, fe, sums + k));
+  scale_by_volume_kernel<<<1, 1, 0, ctx->stream>>>(d, h_dev, sums);
+  ctx->launches++;
+  std::vector<double> pts_host((size_t)fe * d);
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(stored_evals, fx_dev, (size_t)fe * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(pts_host.data(), p_dev, (size_t)fe * d * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(values, sums, 5 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < fe; ++i) {
+    if (!std::isfinite(stored_evals[i])) {
+      if (bad) {
+        bad->region_index = -1;
+        bad->point_index = i;
+        bad->value = stored_evals[i];
+        std::memset(bad->point, 0, sizeof bad->point);
+        std::memcpy(bad->point, &pts_host[(size_t)i * d], sizeof(double) * d);
+      }
+      return fail(ctx, PCB_NONFINITE, "non-finite integrand value %g at rule point %d", stored_evals[i], i);
+    }
+  }
+  return PCB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// Host-side runtime shared by the C-ABI translation units: context, device buffers, launch helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/parcube_b200.h"
+
+namespace pcb {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  // grow-only; contents are NOT preserved
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    release();
+    size_t want = bytes + bytes / 8 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      e = cudaMalloc(&p, bytes);
+      want = bytes;
+    }
+    if (e == cudaSuccess) cap = want;
+    else p = nullptr;
+    return e;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+}  // namespace pcb
+
+struct pcb_ctx {
+  int device = 0;
+  int sm_count = 0;
+  int clock_khz = 0;
+  size_t smem_optin = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  long long launches = 0;
+  char name[256] = {0};
+  void* pinned = nullptr;  // 64 KiB staging for small device->host reads
+  // scratch device buffers, grown on demand and reused across calls
+  pcb::DevBuf lefts[2], lengths[2], est_i, est_e, est_k, flags, counts, offsets, ret_i, ret_e, tree[2], scalars;
+  pcb::DevBuf rows_a, rows_b, k64;
+  pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject;
+};
+
+namespace pcb {
+
+inline pcb_status fail(pcb_ctx* ctx, pcb_status code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf;
+  return code;
+}
+
+#define PCB_CUDA_TRY(ctx, expr)                                                                         \
+  do {                                                                                                  \
+    cudaError_t _e = (expr);                                                                            \
+    if (_e != cudaSuccess) {                                                                            \
+      (void)cudaGetLastError();                                                                         \
+      return pcb::fail(ctx, PCB_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    }                                                                                                   \
+  } while (0)
+
+#define PCB_TRY(expr)                     \
+  do {                                    \
+    pcb_status _s = (expr);               \
+    if (_s != PCB_OK) return _s;          \
+  } while (0)
+
+// kernel getters, one translation unit per integrand family (pagani_inst.cu / mcubes_inst.cu)
+typedef const void* (*kernel_getter)(int d);
+const void* eval_kernel(int family, int d);
+const void* points_kernel(int family, int d);
+const void* vsample_kernel_ptr(int family, int d);
+
+inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+pcb_status validate_integrand(pcb_ctx* ctx, const pcb_integrand* f);
+
+// internal entry points shared between translation units
+pcb_status tree_sum_dev(pcb_ctx* ctx, const double* in_dev, long long n, double* out_dev_scalar);
+pcb_status fetch_nonfinite_pagani(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, long long ld,
+                                  const double* lefts_dev, const double* lengths_dev, unsigned long long flat,
+                                  pcb_nonfinite* bad);
+
+}  // namespace pcb

@@ -222,7 +222,7 @@ class OrbitRule(_Frozen):
     """
 
     __slots__ = ("d", "f_eval", "offsets", "weights", "corner_parity", "split_weights",
-                 "high_mask", "inv_scales_low")
+                 "high_mask", "null_scales")
 
 
 def orbit_form(rule: RuleTable) -> OrbitRule:
@@ -289,7 +289,7 @@ def orbit_form(rule: RuleTable) -> OrbitRule:
     out._put("corner_parity", parity_flag)
     out._put("split_weights", np.array(rule.split_weights, dtype=np.float64))
     out._put("high_mask", (degrees >= 5).astype(np.int32))
-    out._put("inv_scales_low", scales)
+    out._put("null_scales", scales)
     return out
 
 
