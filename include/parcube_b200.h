@@ -182,6 +182,13 @@ int64_t pcb_launch_count(const pcb_ctx* ctx);
 /* Measured FP64 peak: runs a dependent-free DFMA loop on every SM; returns TFLOP/s. */
 pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops);
 
+/* ---- per-kernel timing for the roofline report -------------------------------------------
+ * Between begin and end every launch of the two dominant kernels (PAGANI evaluate, m-Cubes
+ * V-Sample) is bracketed by CUDA events on the launching stream.  `kind` 0 = evaluate (units =
+ * regions), 1 = V-Sample (units = samples).  end() synchronises and returns the sums.          */
+pcb_status pcb_profile_begin(pcb_ctx* ctx);
+pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_t* launches, double* units);
+
 /* ---- integrand functors: replaces Integrand.eval_many (core.py:66-68, integrands.py) --- */
 pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points /* (n,d) */,
                            double* values /* (n) */);
@@ -232,6 +239,12 @@ pcb_status pcb_grid_refine(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double
                            const double* contributions, double alpha, int32_t smoothing,
                            double* new_boundaries);
 
+/* ---- grid transform: replaces transform / transform_many (vegas_grid.py:87-114) -------------
+ * y: (n,d) in [0,1); outputs x (n,d), jac (n), bins (n,d) int64.  Returns PCB_INVALID when a
+ * coordinate lies outside [0,1) (the reference's ValueError).                                   */
+pcb_status pcb_grid_transform(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double* boundaries, int64_t n,
+                              const double* y, double* x, double* jac, int64_t* bins);
+
 /* ---- m-Cubes driver: replaces run (mcubes.py:332-382), loop device-resident ---------------
  * rel_tol <= 0 reproduces the reference (fixed iteration count); rel_tol > 0 adds the
  * time-to-epsrel stop of BASELINE.md section 3.  iterations_out: capacity `iterations`.
@@ -246,6 +259,10 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
 /* ---- RNG mirror: replaces mcubes._uniform / derive_seed (mcubes.py:51-60) -------------- */
 pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,
                         const uint64_t* counters, double* out);
+
+/* ---- self-test hook: the sampler's division-by-constant sequence, out[i] = x[i] / g ----------
+ * (tests compare it bit-for-bit with IEEE division; not part of the reference surface)          */
+pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g, double* out);
 
 #ifdef __cplusplus
 }

@@ -218,7 +218,7 @@ def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1
     fin_i = fin_e = 0.0
     fin_n = 0
     processed = len(lefts)
-    history, active_counts = [], []
+    history, active_counts, forced = [], [], []
     converged, reason = False, ""
     for it in range(max_iterations + 1):
         estimate = fin_i + tree_sum(act_i)
@@ -242,6 +242,7 @@ def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1
         mask = act_e > budget * vol
         if not mask.any():
             mask = act_e >= act_e.max()
+            forced.append(it)
         n_split = int(np.count_nonzero(mask))
         if processed + 2 * n_split > region_cap:
             reason = "region cap reached"
@@ -255,7 +256,7 @@ def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1
                                               bounds=bounds, **kw)
     return dict(estimate=estimate, errorest=errorest, iterations=len(history) - 1,
                 regions_processed=processed, converged=converged, history=history,
-                reason=reason, active_counts=active_counts)
+                reason=reason, active_counts=active_counts, forced_iterations=forced)
 
 
 # =========================================================================== m-Cubes RNG

@@ -101,6 +101,8 @@ SIGNATURES = {
     "pcb_device_info": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pcb_launch_count": (C.c_int64, [C.c_void_p]),
     "pcb_measure_fp64_peak": (C.c_int, [C.c_void_p, _DP]),
+    "pcb_profile_begin": (C.c_int, [C.c_void_p]),
+    "pcb_profile_end": (C.c_int, [C.c_void_p, C.c_int32, _DP, C.POINTER(C.c_int64), _DP]),
     "pcb_eval_points": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_void_p]),
     "pcb_pagani_evaluate": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
                                       C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -123,6 +125,9 @@ SIGNATURES = {
                                  C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.POINTER(McubesIterationC),
                                  C.POINTER(C.c_int32), MCUBES_PROGRESS_FN, C.c_void_p, C.c_void_p, C.c_void_p, _DP,
                                  C.POINTER(NonFiniteC)]),
+    "pcb_grid_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
+    "pcb_debug_divide": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
     "pcb_uniforms": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
@@ -200,6 +205,15 @@ class Context:
 
     def launch_count(self) -> int:
         return int(self.lib.pcb_launch_count(self.handle))
+
+    def profile_begin(self):
+        self.check(self.lib.pcb_profile_begin(self.handle))
+
+    def profile_end(self, kind: int):
+        """(kernel_ms, launches, units) of the evaluate (0) or V-Sample (1) launches since profile_begin."""
+        ms, n, units = C.c_double(), C.c_int64(), C.c_double()
+        self.check(self.lib.pcb_profile_end(self.handle, kind, C.byref(ms), C.byref(n), C.byref(units)))
+        return ms.value, n.value, units.value
 
     def measure_fp64_peak(self) -> float:
         out = C.c_double()
@@ -446,4 +460,24 @@ def uniforms(seed: int, streams, counters, rng_kind: int = RNG_REFERENCE_HASH, d
     out = np.empty(s.size)
     with ctx.call_lock:
         ctx.check(ctx.lib.pcb_uniforms(ctx.handle, C.c_uint64(seed & (2**64 - 1)), rng_kind, s.size, _ptr(s), _ptr(c), _ptr(out)))
+    return out
+
+
+def grid_transform(boundaries: np.ndarray, y: np.ndarray, device=None):
+    ctx = context(device)
+    d, nb1 = boundaries.shape
+    b, yy = _f64(boundaries), _f64(y)
+    n = yy.shape[0]
+    x, jac, bins = np.empty((n, d)), np.empty(n), np.empty((n, d), dtype=np.int64)
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_grid_transform(ctx.handle, d, nb1 - 1, _ptr(b), n, _ptr(yy), _ptr(x), _ptr(jac), _ptr(bins)))
+    return x, jac, bins
+
+
+def debug_divide(x: np.ndarray, g: int, device=None) -> np.ndarray:
+    ctx = context(device)
+    xx = _f64(x).ravel()
+    out = np.empty_like(xx)
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_debug_divide(ctx.handle, xx.size, _ptr(xx), int(g), _ptr(out)))
     return out

@@ -89,6 +89,12 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
     cudaStreamDestroy(ctx->stream);
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (int k = 0; k < 2; ++k)
+    for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
+  for (auto& sp : ctx->span_pool) {
+    cudaEventDestroy(sp.a);
+    cudaEventDestroy(sp.b);
+  }
   delete ctx;
 }
 
@@ -129,6 +135,34 @@ pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops) {
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *tflops = best;
+  return PCB_OK;
+}
+
+pcb_status pcb_profile_begin(pcb_ctx* ctx) {
+  if (!ctx) return PCB_INVALID;
+  for (int k = 0; k < 2; ++k) {
+    for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
+    ctx->spans[k].clear();
+    ctx->span_units[k] = 0;
+  }
+  ctx->profiling = true;
+  return PCB_OK;
+}
+
+pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_t* launches, double* units) {
+  if (!ctx || kind < 0 || kind > 1) return PCB_INVALID;
+  ctx->profiling = false;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  double total = 0;
+  for (auto& sp : ctx->spans[kind]) {
+    float ms = 0;
+    PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, sp.a, sp.b));
+    total += ms;
+  }
+  if (kernel_ms) *kernel_ms = total;
+  if (launches) *launches = (int64_t)ctx->spans[kind].size();
+  if (units) *units = ctx->span_units[kind];
   return PCB_OK;
 }
 

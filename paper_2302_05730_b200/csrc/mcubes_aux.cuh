@@ -50,6 +50,34 @@ __global__ void group_tree_kernel(const double* __restrict__ seg_partials, int n
   }
 }
 
+// transform_many (vegas_grid.py:99-114) for caller-supplied points; flags[0] set on y outside [0,1)
+__global__ void grid_transform_kernel(int d, int nb, const double* __restrict__ bnd, long long n, const double* __restrict__ y,
+                                      double* __restrict__ x, double* __restrict__ jac, long long* __restrict__ bins, int* flags) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    double jj = 1.0;
+    for (int j = 0; j < d; ++j) {
+      const double yy = y[i * d + j];
+      if (!(yy >= 0.0 && yy < 1.0)) { flags[0] = 1; x[i * d + j] = yy; bins[i * d + j] = 0; continue; }
+      const double z = yy * (double)nb;
+      const double zi = __dadd_rz(z, 4503599627370496.0);
+      int b = __double2loint(zi);
+      const double frac = z - (zi - 4503599627370496.0);
+      const double lo = bnd[j * (nb + 1) + b];
+      const double w = bnd[j * (nb + 1) + b + 1] - lo;
+      x[i * d + j] = lo + frac * w;
+      const double jw = (double)nb * w;
+      jj = (j == 0) ? jw : jj * jw;
+      bins[i * d + j] = b;
+    }
+    jac[i] = jj;
+  }
+}
+
+__global__ void debug_divide_kernel(long long n, const double* __restrict__ x, double g, double rg, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = div_by_const(x[i], g, rg);
+}
+
 __global__ void deinterleave2_kernel(const double* __restrict__ in, int n, double* __restrict__ a, double* __restrict__ b) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { a[i] = in[2 * i]; b[i] = in[2 * i + 1]; }

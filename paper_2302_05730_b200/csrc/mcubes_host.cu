@@ -125,7 +125,12 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   a.bad = sc_u + M_BAD;
   a.block_hist = ctx->mc_hist.as<double>();
   void* args[] = {&a};
-  PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(L.blocks), dim3(L.warps * 32), args, L.smem, ctx->stream));
+  {
+    const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
+    ProfileSpan span(ctx, 1, (double)(c1 - c0) * plan->p);
+    PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(L.blocks), dim3(L.warps * 32), args, L.smem, ctx->stream));
+    ctx->launches++;
+  }
   merge_hist_kernel<<<(d * nb + 255) / 256, 256, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), L.blocks, d * nb,
                                                                      ctx->mc_contrib.as<double>());
   int pow2 = 1;
@@ -136,7 +141,7 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
   double* ge = gi + n_groups;
   deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
-  ctx->launches += 4;
+  ctx->launches += 3;
   PCB_CUDA_TRY(ctx, cudaGetLastError());
   PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));   // engine.reduce in group order (mcubes.py:292-293)
   PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
@@ -234,6 +239,52 @@ pcb_status pcb_grid_refine(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double
   PCB_TRY(refine_dev(ctx, d, n_bins, ctx->mc_bounds[0].as<double>(), ctx->mc_contrib.as<double>(), alpha, smoothing,
                      ctx->mc_bounds[1].as<double>()));
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(new_boundaries, ctx->mc_bounds[1].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_grid_transform(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double* boundaries, int64_t n, const double* y,
+                              double* x, double* jac, int64_t* bins) {
+  if (!ctx) return PCB_INVALID;
+  if (d < 1 || d > PCB_MAX_DIM || n_bins < 2 || n < 0 || !boundaries || (n > 0 && (!y || !x || !jac || !bins)))
+    return fail(ctx, PCB_INVALID, "grid_transform: bad arguments");
+  if (n == 0) return PCB_OK;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t bbytes = (size_t)d * (n_bins + 1) * sizeof(double), pbytes = (size_t)n * d * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure(3 * pbytes + (size_t)n * sizeof(double) + 64));
+  double* y_dev = ctx->mc_tmp.as<double>();
+  double* x_dev = y_dev + (size_t)n * d;
+  long long* b_dev = reinterpret_cast<long long*>(x_dev + (size_t)n * d);
+  double* j_dev = reinterpret_cast<double*>(b_dev + (size_t)n * d);
+  int* flag_dev = reinterpret_cast<int*>(ctx->scalars.as<double>() + 60);
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(flag_dev, 0, sizeof(int), ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, boundaries, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(y_dev, y, pbytes, cudaMemcpyHostToDevice, ctx->stream));
+  grid_transform_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+      d, n_bins, ctx->mc_bounds[0].as<double>(), n, y_dev, x_dev, j_dev, b_dev, flag_dev);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  int flag = 0;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(&flag, flag_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(x, x_dev, pbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(jac, j_dev, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(bins, b_dev, (size_t)n * d * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (flag) return fail(ctx, PCB_INVALID, "transform inputs must lie in [0, 1)");
+  return PCB_OK;
+}
+
+pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g, double* out) {
+  if (!ctx || n < 0 || g < 1 || (n > 0 && (!x || !out))) return fail(ctx, PCB_INVALID, "debug_divide: bad arguments");
+  if (n == 0) return PCB_OK;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure((size_t)n * 16));
+  double* x_dev = ctx->mc_tmp.as<double>();
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(x_dev, x, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  debug_divide_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(n, x_dev, (double)g, 1.0 / (double)g, x_dev + n);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out, x_dev + n, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return PCB_OK;
 }

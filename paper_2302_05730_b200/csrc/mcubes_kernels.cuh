@@ -60,7 +60,7 @@ __device__ __forceinline__ void hist_add(double* hist, unsigned char* tags, cons
 }
 
 template <int FAM, int D>
-__global__ void __launch_bounds__(1024) vsample_kernel(const __grid_constant__ SampleArgs a) {
+__global__ void __launch_bounds__(512) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb, nb1 = a.nb + 1;

@@ -55,6 +55,7 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   a.err_mode = cfg->err_mode;
   a.rel_floor = cfg->rel_floor;
   const void* fn = eval_kernel(f->family, f->d);
+  ProfileSpan span(ctx, 0, (double)n);
   PCB_CUDA_TRY(ctx, launch(ctx, fn, dim3(eval_grid(ctx, fn, n)), dim3(kEvalWarps * 32), 0, a));
   return PCB_OK;
 }

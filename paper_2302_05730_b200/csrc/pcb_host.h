@@ -55,6 +55,12 @@ struct pcb_ctx {
   // scratch device buffers, grown on demand and reused across calls
   pcb::DevBuf lefts[2], lengths[2], est_i, est_e, est_k, flags, counts, offsets, ret_i, ret_e, tree[2], scalars;
   pcb::DevBuf rows_a, rows_b, k64;
+  // roofline profiling (pcb_profile_begin/end)
+  bool profiling = false;
+  struct Span { cudaEvent_t a, b; };
+  std::vector<Span> spans[2];
+  std::vector<Span> span_pool;
+  double span_units[2] = {0, 0};
   pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject;
 };
 
@@ -90,6 +96,31 @@ typedef const void* (*kernel_getter)(int d);
 const void* eval_kernel(int family, int d);
 const void* points_kernel(int family, int d);
 const void* vsample_kernel_ptr(int family, int d);
+
+// bracket one dominant-kernel launch with events when profiling is on
+struct ProfileSpan {
+  pcb_ctx* ctx;
+  int kind;
+  pcb_ctx::Span span{};
+  bool on;
+  ProfileSpan(pcb_ctx* c, int k, double units) : ctx(c), kind(k), on(c->profiling) {
+    if (!on) return;
+    if (!ctx->span_pool.empty()) {
+      span = ctx->span_pool.back();
+      ctx->span_pool.pop_back();
+    } else {
+      cudaEventCreate(&span.a);
+      cudaEventCreate(&span.b);
+    }
+    ctx->span_units[kind] += units;
+    cudaEventRecord(span.a, ctx->stream);
+  }
+  ~ProfileSpan() {
+    if (!on) return;
+    cudaEventRecord(span.b, ctx->stream);
+    ctx->spans[kind].push_back(span);
+  }
+};
 
 inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
 

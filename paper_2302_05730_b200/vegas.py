@@ -72,6 +72,21 @@ def init_grid(d: int, n_bins: int = DEFAULT_N_BINS) -> VegasGrid:
     return VegasGrid(d, n_bins, np.tile(np.arange(n_bins + 1) / n_bins, (d, 1)))
 
 
+def transform_many(y, grid: VegasGrid, device=None):
+    """(x, jacobian, bin_ids) for an (n, d) array of uniform points (vegas_grid.py:99-114), on the device."""
+    y = np.asarray(y, dtype=float)
+    if y.ndim != 2 or y.shape[1] != grid.d:
+        raise ValueError(f"expected (n, {grid.d}) points")
+    return _native.grid_transform(grid.boundaries, y, device=device)
+
+
+def transform(y, grid: VegasGrid):
+    """One uniform point through the grid (vegas_grid.py:87-96)."""
+    y = np.atleast_1d(np.asarray(y, dtype=float))
+    x, jac, bins = transform_many(y[None, :], grid)
+    return x[0], float(jac[0]), bins[0]
+
+
 def refine_grid(grid: VegasGrid, contributions: BinContributions, params: GridRefineParams | None = None,
                 device=None) -> VegasGrid:
     """Equal-damped-contribution boundaries, per axis (vegas_grid.py:142-193); csrc/mcubes_aux.cuh."""

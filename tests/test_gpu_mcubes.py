@@ -1,0 +1,294 @@
+"""m-Cubes parity on the B200, through the C-ABI behind the reference-named API.
+
+Bars (BASELINE.json north_star): with the reference's counter hash the draws are bit-identical,
+so a pass must reproduce the reference's sums to 1e-12 relative (injected sample set included);
+runs agree within 3 combined sigma (in fact to 1e-10); Philox runs agree within 3 sigma.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2302_05730_b200 as pb
+from conftest import fromhex
+from oracle import parcube_oracle as po
+from paper_2302_05730_b200 import _native, stratified, vegas
+
+pytestmark = pytest.mark.gpu
+
+REL_SUM = 1e-12
+
+
+def _bounds(meta):
+    if "low" not in meta:
+        return None
+    return pb.IntegrationBounds(meta["low"], meta["high"])
+
+
+def _integrand(meta):
+    f = pb.get_integrand(meta["family"], meta["d"])
+    b = _bounds(meta)
+    return pb.scale_to_bounds(f, b) if b is not None else f
+
+
+# ------------------------------------------------------------------ primitives
+def test_hash_rng_bit_exact(golden):
+    for key, want in golden["rng"]["uniform"].items():
+        s, t, c = map(int, key.split(","))
+        assert float(stratified._uniform(s, np.uint64(t), np.uint64(c))).hex() == want
+    rng = np.random.default_rng(1)
+    streams = rng.integers(0, 2**63, 100000, dtype=np.uint64)
+    counters = rng.integers(0, 2**63, 100000, dtype=np.uint64)
+    for seed in (0, 12345, 2**64 - 1):
+        assert np.array_equal(_native.uniforms(seed, streams, counters), po.uniform(seed, streams, counters))
+    assert np.array_equal(pb.RngStream(7, 3).take(5), po.uniform(7, np.uint64(3), np.arange(5, dtype=np.uint64)))
+
+
+def test_philox_rng_is_uniform_and_deterministic():
+    s = np.repeat(np.arange(100, dtype=np.uint64), 10000)
+    c = np.tile(np.arange(10000, dtype=np.uint64), 100)
+    u = _native.uniforms(42, s, c, _native.RNG_PHILOX)
+    assert np.array_equal(u, _native.uniforms(42, s, c, _native.RNG_PHILOX))
+    assert 0.0 <= u.min() and u.max() < 1.0
+    assert abs(u.mean() - 0.5) < 5e-4 * 3 and abs(u.var() - 1 / 12) < 3e-4
+    assert not np.array_equal(u, _native.uniforms(43, s, c, _native.RNG_PHILOX))
+    # Philox4x32-10 known answer (Random123 kat_vectors: counter 0, key 0)
+    z = _native.uniforms(0, np.zeros(2, dtype=np.uint64), np.arange(2, dtype=np.uint64), _native.RNG_PHILOX)
+    w = [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    want = [((((w[1] << 32) | w[0]) >> 11) * 2.0**-53), ((((w[3] << 32) | w[2]) >> 11) * 2.0**-53)]
+    assert list(z) == want
+
+
+def test_division_by_constant_is_ieee_exact():
+    rng = np.random.default_rng(5)
+    for g in (2, 3, 5, 6, 7, 9, 11, 12, 13, 17, 100, 1291):
+        x = np.concatenate([rng.random(200000) * g, rng.integers(0, g, 1000) + rng.random(1000),
+                            np.nextafter(np.arange(1.0, g + 1), 0), np.arange(0.0, g)])
+        assert np.array_equal(_native.debug_divide(x, g), x / g), g
+
+
+def test_transform_matches_reference_example():
+    x, jac, b = pb.transform(0.75, vegas.VegasGrid(1, 2, [[0.0, 0.8, 1.0]]))
+    assert abs(x[0] - 0.9) < 1e-15 and abs(jac - 0.4) < 1e-15 and b[0] == 1
+    grid = pb.refine_grid(pb.init_grid(3, 50), _peaked(3, 50))
+    y = np.random.default_rng(0).random((5000, 3))
+    gx, gj, gb = vegas.transform_many(y, grid)
+    ox, oj, ob = po.grid_transform(y, grid.boundaries)
+    assert np.array_equal(gx, ox) and np.array_equal(gj, oj) and np.array_equal(gb, ob)
+    with pytest.raises(ValueError):
+        vegas.transform_many(np.array([[0.1, 1.0, 0.2]]), grid)
+
+
+def _peaked(d, nb):
+    t = vegas.BinContributions(d, nb)
+    t.c[:] = np.linspace(0.0, 1.0, nb) ** 6
+    return t
+
+
+# ------------------------------------------------------------------ V-Sample vs the reference fixtures
+def test_vsample_matches_reference_fixtures(golden):
+    z, metas = golden["_mcubes"], golden["mcubes"]
+    for tag, meta in metas.items():
+        if tag in ("runs", "inj"):
+            continue
+        plan = pb.make_plan(meta["n"], meta["d"])
+        assert dict(g=plan.g, m=plan.m, p=plan.p, s=plan.s) == meta["plan"]
+        d = meta["d"]
+        grid = vegas.VegasGrid(d, 500, z[f"{meta['grid_from']}_B"]) if "grid_from" in meta else pb.init_grid(d)
+        res = pb.mcubes_kernel(_integrand(meta), plan, grid, seed=meta["seed"])
+        want_i, want_v = fromhex(meta["integral"]), fromhex(meta["variance"])
+        assert abs(res.integral - want_i) <= REL_SUM * abs(want_i), tag
+        assert abs(res.variance - want_v) <= 1e-10 * want_v, tag
+        want_c = z[f"{tag}_C"]
+        assert np.all(np.abs(res.contributions.c - want_c) <= REL_SUM * np.maximum(want_c, 1e-6 * want_c.max())), tag
+        assert res.clamp_events == meta["clamps"] and res.n_samples == meta["n_samples"]
+        new = pb.refine_grid(grid, res.contributions)
+        assert np.max(np.abs(new.boundaries - z[f"{tag}_B"])) <= 1e-12, tag
+        assert np.all(np.diff(new.boundaries, axis=1) > 0)
+
+
+def test_vsample_injected_sample_set(golden):
+    """north_star: 'a fixed injected sample set must reproduce the reference's sums to 1e-12 relative'."""
+    meta, z = golden["mcubes"]["inj"], golden["_mcubes"]
+    plan = pb.make_plan(meta["n"], meta["d"])
+    table = np.random.default_rng(meta["table_seed"]).random(plan.m * plan.p * plan.d)
+    res = pb.mcubes_kernel(pb.get_integrand(meta["family"], meta["d"]), plan, pb.init_grid(meta["d"]),
+                           injected_uniforms=table)
+    assert abs(res.integral - fromhex(meta["integral"])) <= REL_SUM * abs(fromhex(meta["integral"]))
+    assert abs(res.variance - fromhex(meta["variance"])) <= 1e-10 * fromhex(meta["variance"])
+    assert np.all(np.abs(res.contributions.c - z["inj_C"]) <= REL_SUM * np.maximum(z["inj_C"], 1e-6 * z["inj_C"].max()))
+
+
+@pytest.mark.parametrize("fam,d,n", [("sum", 2, 32), ("f2", 3, 5000), ("sum", 5, 100000), ("f2", 6, 300000), ("f2", 8, 40000),
+                                     ("sum", 1, 1000), ("f2", 10, 300000), ("sum", 12, 20000)])
+def test_vsample_sums_on_exact_families(fam, d, n, monkeypatch):
+    """Families without transcendentals see bit-identical samples and bit-identical per-cube (S1, S2,
+    estimate, variance): the only freedom left is summation order.  Per logical thread the reference
+    adds its cubes as first + numpy-pairwise(rest) (np.add.reduceat), the kernel serially; above that both
+    use the same pair trees.  Agreement is therefore a few ulp, far inside the 1e-12 bar; the clamp
+    counter (an integer classification) is identical."""
+    monkeypatch.setenv("PCB_MCUBES_SEGMENTS", "1")
+    plan, oplan = pb.make_plan(n, d), po.make_plan(n, d)
+    grid = pb.refine_grid(pb.init_grid(d), _peaked(d, 500))
+    res = pb.mcubes_kernel(pb.get_integrand(fam, d), plan, grid, seed=77)
+    want = po.vsample(fam, oplan, grid.boundaries, seed=77, workers=4)
+    assert abs(res.integral - want["integral"]) <= 1e-14 * abs(want["integral"])
+    assert abs(res.variance - want["variance"]) <= 1e-14 * want["variance"]
+    if plan.s <= 2:  # at most two cubes per thread: no association freedom at all
+        assert res.integral == want["integral"] and res.variance == want["variance"]
+    assert res.clamp_events == want["clamp_events"]
+    c = want["contributions"]
+    assert np.all(np.abs(res.contributions.c - c) <= REL_SUM * np.maximum(c, 1e-9 * c.max()))
+
+
+def test_vsample_segmented_matches_unsegmented(monkeypatch):
+    plan = pb.make_plan(2 * 10**6, 7)
+    f, grid = pb.get_integrand("f5", 7), pb.init_grid(7)
+    monkeypatch.setenv("PCB_MCUBES_SEGMENTS", "1")
+    a = pb.mcubes_kernel(f, plan, grid, seed=5)
+    monkeypatch.setenv("PCB_MCUBES_SEGMENTS", "5")
+    b = pb.mcubes_kernel(f, plan, grid, seed=5)
+    assert abs(a.integral - b.integral) <= 1e-14 * abs(a.integral) and abs(a.variance - b.variance) <= 1e-13 * a.variance
+    assert np.allclose(a.contributions.c, b.contributions.c, rtol=1e-13, atol=0)
+    assert a.clamp_events == b.clamp_events
+
+
+def test_vsample_unweighted_contributions():
+    plan = pb.make_plan(50000, 4)
+    grid = pb.refine_grid(pb.init_grid(4), _peaked(4, 500))
+    res = pb.mcubes_kernel(pb.get_integrand("f2", 4), plan, grid, seed=1, squared_weighted=False)
+    want = po.vsample("f2", po.make_plan(50000, 4), grid.boundaries, seed=1, squared_weighted=False)
+    c = want["contributions"]
+    assert np.all(np.abs(res.contributions.c - c) <= REL_SUM * np.maximum(c, 1e-9 * c.max()))
+
+
+def test_vsample_thread_shards_reassemble(monkeypatch):
+    """Multi-GPU contract: shards of logical threads (aligned to work-groups) produce per-group
+    partials whose pair tree equals the single-device result bit for bit, and tables that add up."""
+    monkeypatch.setenv("PCB_MCUBES_SEGMENTS", "1")
+    d, n = 5, 400000
+    plan = pb.make_plan(n, d)
+    grid = pb.init_grid(d)
+    spec = pb.get_integrand("f2", d).device_spec()
+    whole, c_whole, _ = _native.mcubes_sample(spec, plan, grid.boundaries, 9, want_group_partials=True)
+    cuts = [0, 3 * plan.group_size, 100 * plan.group_size, plan.n_threads]
+    parts, tables, clamps = [], [], 0
+    for t0, t1 in zip(cuts[:-1], cuts[1:]):
+        it, c, gp = _native.mcubes_sample(spec, plan, grid.boundaries, 9, thread_range=(t0, t1), want_group_partials=True)
+        parts.append(gp)
+        tables.append(c)
+        clamps += it.clamp_events
+    gp = np.concatenate(parts)
+    assert gp.shape[0] == plan.n_groups
+    assert po.tree_sum(gp[:, 0]) == whole.integral and max(po.tree_sum(gp[:, 1]), 0.0) == whole.variance
+    assert np.allclose(sum(tables), c_whole, rtol=1e-13, atol=0) and clamps == whole.clamp_events
+    with pytest.raises(ValueError):
+        _native.mcubes_sample(spec, plan, grid.boundaries, 9, thread_range=(5, 100))
+
+
+def test_vsample_non_finite_report():
+    f = pb.get_integrand("f2", 2)
+    f.a2 = 0.0
+    grid = pb.init_grid(2)
+    plan = pb.make_plan(64, 2)
+    table = np.random.default_rng(0).random(plan.m * plan.p * 2)
+    # sample 1 of sub-cube 9 lands exactly on x = (1/2, 1/2): cube 9 of a g=5 lattice is (1, 4) ... pick by search
+    g = plan.g
+    cube = (g // 2) * g + g // 2
+    table[(cube * plan.p + 1) * 2:(cube * plan.p + 1) * 2 + 2] = 0.5 * g - g // 2
+    with pytest.raises(pb.GroupTaskError) as info:
+        pb.mcubes_kernel(f, plan, grid, injected_uniforms=table)
+    assert isinstance(info.value.cause, pb.NonFiniteEvaluationError) and info.value.cause.region_index == cube
+
+
+def test_argument_errors():
+    with pytest.raises(ValueError):
+        pb.mcubes_kernel(pb.get_integrand("f2", 3), pb.make_plan(1000, 4), pb.init_grid(4))
+    with pytest.raises(ValueError):
+        pb.mcubes_run(pb.get_integrand("f2", 3), 1000, 3, 0)
+    with pytest.raises(ValueError):
+        pb.refine_grid(pb.init_grid(3), vegas.BinContributions(3, 100))
+
+
+# ------------------------------------------------------------------ refine_grid
+def test_refine_grid_peaked_fixture(golden):
+    z = golden["_mcubes"]
+    t = vegas.BinContributions(2, 500)
+    t.c[:] = z["peaked_C"]
+    new = pb.refine_grid(pb.init_grid(2), t)
+    assert np.max(np.abs(new.boundaries - z["peaked_B"])) <= 1e-12
+    assert np.all(np.diff(new.boundaries, axis=1) > 0) and new.boundaries[0, 0] == 0.0 and new.boundaries[0, -1] == 1.0
+    # untouched axis (all-zero contributions) keeps its boundaries (vegas_grid.py:156-157)
+    t.c[1] = 0.0
+    again = pb.refine_grid(pb.init_grid(2), t)
+    assert np.array_equal(again.boundaries[1], pb.init_grid(2).boundaries[1])
+
+
+@pytest.mark.parametrize("alpha,smoothing,nb", [(1.5, True, 500), (0.5, False, 500), (2.0, True, 64), (0.0, True, 17)])
+def test_refine_grid_against_oracle(alpha, smoothing, nb):
+    rng = np.random.default_rng(nb)
+    d = 4
+    t = vegas.BinContributions(d, nb)
+    t.c[:] = rng.random((d, nb)) ** 8 * 10.0 ** rng.integers(-3, 3, (d, 1))
+    grid = pb.init_grid(d, nb)
+    for _ in range(3):
+        new = pb.refine_grid(grid, t, pb.GridRefineParams(alpha, smoothing))
+        want = po.refine_grid(grid.boundaries, t.c, alpha, smoothing)
+        assert np.max(np.abs(new.boundaries - want)) <= 1e-12
+        grid = new
+
+
+# ------------------------------------------------------------------ run
+def test_run_matches_reference_fixtures(golden):
+    for run in golden["mcubes"]["runs"]:
+        recs = []
+        res = pb.mcubes_run(pb.get_integrand(run["family"], run["d"]), run["n"], run["d"], run["iterations"],
+                            seed=run["seed"], progress=recs.append)
+        want_est, want_err = fromhex(run["estimate"]), fromhex(run["errorest"])
+        # north_star bar: within 3 combined sigma; with identical draws the agreement is ~1e-10
+        assert abs(res.estimate - want_est) <= 3.0 * np.hypot(res.errorest, want_err)
+        assert abs(res.estimate - want_est) <= 1e-9 * abs(want_est), run
+        assert abs(res.errorest - want_err) <= 1e-8 * want_err
+        assert abs(res.chi2_per_dof - fromhex(run["chi2"])) <= 1e-6 * max(fromhex(run["chi2"]), 1e-12)
+        assert len(res.iterations) == run["iterations"] == len(recs)
+        for got, want in zip(recs, run["progress"]):
+            assert got["iteration"] == want["iteration"]
+            assert abs(got["iter_integral"] - fromhex(want["iter_integral"])) <= 1e-9 * abs(fromhex(want["iter_integral"]))
+            assert abs(got["estimate"] - fromhex(want["estimate"])) <= 1e-9 * abs(fromhex(want["estimate"]))
+        assert res.iterations[0].contributions.c.shape == (run["d"], 500)
+
+
+def test_run_reproduces_reference_misconvergence(golden):
+    """m-Cubes f4 d=8 n=1e6 seed 0 is ~26 sigma off with a huge chi2 -- reference
+    behaviour that a drop-in must reproduce, not fix."""
+    run = [r for r in golden["mcubes"]["runs"] if r["family"] == "f4" and r["d"] == 8][0]
+    res = pb.mcubes_run(pb.get_integrand("f4", 8), run["n"], 8, run["iterations"], seed=0)
+    truth = pb.reference_value("f4", 8).value
+    assert abs(res.estimate - truth) / res.errorest > 20 and res.chi2_per_dof > 1e4
+
+
+def test_run_tolerance_stop_config2():
+    """BASELINE config 2: f2 d=6 n=1e6 seed 0 first meets 1e-3 at iteration index 3 (4 iterations)."""
+    recs = []
+    res = pb.mcubes_run(pb.get_integrand("f2", 6), 10**6, 6, 15, seed=0, rel_tol=1e-3, progress=recs.append)
+    assert len(res.iterations) == 4 and recs[-1]["errorest"] <= 1e-3 * abs(recs[-1]["estimate"])
+    assert abs(res.estimate - 1.2875604971888545e13) <= 1e-9 * 1.2875604971888545e13
+
+
+def test_run_philox_within_three_sigma():
+    for fam, d in (("f2", 6), ("f3", 8), ("f5", 5)):
+        a = pb.mcubes_run(pb.get_integrand(fam, d), 10**6, d, 8, seed=1, rng="philox")
+        b = pb.mcubes_run(pb.get_integrand(fam, d), 10**6, d, 8, seed=1)
+        assert abs(a.estimate - b.estimate) <= 3.0 * np.hypot(a.errorest, b.errorest), fam
+        assert abs(a.estimate - pb.reference_value(fam, d).value) <= 5.0 * a.errorest
+
+
+def test_run_without_adaptation_keeps_uniform_grid():
+    res = pb.mcubes_run(pb.get_integrand("f5", 4), 50000, 4, 3, seed=2, adapt=False)
+    want = po.mcubes_run("f5", 50000, 4, 3, seed=2, adapt=False)
+    assert abs(res.estimate - want["estimate"]) <= 1e-10 * abs(want["estimate"])
+
+
+def test_constant_integrand_is_exact():
+    from paper_2302_05730_b200.genz import ConstantOne
+    res = pb.mcubes_kernel(ConstantOne(3), pb.make_plan(10000, 3), pb.init_grid(3))
+    assert abs(res.integral - 1.0) <= 1e-12 and res.variance <= 1e-24
