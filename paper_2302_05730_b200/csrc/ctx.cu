@@ -11,7 +11,7 @@ namespace pcb {
 #define PCB_DECL(F, _) \
   const void* eval_kernel_fam##F(int d); \
   const void* points_kernel_fam##F(int d); \
-  const void* vsample_kernel_fam##F(int d);
+  const void* vsample_kernel_fam##F(int d, int rng);
 PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5, ) PCB_DECL(6, ) PCB_DECL(7, )
 #undef PCB_DECL
 
@@ -19,12 +19,13 @@ static const kernel_getter kEval[PCB_N_FAMILIES] = {eval_kernel_fam0, eval_kerne
                                                     eval_kernel_fam4, eval_kernel_fam5, eval_kernel_fam6, eval_kernel_fam7};
 static const kernel_getter kPoints[PCB_N_FAMILIES] = {points_kernel_fam0, points_kernel_fam1, points_kernel_fam2, points_kernel_fam3,
                                                       points_kernel_fam4, points_kernel_fam5, points_kernel_fam6, points_kernel_fam7};
-static const kernel_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsample_kernel_fam1, vsample_kernel_fam2, vsample_kernel_fam3,
+typedef const void* (*sample_getter)(int d, int rng);
+static const sample_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsample_kernel_fam1, vsample_kernel_fam2, vsample_kernel_fam3,
                                                       vsample_kernel_fam4, vsample_kernel_fam5, vsample_kernel_fam6, vsample_kernel_fam7};
 
 const void* eval_kernel(int family, int d) { return kEval[family](d); }
 const void* points_kernel(int family, int d) { return kPoints[family](d); }
-const void* vsample_kernel_ptr(int family, int d) { return kSample[family](d); }
+const void* vsample_kernel_ptr(int family, int d, int rng) { return kSample[family](d, rng); }
 
 pcb_status validate_integrand(pcb_ctx* ctx, const pcb_integrand* f) {
   if (!f) return fail(ctx, PCB_INVALID, "integrand is NULL");

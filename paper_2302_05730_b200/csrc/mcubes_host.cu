@@ -42,7 +42,7 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
   if (avail < bounds_bytes + per_warp)
     return fail(ctx, PCB_INVALID, "d=%d, n_bins=%d needs %zu B of shared memory per CTA, device offers %zu", plan->d,
                 plan->n_bins, bounds_bytes + per_warp + 1024, ctx->smem_optin);
-  int warps = (int)std::min<size_t>((avail - bounds_bytes) / per_warp, 16);
+  int warps = (int)std::min<size_t>((avail - bounds_bytes) / per_warp, (size_t)vsample_max_warps(plan->d));
   const long long n_lw = (n_local_threads + 31) / 32;
   // tiny passes do not need every SM
   long long blocks = std::min<long long>(ctx->sm_count, std::max<long long>(1, (n_lw + warps - 1) / warps));
@@ -84,7 +84,7 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   const long long nt = t_end - t_begin;
   SampleLaunch L;
   PCB_TRY(plan_launch(ctx, plan, nt, &L));
-  const void* fn = vsample_kernel_ptr(f->family, d);
+  const void* fn = vsample_kernel_ptr(f->family, d, rng_kind);
   PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
 
   PCB_CUDA_TRY(ctx, ctx->mc_seg.ensure((size_t)nt * L.nseg * 2 * sizeof(double)));

@@ -11,11 +11,20 @@
 
 namespace pcb {
 
-const void* PCB_CAT(vsample_kernel_fam, PCB_FAM)(int d) {
-  switch (d) {
-#define X(D) case D: return (const void*)&vsample_kernel<PCB_FAM, D>;
-    PCB_DIMS(X)
+// rng 0: the reference counter hash (hot path); any other kind: generic kernel (Philox / injected table)
+const void* PCB_CAT(vsample_kernel_fam, PCB_FAM)(int d, int rng) {
+  if (rng == PCB_RNG_REFERENCE_HASH) {
+    switch (d) {
+#define X(D) case D: return (const void*)&vsample_kernel<PCB_FAM, D, PCB_RNG_REFERENCE_HASH>;
+      PCB_DIMS(X)
 #undef X
+    }
+  } else {
+    switch (d) {
+#define X(D) case D: return (const void*)&vsample_kernel<PCB_FAM, D, PCB_RNG_PHILOX>;
+      PCB_DIMS(X)
+#undef X
+    }
   }
   return nullptr;
 }

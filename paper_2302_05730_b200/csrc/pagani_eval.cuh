@@ -4,12 +4,18 @@
 //   1. tabulates, per axis, the integrand's per-axis term at the 7 distinct abscissae
 //      left + length*offset (quadrature.py:301-302; mul then add) -- 7*D terms instead of F*D;
 //   2. evaluates the F rule points: lane l plays the reference's virtual threads l and l+32 of
-//      the G=64 strided schedule (point indices t, t+G, ...; pagani.py:175-192), assembling each
-//      point's terms from the table in numpy's combine order;
+//      the G-wide strided schedule (point indices t, t+G, ...; pagani.py:175-192).  A point's
+//      terms are gathered from the table and combined in numpy's order:
+//        * centre/axial/pair points through a per-point code word (one byte per axis = byte offset
+//          of the abscissa candidate), built once per CTA;
+//        * corner points straight from the point's bit pattern; with G = 64 the low six bits are
+//          constant per virtual thread, so the partial combine over axes 0..5 is hoisted out of
+//          the step loop;
 //   3. reduces the 2x5 partial sums with a reduce-scatter butterfly whose add tree is exactly the
 //      adjacent-pair tree of engine.tree_sum over 64 virtual threads (xor 1,2,4,8,16, then A+B);
 //   4. scales by the volume, forms the error estimate (pagani.py:104-132) and the split axis
 //      (pagani.py:215-223, first maximum wins).
+// The next region's geometry is prefetched while the current one is evaluated.
 #pragma once
 
 #include "pcb_device.cuh"
@@ -102,16 +108,73 @@ __device__ __forceinline__ void schedule_tree(const double (&a)[5], const double
   out[4] = shfl_idx_d(c1, 2);
 }
 
+// term table row of axis j starts at byte j*64; candidate c sits at byte offset c*8
+template <int D>
+__device__ __forceinline__ double term_at(const char* table, int j, unsigned byte_off) {
+  return *reinterpret_cast<const double*>(table + j * 64 + byte_off);
+}
+
+// ---- corner points: combine over all axes, split into a hoistable part (axes < LO) and the rest.
+// The split reproduces numpy's association exactly for every combine kind.
+template <class F, int D, int LO>
+struct CornerCombine {
+  // partial state after the first LO axes
+  double p0, p1;  // seq kinds: p0 = t0 (+) ... (+) t_{LO-1};  numpy-sum with D >= 8 and LO == 6: p0 = (a0+a1)+(a2+a3), p1 = a4+a5
+  __device__ __forceinline__ void head(const char* table, unsigned bits) {
+    double t[LO > 0 ? LO : 1];
+#pragma unroll
+    for (int j = 0; j < LO; ++j) t[j] = term_at<D>(table, j, 40u + ((bits >> j) & 1u) * 8u);
+    if constexpr (LO == 0) {
+      p0 = 0.0; p1 = 0.0;
+    } else if constexpr (F::combine == kSumNumpy && D >= 8) {
+      static_assert(LO == 6 || LO == 0, "hoisting is laid out for six lane-constant axes");
+      p0 = (t[0] + t[1]) + (t[2] + t[3]);
+      p1 = t[4] + t[5];
+    } else {
+      double s = t[0];
+#pragma unroll
+      for (int j = 1; j < LO; ++j) s = (F::combine == kProdSeq) ? s * t[j] : s + t[j];
+      p0 = s; p1 = 0.0;
+    }
+  }
+  __device__ __forceinline__ double tail(const char* table, unsigned bits) const {
+    if constexpr (LO == 0) {
+      double t[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) t[j] = term_at<D>(table, j, 40u + ((bits >> j) & 1u) * 8u);
+      return combine_terms<F, D>(t);
+    } else if constexpr (F::combine == kSumNumpy && D >= 8) {
+      const double a6 = term_at<D>(table, 6, 40u + ((bits >> 6) & 1u) * 8u);
+      const double a7 = term_at<D>(table, 7, 40u + ((bits >> 7) & 1u) * 8u);
+      double s = p0 + (p1 + (a6 + a7));
+#pragma unroll
+      for (int j = 8; j < D; ++j) s = s + term_at<D>(table, j, 40u + ((bits >> j) & 1u) * 8u);
+      return s;
+    } else {
+      double s = p0;
+#pragma unroll
+      for (int j = LO; j < D; ++j) {
+        const double t = term_at<D>(table, j, 40u + ((bits >> j) & 1u) * 8u);
+        s = (F::combine == kProdSeq) ? s * t : s + t;
+      }
+      return s;
+    }
+  }
+};
+
 template <int FAM, int D>
 __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
-  constexpr int kStore = 4 * D + 1;           // f(centre), f(+-l2 e_j), f(+-l3 e_j): split-axis inputs
-  constexpr int kPairs = D * (D - 1) / 2;
-  __shared__ double s_term[kEvalWarps][D * 8];
+  constexpr int kStore = 4 * D + 1;            // f(centre), f(+-l2 e_j), f(+-l3 e_j): split-axis inputs
+  constexpr int kCorner0 = 2 * D * D + 2 * D + 1;  // first corner point
+  constexpr int kWords = (D + 7) / 8;          // 64-bit code words per non-corner point
+  constexpr int kLo = D < 6 ? D : 6;           // axes whose corner bit is fixed per virtual thread when G = 64
+  __shared__ __align__(16) double s_term[kEvalWarps][D * 8];
   __shared__ double s_store[kEvalWarps][kStore + 1];
-  __shared__ double s_w[6][5];                 // orbit weights; rows 4/5 = corners with even/odd bit count
+  __shared__ double s_geo[kEvalWarps][2][2 * D];   // double-buffered left[0..D), length[0..D)
+  __shared__ __align__(16) double s_w[6][6];   // orbit weights (+pad); rows 4/5 = corners with even/odd bit count
   __shared__ double s_off[8];
-  __shared__ unsigned char s_pair[kPairs > 0 ? kPairs : 1][2];
+  __shared__ unsigned long long s_code[kCorner0][kWords];  // byte j: candidate byte offset on axis j; bits 6-7 of byte 0: orbit
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const pcb_rule& rule = args.rule;
@@ -122,36 +185,62 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
     s_w[o][k] = w;
   }
   if (threadIdx.x < 7) s_off[threadIdx.x] = rule.offsets[threadIdx.x];
-  if (threadIdx.x == 0) {
-    int q = 0;
-    for (int j = 0; j < D; ++j)
-      for (int k = j + 1; k < D; ++k) { s_pair[q][0] = j; s_pair[q][1] = k; ++q; }
+  for (int i = threadIdx.x; i < kCorner0; i += blockDim.x) {
+    // decode point i (centre | +-l2 e_j | +-l3 e_j | l4 pairs) once per CTA
+    int a = -1, b = -1, ca = 0, cb = 0, orbit = 0;
+    if (i == 0) {
+    } else if (i <= 2 * D) {
+      int q = i - 1; a = q >> 1; ca = 1 + (q & 1); orbit = 1;
+    } else if (i <= 4 * D) {
+      int q = i - 1 - 2 * D; a = q >> 1; ca = 3 + (q & 1); orbit = 2;
+    } else {
+      int q = i - 1 - 4 * D, pr = q >> 2, sg = q & 3, idx = 0;
+      for (int j = 0; j < D; ++j)
+        for (int k = j + 1; k < D; ++k, ++idx)
+          if (idx == pr) { a = j; b = k; }
+      ca = 3 + (sg & 1); cb = 3 + (sg >> 1); orbit = 3;
+    }
+    unsigned long long w[kWords];
+    for (int q = 0; q < kWords; ++q) w[q] = 0;
+    if (a >= 0) w[a >> 3] |= (unsigned long long)(ca * 8) << (8 * (a & 7));
+    if (b >= 0) w[b >> 3] |= (unsigned long long)(cb * 8) << (8 * (b & 7));
+    w[0] |= (unsigned long long)orbit << 6;
+    for (int q = 0; q < kWords; ++q) s_code[i][q] = w[q];
   }
   __syncthreads();
 
   const int fe = rule.f_eval, G = args.group;
-  const int corner0 = fe - (1 << D);
-  const int steps = (fe + G - 1) / G;
+  const char* term_b = reinterpret_cast<const char*>(s_term[wib]);
   double* term = s_term[wib];
   double* store = s_store[wib];
-  const long long ld = args.ld;
+  const long long ld = args.ld, stride = (long long)gridDim.x * kEvalWarps;
+  long long r = (long long)blockIdx.x * kEvalWarps + wib;
+  int buf = 0;
+  // geometry of the first region
+  if (r < args.n && lane < 2 * D)
+    s_geo[wib][0][lane] = (lane < D) ? args.lefts[lane * ld + r] : args.lengths[(lane - D) * ld + r];
+  __syncwarp();
 
-  for (long long r = (long long)blockIdx.x * kEvalWarps + wib; r < args.n; r += (long long)gridDim.x * kEvalWarps) {
+  for (; r < args.n; r += stride, buf ^= 1) {
+    const double* geo = s_geo[wib][buf];
+    // prefetch the next region's geometry (consumed at the bottom of the loop)
+    const long long rn = r + stride;
+    double next_geo = 0.0;
+    if (rn < args.n && lane < 2 * D) next_geo = (lane < D) ? args.lefts[lane * ld + rn] : args.lengths[(lane - D) * ld + rn];
+
     // ---- 1. per-axis term table at the 7 distinct abscissae
-    for (int e = lane; e < 8 * D; e += 32) {
-      int j = e >> 3, c = e & 7;
-      if (c < 7) {
-        double x = args.lefts[j * ld + r] + args.lengths[j * ld + r] * s_off[c];
+#pragma unroll
+    for (int e0 = 0; e0 < 8 * D; e0 += 32) {
+      const int e = e0 + lane, j = e >> 3, c = e & 7;
+      if (e < 8 * D && c < 7) {
+        const double x = geo[j] + geo[D + j] * s_off[c];
         term[e] = axis_term<F>(j, x, args.f);
       }
     }
-    double vol = args.lengths[r];
+    double vol = geo[D];
 #pragma unroll
-    for (int j = 1; j < D; ++j) vol = vol * args.lengths[j * ld + r];  // np.prod, left to right
+    for (int j = 1; j < D; ++j) vol = vol * geo[D + j];  // np.prod, left to right
     __syncwarp();
-    double t0[D];
-#pragma unroll
-    for (int j = 0; j < D; ++j) t0[j] = term[j * 8];
 
     // ---- 2. rule points of my two virtual threads
     double acc[2][5];
@@ -161,48 +250,67 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
       for (int k = 0; k < 5; ++k) acc[set][k] = 0.0;
       const int vt = lane + 32 * set;
       if (vt >= G) continue;
-      for (int s = 0; s < steps; ++s) {
-        const int i = vt + G * s;
-        if (i >= fe) break;
+      int i = vt;
+      bool first = true;
+      // centre, axial and pair points
+      for (; i < kCorner0; i += G) {
+        unsigned long long code[kWords];
+#pragma unroll
+        for (int q = 0; q < kWords; ++q) code[q] = s_code[i][q];
+        const int orbit = (int)((unsigned)code[0] >> 6) & 3;
+        code[0] &= ~0xC0ULL;
         double t[D];
-        int orbit;
-        if (i < corner0) {
-          int a = -1, b = -1;
-          double va = 0.0, vb = 0.0;
-          if (i == 0) {
-            orbit = 0;
-          } else if (i <= 2 * D) {
-            int q = i - 1;
-            a = q >> 1; va = term[a * 8 + 1 + (q & 1)]; orbit = 1;
-          } else if (i <= 4 * D) {
-            int q = i - 1 - 2 * D;
-            a = q >> 1; va = term[a * 8 + 3 + (q & 1)]; orbit = 2;
-          } else {
-            int q = i - 1 - 4 * D;
-            int pr = q >> 2, sg = q & 3;
-            a = s_pair[pr][0]; b = s_pair[pr][1];
-            va = term[a * 8 + 3 + (sg & 1)];
-            vb = term[b * 8 + 3 + (sg >> 1)];
-            orbit = 3;
-          }
 #pragma unroll
-          for (int j = 0; j < D; ++j) t[j] = (j == a) ? va : ((j == b) ? vb : t0[j]);
-        } else {
-          const int bits = i - corner0;
-#pragma unroll
-          for (int j = 0; j < D; ++j) t[j] = term[j * 8 + 5 + ((bits >> j) & 1)];
-          orbit = 4 + (__popc(bits) & 1);
+        for (int j = 0; j < D; ++j) {
+          const unsigned half = (unsigned)(code[j >> 3] >> (32 * ((j >> 2) & 1)));
+          t[j] = term_at<D>(term_b, j, __byte_perm(half, 0, 0x4440 + (j & 3)));
         }
         const double fx = finish_value<F, D>(combine_terms<F, D>(t), args.f);
         if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
         if (i < kStore) store[i] = fx;
         const double* w = s_w[orbit];
-        if (s == 0) {
+        if (first) {
 #pragma unroll
           for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
+          first = false;
         } else {
 #pragma unroll
           for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+        }
+      }
+      // corner points: bit j of (i - kCorner0) set => abscissa candidate 6 (minus), else 5 (plus)
+      if (G == 64) {
+        CornerCombine<F, D, kLo> cc;
+        if (i < fe) cc.head(term_b, (unsigned)(i - kCorner0));
+        for (; i < fe; i += 64) {
+          const unsigned bits = (unsigned)(i - kCorner0);
+          const double fx = finish_value<F, D>(cc.tail(term_b, bits), args.f);
+          if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+          const double* w = s_w[4 + (__popc(bits) & 1)];
+          if (first) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
+            first = false;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+          }
+        }
+      } else {
+        CornerCombine<F, D, 0> cc;
+        for (; i < fe; i += G) {
+          const unsigned bits = (unsigned)(i - kCorner0);
+          const double fx = finish_value<F, D>(cc.tail(term_b, bits), args.f);
+          if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+          const double* w = s_w[4 + (__popc(bits) & 1)];
+          if (first) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
+            first = false;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+          }
         }
       }
     }
@@ -237,6 +345,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
       args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
       args.split_axes[r] = axis;
     }
+    if (lane < 2 * D) s_geo[wib][buf ^ 1][lane] = next_geo;
     __syncwarp();
   }
 }

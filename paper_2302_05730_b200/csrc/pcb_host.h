@@ -95,7 +95,7 @@ inline pcb_status fail(pcb_ctx* ctx, pcb_status code, const char* fmt, ...) {
 typedef const void* (*kernel_getter)(int d);
 const void* eval_kernel(int family, int d);
 const void* points_kernel(int family, int d);
-const void* vsample_kernel_ptr(int family, int d);
+const void* vsample_kernel_ptr(int family, int d, int rng);
 
 // bracket one dominant-kernel launch with events when profiling is on
 struct ProfileSpan {

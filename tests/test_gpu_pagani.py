@@ -43,7 +43,7 @@ def _integrand(meta):
     return f
 
 
-def _check_regions(tag, fam, got, want_i, want_e, want_k, exact):
+def _check_regions(tag, fam, got, want_i, want_e, want_k, exact, volumes=None):
     if exact:
         assert np.array_equal(got.integrals, want_i), tag
         assert np.array_equal(got.errors, want_e), tag
@@ -52,6 +52,9 @@ def _check_regions(tag, fam, got, want_i, want_e, want_k, exact):
     # 1e-12 relative to the region's own scale: |I| or, for sign-changing integrands whose I cancels,
     # the largest |I| of a congruent region in the batch
     scale = np.maximum(np.abs(want_i), 1e-3 * np.max(np.abs(want_i)))
+    if fam == "f1" and volumes is not None:
+        # oscillatory: I cancels inside a region; the natural scale is volume * max|f| = volume
+        scale = np.maximum(np.abs(want_i), volumes)
     assert np.all(np.abs(got.integrals - want_i) <= REL_I * scale), (tag, np.max(np.abs(got.integrals - want_i) / scale))
     # the null-rule sums cancel to ~1e-3..1e-10 of |I|; compare E where it is resolved
     resolved = want_e > 1e-7 * np.abs(want_i)
@@ -97,7 +100,8 @@ def test_evaluate_matches_reference_fixtures(golden):
         got = pb.pagani_kernel(_integrand(meta), pb.RegionList(lefts, lengths), pb.build_rule(d), None, cfg)
         assert got.split_axes.dtype == np.int64 and not got.integrals.flags.writeable
         exact = meta["family"] in EXACT and "low" not in meta
-        _check_regions(tag, meta["family"], got, z[f"{tag}_I"], z[f"{tag}_E"], z[f"{tag}_K"].astype(np.int64), exact)
+        _check_regions(tag, meta["family"], got, z[f"{tag}_I"], z[f"{tag}_E"], z[f"{tag}_K"].astype(np.int64), exact,
+                       volumes=np.prod(lengths, axis=1))
         if not exact:
             # split axis: identical wherever the reference's own indicator is not a numerical tie
             same = got.split_axes == z[f"{tag}_K"]
