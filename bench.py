@@ -269,6 +269,7 @@ def main():
         region_s = time.perf_counter() - t_region
     kind = 0 if w["kind"] == "pagani" else 1
     k_ms, k_launches, k_units = ctx.profile_end(kind)
+    bin_ms, bin_launches, _ = ctx.profile_end(2) if kind == 1 else (0.0, 0, 0.0)
     launches = ctx.launch_count() - launches0
 
     # max over ranks of the timed durations (device seconds and API wall-clock)
@@ -296,6 +297,7 @@ def main():
                      "traffic": None, "launches": int(k_launches), "avg_launch_ms": k_ms / max(k_launches, 1),
                      "flops_per_eval": fpe, "evals_per_launch": k_units * evals_per_unit / max(k_launches, 1),
                      "kernel_share_of_step": k_ms * 1e-3 / dev_s if dev_s else None,
+                     "bin_kernel_avg_launch_ms": bin_ms / max(bin_launches, 1) if kind == 1 else None,
                      "peak_source": "DFMA micro-benchmark run live (MEASURED_PEAKS.json has no FP64 entry; nominal 37 TFLOP/s)"},
         "clocks": clocks.summary(),
         "timed_region_s": region_s,

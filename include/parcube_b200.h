@@ -184,8 +184,8 @@ pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops);
 
 /* ---- per-kernel timing for the roofline report -------------------------------------------
  * Between begin and end every launch of the two dominant kernels (PAGANI evaluate, m-Cubes
- * V-Sample) is bracketed by CUDA events on the launching stream.  `kind` 0 = evaluate (units =
- * regions), 1 = V-Sample (units = samples).  end() synchronises and returns the sums.          */
+ * V-Sample and its bin accumulation) is bracketed by CUDA events on the launching stream.  `kind` 0 =
+ * evaluate (units = regions), 1 = V-Sample (units = samples), 2 = bin accumulation (units = records).  end() synchronises and returns the sums.          */
 pcb_status pcb_profile_begin(pcb_ctx* ctx);
 pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_t* launches, double* units);
 

@@ -72,6 +72,7 @@ pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out) {
                 device_ordinal, prop.name, prop.major, prop.minor);
   ctx->sm_count = prop.multiProcessorCount;
   ctx->smem_optin = prop.sharedMemPerBlockOptin;
+  ctx->total_mem = prop.totalGlobalMem;
   int khz = 0;
   cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device_ordinal);
   ctx->clock_khz = khz;
@@ -90,7 +91,7 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
     cudaStreamDestroy(ctx->stream);
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 3; ++k)
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
   for (auto& sp : ctx->span_pool) {
     cudaEventDestroy(sp.a);
@@ -141,7 +142,7 @@ pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops) {
 
 pcb_status pcb_profile_begin(pcb_ctx* ctx) {
   if (!ctx) return PCB_INVALID;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
     ctx->spans[k].clear();
     ctx->span_units[k] = 0;
@@ -151,7 +152,7 @@ pcb_status pcb_profile_begin(pcb_ctx* ctx) {
 }
 
 pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_t* launches, double* units) {
-  if (!ctx || kind < 0 || kind > 1) return PCB_INVALID;
+  if (!ctx || kind < 0 || kind > 2) return PCB_INVALID;
   ctx->profiling = false;
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

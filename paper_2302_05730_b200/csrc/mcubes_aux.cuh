@@ -2,9 +2,79 @@
 // grid refinement (reference: mcubes.py:255-265, 292-298; vegas_grid.py:133-193).
 #pragma once
 
+#include "mcubes_kernels.cuh"
 #include "pcb_device.cuh"
 
 namespace pcb {
+
+// Accumulate sample records into the contribution table.  Each warp serves ONE axis: its private
+// table is a single row (n_bins doubles + n_bins tag bytes, 4.5 KB at 500 bins), so a CTA holds
+// d x R warps (up to 32) and the SM's latency is hidden by occupancy instead of by a 36 KB table per
+// warp.  The d warps of a stream read the same records (L1/L2 hits on the contributions), two
+// records per lane and round.  Tables are merged stream -> CTA here, CTA -> grid by merge_hist_kernel.
+__global__ void __launch_bounds__(1024) bin_kernel(const __grid_constant__ BinArgs a, int d, int streams) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nb = a.nb;
+  const int W = blockDim.x >> 5;                                  // = d * streams
+  double* s_hist = reinterpret_cast<double*>(smem_raw);           // [W][nb]
+  unsigned char* s_tag = reinterpret_cast<unsigned char*>(s_hist + (size_t)W * nb);  // [W][nb]
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int axis = wib % d, stream = wib / d;
+  for (int i = threadIdx.x; i < W * nb; i += blockDim.x) s_hist[i] = 0.0;
+  __syncthreads();
+  double* __restrict__ hist = s_hist + (size_t)wib * nb;
+  unsigned char* __restrict__ tags = s_tag + (size_t)wib * nb;
+  const unsigned short* __restrict__ bins = a.rec_b + (long long)axis * a.rec_capacity;
+
+  const long long n_pairs = (a.n_groups + 1) / 2, step = (long long)gridDim.x * streams;
+  long long pr = (long long)blockIdx.x * streams + stream;
+  auto fetch = [&](long long q, double (&w)[2], int (&b)[2]) {
+    const long long r0 = q * 64 + lane, r1 = r0 + 32;
+    const bool has0 = q < n_pairs, has1 = has0 && 2 * q + 1 < a.n_groups;
+    w[0] = has0 ? a.rec_w[r0] : 0.0;
+    w[1] = has1 ? a.rec_w[r1] : 0.0;
+    b[0] = has0 ? bins[r0] : 0;
+    b[1] = has1 ? bins[r1] : 0;
+  };
+  double w[2], wn[2];
+  int b[2], bn[2];
+  fetch(pr, w, b);
+  for (; pr < n_pairs; pr += step) {
+    fetch(pr + step, wn, bn);
+    // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
+    // two records of one lane in the same bin become one update
+    const bool same = b[0] == b[1];
+    const double add0 = same ? w[0] + w[1] : w[0], add1 = w[1];
+    unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
+    for (int round = 0; round < 2 && __any_sync(PCB_FULL_MASK, want); ++round) {
+      if (want & 1u) tags[b[0]] = (unsigned char)lane;
+      if (want & 2u) tags[b[1]] = (unsigned char)lane;
+      __syncwarp();
+      const unsigned char t0 = tags[b[0]], t1 = tags[b[1]];
+      const double o0 = hist[b[0]], o1 = hist[b[1]];
+      const bool win0 = (want & 1u) && t0 == lane, win1 = (want & 2u) && t1 == lane;
+      if (win0) hist[b[0]] = o0 + add0;
+      if (win1) hist[b[1]] = o1 + add1;
+      want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
+      __syncwarp();
+    }
+    if (__any_sync(PCB_FULL_MASK, want)) {  // triple collisions: shared-memory CAS atomic
+      if (want & 1u) atomicAdd(hist + b[0], add0);
+      if (want & 2u) atomicAdd(hist + b[1], add1);
+      __syncwarp();
+    }
+    w[0] = wn[0]; w[1] = wn[1]; b[0] = bn[0]; b[1] = bn[1];
+  }
+  __syncthreads();
+  double* dst = a.block_hist + (size_t)blockIdx.x * d * nb;
+  for (int i = threadIdx.x; i < d * nb; i += blockDim.x) {
+    const int j = i / nb, k = i - j * nb;
+    double t = s_hist[(size_t)j * nb + k];
+    for (int q = 1; q < streams; ++q) t = t + s_hist[(size_t)(q * d + j) * nb + k];
+    dst[i] = a.accumulate ? dst[i] + t : t;
+  }
+}
+
 
 // CTA tables -> contribution table, fixed CTA order
 __global__ void merge_hist_kernel(const double* __restrict__ block_hist, int nblocks, int nbins_total, double* __restrict__ out) {

@@ -16,11 +16,12 @@ enum { M_BAD = 0, M_CLAMPS = 1, M_INTEGRAL = 2, M_VARIANCE = 3 };  // slots in c
 constexpr int kMcSlot = 40;
 
 struct SampleLaunch {
-  int warps = 0;
-  int blocks = 0;
-  size_t smem = 0;
+  int blocks = 0;        // sampling CTAs (kSampleWarps warps each)
+  size_t smem = 0;       // boundaries table
   int nseg = 1;
   long long seg_len = 0;
+  int bin_warps = 0;     // warps per accumulation CTA (one private table each)
+  size_t bin_smem = 0;
 };
 
 static pcb_status validate_plan(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan) {
@@ -32,33 +33,35 @@ static pcb_status validate_plan(pcb_ctx* ctx, const pcb_integrand* f, const pcb_
   for (int j = 0; j < plan->d; ++j) m *= plan->g;
   if (m != (long double)plan->m) return fail(ctx, PCB_INVALID, "m must equal g^d");
   if (plan->group_size > 4096) return fail(ctx, PCB_INVALID, "group_size %d > 4096 unsupported", plan->group_size);
+  if (plan->n_bins > 65535) return fail(ctx, PCB_INVALID, "n_bins %d > 65535 unsupported (16-bit bin ids)", plan->n_bins);
   return PCB_OK;
 }
 
 static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long long n_local_threads, SampleLaunch* out) {
   const size_t bounds_bytes = (size_t)plan->d * (plan->n_bins + 1) * sizeof(double);
-  const size_t per_warp = (size_t)plan->d * plan->n_bins * (sizeof(double) + 1);
+  const size_t per_warp = (size_t)plan->n_bins * (sizeof(double) + 1);  // one axis row + its tag bytes
   const size_t avail = ctx->smem_optin > 1024 ? ctx->smem_optin - 1024 : 0;
-  if (avail < bounds_bytes + per_warp)
+  if (avail < bounds_bytes || avail < per_warp * plan->d)
     return fail(ctx, PCB_INVALID, "d=%d, n_bins=%d needs %zu B of shared memory per CTA, device offers %zu", plan->d,
-                plan->n_bins, bounds_bytes + per_warp + 1024, ctx->smem_optin);
-  int warps = (int)std::min<size_t>((avail - bounds_bytes) / per_warp, (size_t)vsample_max_warps(plan->d));
+                plan->n_bins, std::max(bounds_bytes, per_warp * plan->d) + 1024, ctx->smem_optin);
   const long long n_lw = (n_local_threads + 31) / 32;
-  // tiny passes do not need every SM
-  long long blocks = std::min<long long>(ctx->sm_count, std::max<long long>(1, (n_lw + warps - 1) / warps));
-  out->warps = warps;
-  out->blocks = (int)blocks;
-  out->smem = bounds_bytes + (size_t)warps * per_warp + 16;
-  const long long phys = blocks * warps;
-  int nseg = 1;
-  if (n_lw < 4 * phys) nseg = (int)std::min<long long>(plan->s, (6 * phys + n_lw - 1) / n_lw);
+  out->smem = bounds_bytes;
+  // accumulation CTA: d warps (one per axis) per record stream, as many streams as fit in 32 warps / shared memory
+  const int streams = (int)std::max<size_t>(1, std::min<size_t>(32 / plan->d, avail / (per_warp * plan->d)));
+  out->bin_warps = streams * plan->d;
+  out->bin_smem = (size_t)out->bin_warps * per_warp + 16;
+  // work units = logical warps x segments; aim at >= 8 units per resident warp for balance
+  const long long resident = 2LL * ctx->sm_count * kSampleWarps;
+  int nseg = (int)std::max<long long>(1, std::min<long long>(plan->s, (8 * resident + n_lw - 1) / n_lw));
   if (const char* env = std::getenv("PCB_MCUBES_SEGMENTS")) {
     int v = std::atoi(env);
     if (v >= 1) nseg = (int)std::min<long long>(plan->s, v);
   }
-  long long seg_len = (plan->s + nseg - 1) / nseg;
+  const long long seg_len = (plan->s + nseg - 1) / nseg;
   out->seg_len = seg_len;
   out->nseg = (int)((plan->s + seg_len - 1) / seg_len);
+  const long long units = n_lw * out->nseg;
+  out->blocks = (int)std::max<long long>(1, std::min<long long>(2LL * ctx->sm_count, (units + kSampleWarps - 1) / kSampleWarps));
   return PCB_OK;
 }
 
@@ -85,10 +88,30 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   SampleLaunch L;
   PCB_TRY(plan_launch(ctx, plan, nt, &L));
   const void* fn = vsample_kernel_ptr(f->family, d, rng_kind);
-  PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem));
+  const void* bin_fn = (const void*)&bin_kernel;
+  for (auto kv : {std::make_pair(fn, L.smem), std::make_pair(bin_fn, L.bin_smem)}) {
+    size_t& have = ctx->smem_attr[kv.first];  // cudaFuncSetAttribute is not free: once per kernel and size
+    if (have < kv.second) {
+      PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(kv.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.second));
+      have = kv.second;
+    }
+  }
 
+  // record buffer: one contribution (8 B) + d bin ids (2 B each) per sample slot, chunked over work units
+  const long long n_lw = (nt + 31) / 32, units = n_lw * L.nseg;
+  const long long rec_per_unit = L.seg_len * plan->p * 32;
+  const size_t rec_bytes = 8 + 2 * (size_t)d;
+  size_t budget = (size_t)24 << 30;
+  if (const char* env = std::getenv("PCB_MCUBES_RECORD_BYTES")) budget = (size_t)std::max(1LL, std::atoll(env));
+  budget = std::min(budget, (size_t)(ctx->total_mem * 0.4));
+  long long chunk_units = (long long)std::max<size_t>(1, budget / ((size_t)rec_per_unit * rec_bytes));
+  chunk_units = std::min(chunk_units, units);
+  const long long rec_capacity = round_up(chunk_units * rec_per_unit, 64);
+  PCB_CUDA_TRY(ctx, ctx->mc_rec.ensure((size_t)rec_capacity * rec_bytes));
+
+  const int bin_blocks = ctx->sm_count;
   PCB_CUDA_TRY(ctx, ctx->mc_seg.ensure((size_t)nt * L.nseg * 2 * sizeof(double)));
-  PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)L.blocks * d * nb * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)bin_blocks * d * nb * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure((size_t)d * nb * sizeof(double)));
   const long long n_groups = (nt + plan->group_size - 1) / plan->group_size;
   PCB_CUDA_TRY(ctx, ctx->mc_group.ensure((size_t)n_groups * 4 * sizeof(double)));
@@ -103,7 +126,7 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   a.m = plan->m; a.s = plan->s;
   a.n_threads = n_threads;
   a.t_begin = t_begin; a.t_end = t_end;
-  a.n_lw = (nt + 31) / 32;
+  a.n_lw = n_lw;
   a.nseg = L.nseg;
   a.rng_kind = rng_kind;
   a.seg_len = L.seg_len;
@@ -123,15 +146,43 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   a.seg_partials = ctx->mc_seg.as<double>();
   a.clamps = sc_u + M_CLAMPS;
   a.bad = sc_u + M_BAD;
-  a.block_hist = ctx->mc_hist.as<double>();
-  void* args[] = {&a};
-  {
-    const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
-    ProfileSpan span(ctx, 1, (double)(c1 - c0) * plan->p);
-    PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(L.blocks), dim3(L.warps * 32), args, L.smem, ctx->stream));
-    ctx->launches++;
+  a.rec_per_unit = rec_per_unit;
+  a.rec_capacity = rec_capacity;
+  a.rec_w = ctx->mc_rec.as<double>();
+  a.rec_b = reinterpret_cast<unsigned short*>(ctx->mc_rec.as<double>() + rec_capacity);
+
+  BinArgs b;
+  b.nb = nb;
+  b.rec_capacity = rec_capacity;
+  b.rec_w = a.rec_w;
+  b.rec_b = a.rec_b;
+  b.block_hist = ctx->mc_hist.as<double>();
+
+  for (long long u0 = 0, chunk = 0; u0 < units; u0 += chunk_units, ++chunk) {
+    a.unit_begin = u0;
+    a.unit_end = std::min(units, u0 + chunk_units);
+    const long long n_units = a.unit_end - a.unit_begin;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(L.blocks, (n_units + kSampleWarps - 1) / kSampleWarps));
+    void* args[] = {&a};
+    {
+      // units of work for the roofline: the samples actually drawn (active lanes) in this chunk
+      const double frac = (double)n_units / (double)units;
+      const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
+      ProfileSpan span(ctx, 1, frac * (double)(c1 - c0) * plan->p);
+      PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
+      ctx->launches++;
+    }
+    b.n_groups = n_units * rec_per_unit / 32;
+    b.accumulate = chunk > 0;
+    int d_arg = d, streams_arg = L.bin_warps / d;
+    void* bargs[] = {&b, &d_arg, &streams_arg};
+    {
+      ProfileSpan span(ctx, 2, (double)b.n_groups * 32.0);
+      PCB_CUDA_TRY(ctx, cudaLaunchKernel(bin_fn, dim3(bin_blocks), dim3(L.bin_warps * 32), bargs, L.bin_smem, ctx->stream));
+      ctx->launches++;
+    }
   }
-  merge_hist_kernel<<<(d * nb + 255) / 256, 256, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), L.blocks, d * nb,
+  merge_hist_kernel<<<(d * nb + 255) / 256, 256, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), bin_blocks, d * nb,
                                                                      ctx->mc_contrib.as<double>());
   int pow2 = 1;
   while (pow2 < plan->group_size) pow2 <<= 1;

@@ -1,16 +1,22 @@
-// m-Cubes V-Sample and grid refinement on the device (reference: mcubes.py:210-308,
-// vegas_grid.py:99-193; arithmetic restated in SURVEY.md appendix A.4).
+// m-Cubes V-Sample on the device (reference: mcubes.py:210-308, vegas_grid.py:99-114; arithmetic
+// restated in SURVEY.md appendix A.4).
 //
 // Work decomposition: the reference's logical thread T owns sub-cubes [T*s, (T+1)*s) and RNG
 // stream T.  A physical warp processes 32 logical threads at a time (lane <-> logical thread,
-// lanes strided far apart in T so their sub-cubes sit in different grid bands), optionally only
-// a segment of each thread's cube range (load balance for huge s).  Every draw is
+// lanes strided far apart in T so their sub-cubes sit in different grid bands), a segment of each
+// thread's cube range per work unit (load balance for huge s).  Every draw is
 // uniform(seed, T, (L*p + k)*d + j), so the sample set is identical to the reference's for any
 // partition of threads over warps, segments or GPUs.
 //
-// Bin contributions: shared-memory FP64 atomicAdd is a CAS loop on sm_100 (ATOMS.CAST.SPIN), so
-// each warp owns a private (d x n_bins) table in shared memory and resolves intra-warp collisions
-// with a tag-and-retry round; tables are merged warp -> CTA -> grid in a fixed order.
+// The pass is two kernels:
+//   vsample_kernel  pure compute at 16 warps/SM: hash -> stratified y -> grid transform -> f -> per-cube
+//                   (S1, S2, estimate, variance); it emits one compact record per sample
+//                   (contribution, d bin ids) to HBM instead of touching a histogram;
+//   bin_kernel      streams the records and accumulates the (d x n_bins) contribution table.
+// Shared-memory FP64 atomicAdd is a CAS loop on sm_100 (ATOMS.CAST.SPIN), so in bin_kernel each warp
+// owns a private table in shared memory, arbitrates intra-warp collisions with one tag round and lets
+// the few losers use the CAS atomic; tables are merged warp -> CTA -> grid in a fixed order.
+// Keeping the table out of the sampling kernel is what lifts it from 5 to 16 resident warps per SM.
 #pragma once
 
 #include "pcb_device.cuh"
@@ -35,59 +41,22 @@ struct SampleArgs {
   double* seg_partials;         // [(t - t_begin) * nseg + q][2]
   unsigned long long* clamps;
   unsigned long long* bad;      // min over non-finite samples of cube*p + k
-  double* block_hist;           // [gridDim.x][d*nb]
+  // sample records of this launch's units [unit_begin, unit_end): record r of unit u sits at
+  // (u - unit_begin) * rec_per_unit + r with r = (cube_step * p + k) * 32 + lane
+  long long unit_begin, unit_end, rec_per_unit, rec_capacity;
+  double* rec_w;                // [rec_capacity] contribution (v^2, or f^2 when not squared_weighted)
+  unsigned short* rec_b;        // [d][rec_capacity] bin ids
 };
 
-// Add one or two samples' contributions to the warp-private table.  One tag round arbitrates lanes
-// that hit the same bin: every contender writes its lane id, whoever reads its own id back owns the
-// bin and does a plain read-modify-write.  The few losers (about one lane per axis) then add theirs
-// with the shared-memory CAS atomic, which is only slow when many lanes use it.  When both samples of
-// a lane fall into the same bin their contributions are merged into one update.
-template <int D, int NS>
-__device__ __forceinline__ void hist_add(double* hist, unsigned char* tags, const int (&bin)[NS][D], int nb,
-                                         const double (&w2)[NS], bool on, int lane) {
-  int off[NS][D];
-  double add[NS][D];
-  bool use[NS][D];
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    off[0][j] = j * nb + bin[0][j];
-    add[0][j] = w2[0];
-    use[0][j] = on;
-    if constexpr (NS == 2) {
-      off[1][j] = j * nb + bin[1][j];
-      const bool same = bin[1][j] == bin[0][j];
-      add[0][j] = same ? w2[0] + w2[1] : w2[0];
-      add[1][j] = w2[1];
-      use[1][j] = on && !same;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < NS; ++q)
-#pragma unroll
-    for (int j = 0; j < D; ++j)
-      if (use[q][j]) tags[off[q][j]] = (unsigned char)lane;
-  __syncwarp();
-  unsigned lost = 0;
-#pragma unroll
-  for (int q = 0; q < NS; ++q)
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      const bool win = use[q][j] && tags[off[q][j]] == lane;
-      const double updated = hist[off[q][j]] + add[q][j];
-      if (win) hist[off[q][j]] = updated;
-      lost |= (use[q][j] && !win) ? (1u << (q * D + j)) : 0u;
-    }
-  __syncwarp();
-  if (__any_sync(PCB_FULL_MASK, lost)) {
-#pragma unroll
-    for (int q = 0; q < NS; ++q)
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-        if ((lost >> (q * D + j)) & 1u) atomicAdd(hist + off[q][j], add[q][j]);
-    __syncwarp();
-  }
-}
+struct BinArgs {
+  int nb;
+  long long n_groups;           // record groups of 32
+  long long rec_capacity;
+  const double* rec_w;
+  const unsigned short* rec_b;
+  double* block_hist;           // [gridDim.x][d*nb], accumulated across launches
+  int accumulate;               // 0: overwrite block_hist, 1: add to it
+};
 
 // One sample: draw u per axis, stratify, push through the grid, evaluate (mcubes.py:224-243).
 template <class F, int D, int RNG>
@@ -125,33 +94,24 @@ __device__ __forceinline__ void draw_sample(const SampleArgs& a, const double* s
   v = fx * jac;
 }
 
-// warps per CTA are bounded by shared memory (one private table each); from d = 4 on at most 8 fit usefully,
-// which lets the compiler use up to 255 registers for the two-sample interleave
-__host__ __device__ constexpr int vsample_max_warps(int d) { return d >= 4 ? 8 : 16; }
+constexpr int kSampleWarps = 8;  // warps per sampling CTA; two CTAs per SM at 128 registers
 
 template <int FAM, int D, int RNG>
-__global__ void __launch_bounds__(vsample_max_warps(D) * 32) vsample_kernel(const __grid_constant__ SampleArgs a) {
+__global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb = a.nb, nb1 = a.nb + 1;
-  const int W = blockDim.x >> 5;
+  const int nb1 = a.nb + 1;
   double* s_b = reinterpret_cast<double*>(smem_raw);            // [D][nb+1]
-  double* s_hist = s_b + D * nb1;                               // [W][D*nb]
-  unsigned char* s_tag = reinterpret_cast<unsigned char*>(s_hist + (size_t)W * D * nb);  // [W][D*nb]
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-
   for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
-  for (int i = threadIdx.x; i < W * D * nb; i += blockDim.x) s_hist[i] = 0.0;
   __syncthreads();
-  double* hist = s_hist + (size_t)wib * D * nb;
-  unsigned char* tags = s_tag + (size_t)wib * D * nb;
 
-  const long long n_units = a.n_lw * a.nseg;
   const int p = a.p;
   const double pd = (double)p;
   unsigned long long clamp_count = 0;
 
-  for (long long u = (long long)blockIdx.x * W + wib; u < n_units; u += (long long)gridDim.x * W) {
+  for (long long u = a.unit_begin + (long long)blockIdx.x * kSampleWarps + wib; u < a.unit_end;
+       u += (long long)gridDim.x * kSampleWarps) {
     const long long lw = u % a.n_lw;
     const int q = (int)(u / a.n_lw);
     const long long T = a.t_begin + lw + (long long)lane * a.n_lw;
@@ -164,12 +124,6 @@ __global__ void __launch_bounds__(vsample_max_warps(D) * 32) vsample_kernel(cons
       long long c_end = T * a.s + l1;
       if (c_end > a.m) c_end = a.m;
       count = c_end > c_begin ? c_end - c_begin : 0;
-    }
-    long long max_count = count;
-#pragma unroll
-    for (int mm = 16; mm >= 1; mm >>= 1) {
-      long long o = __shfl_xor_sync(PCB_FULL_MASK, max_count, mm);
-      max_count = o > max_count ? o : max_count;
     }
     // sub-cube coordinates (axis 0 most significant, mcubes.py:132-140), kept as doubles
     double coord[D];
@@ -187,8 +141,12 @@ __global__ void __launch_bounds__(vsample_max_warps(D) * 32) vsample_kernel(cons
     unsigned long long ctr = (unsigned long long)(q * a.seg_len) * (unsigned long long)p * D;
     unsigned long long kc = key + (ctr + 1ULL) * kGolden;
     double sum_est = 0.0, sum_var = 0.0;
+    double* rw = a.rec_w + (u - a.unit_begin) * a.rec_per_unit + lane;
+    unsigned short* rb = a.rec_b + (u - a.unit_begin) * a.rec_per_unit + lane;
 
-    for (long long i = 0; i < max_count; ++i) {
+    // every lane walks the full segment so that the record block of the unit is completely written;
+    // lanes past their own cube range emit empty records
+    for (long long i = 0; i < a.seg_len; ++i) {
       const bool active = i < count;
       const unsigned long long inj_cube = (unsigned long long)(c_begin + i) * (unsigned long long)p;
       double s1 = 0.0, s2 = 0.0;
@@ -210,21 +168,28 @@ __global__ void __launch_bounds__(vsample_max_warps(D) * 32) vsample_kernel(cons
         // 8-accumulator tree -- only the rounding differs)
         s1 = (k == 0) ? v[0] + v[1] : (s1 + v[0]) + v[1];
         s2 = (k == 0) ? v2[0] + v2[1] : (s2 + v2[0]) + v2[1];
-        const double w2[2] = {a.squared_weighted ? v2[0] : fx[0] * fx[0], a.squared_weighted ? v2[1] : fx[1] * fx[1]};
-        hist_add<D, 2>(hist, tags, bin, nb, w2, active, lane);
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2) {
+          const long long r = (i * p + k + q2) * 32;
+          rw[r] = active ? (a.squared_weighted ? v2[q2] : fx[q2] * fx[q2]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = (unsigned short)bin[q2][j];
+        }
       }
       for (; k < p; ++k) {
-        int bin[1][D];
+        int bin[D];
         double fx, v;
-        draw_sample<F, D, RNG>(a, s_b, coord, kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, bin[0], fx, v);
+        draw_sample<F, D, RNG>(a, s_b, coord, kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, bin, fx, v);
         kc += (unsigned long long)D * kGolden;
         ctr += D;
         if (active && !isfinite(fx)) atomicMin(a.bad, inj_cube + (unsigned long long)k);
         const double v2 = v * v;
         s1 = (k == 0) ? v : s1 + v;
         s2 = (k == 0) ? v2 : s2 + v2;
-        const double w2[1] = {a.squared_weighted ? v2 : fx * fx};
-        hist_add<D, 1>(hist, tags, bin, nb, w2, active, lane);
+        const long long r = (i * p + k) * 32;
+        rw[r] = active ? (a.squared_weighted ? v2 : fx * fx) : 0.0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = (unsigned short)bin[j];
       }
       if (active) {
         const double est = s1 / a.den_est;
@@ -249,14 +214,6 @@ __global__ void __launch_bounds__(vsample_max_warps(D) * 32) vsample_kernel(cons
     }
   }
   if (clamp_count) atomicAdd(a.clamps, clamp_count);
-  __syncthreads();
-  // warp tables -> CTA table, fixed warp order
-  double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
-  for (int i = threadIdx.x; i < D * nb; i += blockDim.x) {
-    double t = s_hist[i];
-    for (int w = 1; w < W; ++w) t = t + s_hist[(size_t)w * D * nb + i];
-    dst[i] = t;
-  }
 }
 
 }  // namespace pcb

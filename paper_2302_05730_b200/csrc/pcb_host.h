@@ -5,7 +5,9 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <map>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/parcube_b200.h"
@@ -47,6 +49,8 @@ struct pcb_ctx {
   int sm_count = 0;
   int clock_khz = 0;
   size_t smem_optin = 0;
+  size_t total_mem = 0;
+  std::map<const void*, size_t> smem_attr;  // dynamic shared memory already granted per kernel
   cudaStream_t stream = nullptr;
   std::string err;
   long long launches = 0;
@@ -58,10 +62,10 @@ struct pcb_ctx {
   // roofline profiling (pcb_profile_begin/end)
   bool profiling = false;
   struct Span { cudaEvent_t a, b; };
-  std::vector<Span> spans[2];
+  std::vector<Span> spans[3];
   std::vector<Span> span_pool;
-  double span_units[2] = {0, 0};
-  pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject;
+  double span_units[3] = {0, 0, 0};
+  pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject, mc_rec;
 };
 
 namespace pcb {
