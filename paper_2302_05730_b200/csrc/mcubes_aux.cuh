@@ -12,7 +12,7 @@ namespace pcb {
 // d x R warps (up to 32) and the SM's latency is hidden by occupancy instead of by a 36 KB table per
 // warp.  The d warps of a stream read the same records (L1/L2 hits on the contributions), two
 // records per lane and round.  Tables are merged stream -> CTA here, CTA -> grid by merge_hist_kernel.
-__global__ void __launch_bounds__(1024) bin_kernel(const __grid_constant__ BinArgs a, int d, int streams) {
+__global__ void __launch_bounds__(512, 3) bin_kernel(const __grid_constant__ BinArgs a, int d, int streams) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb;
   const int W = blockDim.x >> 5;                                  // = d * streams
@@ -26,44 +26,46 @@ __global__ void __launch_bounds__(1024) bin_kernel(const __grid_constant__ BinAr
   unsigned char* __restrict__ tags = s_tag + (size_t)wib * nb;
   const unsigned short* __restrict__ bins = a.rec_b + (long long)axis * a.rec_capacity;
 
-  const long long n_pairs = (a.n_groups + 1) / 2, step = (long long)gridDim.x * streams;
+  // record pairs (64 records) are dealt round-robin to the streams of the grid; n_groups is even (host pads)
+  const long long n_pairs = a.n_groups / 2, step = (long long)gridDim.x * streams;
   long long pr = (long long)blockIdx.x * streams + stream;
-  auto fetch = [&](long long q, double (&w)[2], int (&b)[2]) {
-    const long long r0 = q * 64 + lane, r1 = r0 + 32;
-    const bool has0 = q < n_pairs, has1 = has0 && 2 * q + 1 < a.n_groups;
-    w[0] = has0 ? a.rec_w[r0] : 0.0;
-    w[1] = has1 ? a.rec_w[r1] : 0.0;
-    b[0] = has0 ? bins[r0] : 0;
-    b[1] = has1 ? bins[r1] : 0;
-  };
-  double w[2], wn[2];
-  int b[2], bn[2];
-  fetch(pr, w, b);
+  const double* __restrict__ pw = a.rec_w + pr * 64 + lane;
+  const unsigned short* __restrict__ pb = bins + pr * 64 + lane;
+  const long long hop = step * 64;
+  double w0 = 0.0, w1 = 0.0;
+  int b0 = 0, b1 = 0;
+  if (pr < n_pairs) { w0 = pw[0]; w1 = pw[32]; b0 = pb[0]; b1 = pb[32]; }
   for (; pr < n_pairs; pr += step) {
-    fetch(pr + step, wn, bn);
+    // prefetch the next pair while this one is applied
+    double nw0 = 0.0, nw1 = 0.0;
+    int nb0 = 0, nb1 = 0;
+    pw += hop; pb += hop;
+    if (pr + step < n_pairs) { nw0 = pw[0]; nw1 = pw[32]; nb0 = pb[0]; nb1 = pb[32]; }
     // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
     // two records of one lane in the same bin become one update
-    const bool same = b[0] == b[1];
-    const double add0 = same ? w[0] + w[1] : w[0], add1 = w[1];
+    const bool same = b0 == b1;
+    const double add0 = same ? w0 + w1 : w0, add1 = w1;
     unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
-    for (int round = 0; round < 2 && __any_sync(PCB_FULL_MASK, want); ++round) {
-      if (want & 1u) tags[b[0]] = (unsigned char)lane;
-      if (want & 2u) tags[b[1]] = (unsigned char)lane;
+#pragma unroll
+    for (int round = 0; round < 2; ++round) {
+      if (want & 1u) tags[b0] = (unsigned char)lane;
+      if (want & 2u) tags[b1] = (unsigned char)lane;
       __syncwarp();
-      const unsigned char t0 = tags[b[0]], t1 = tags[b[1]];
-      const double o0 = hist[b[0]], o1 = hist[b[1]];
+      const unsigned char t0 = tags[b0], t1 = tags[b1];
+      const double o0 = hist[b0], o1 = hist[b1];
       const bool win0 = (want & 1u) && t0 == lane, win1 = (want & 2u) && t1 == lane;
-      if (win0) hist[b[0]] = o0 + add0;
-      if (win1) hist[b[1]] = o1 + add1;
+      if (win0) hist[b0] = o0 + add0;
+      if (win1) hist[b1] = o1 + add1;
       want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
       __syncwarp();
+      if (!__any_sync(PCB_FULL_MASK, want)) break;
     }
     if (__any_sync(PCB_FULL_MASK, want)) {  // triple collisions: shared-memory CAS atomic
-      if (want & 1u) atomicAdd(hist + b[0], add0);
-      if (want & 2u) atomicAdd(hist + b[1], add1);
+      if (want & 1u) atomicAdd(hist + b0, add0);
+      if (want & 2u) atomicAdd(hist + b1, add1);
       __syncwarp();
     }
-    w[0] = wn[0]; w[1] = wn[1]; b[0] = bn[0]; b[1] = bn[1];
+    w0 = nw0; w1 = nw1; b0 = nb0; b1 = nb1;
   }
   __syncthreads();
   double* dst = a.block_hist + (size_t)blockIdx.x * d * nb;
@@ -76,13 +78,57 @@ __global__ void __launch_bounds__(1024) bin_kernel(const __grid_constant__ BinAr
 }
 
 
-// CTA tables -> contribution table, fixed CTA order
-__global__ void merge_hist_kernel(const double* __restrict__ block_hist, int nblocks, int nbins_total, double* __restrict__ out) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nbins_total) return;
-  double t = block_hist[i];
-  for (int b = 1; b < nblocks; ++b) t = t + block_hist[(size_t)b * nbins_total + i];
-  out[i] = t;
+// CTA tables -> contribution table in a fixed order: a CTA owns 32 bins; thread (chunk c, bin i) adds the
+// tables of blocks [c*per, (c+1)*per) serially, then the 32 chunk sums of a bin are added in chunk order.
+constexpr int kMergeChunks = 32;
+__global__ void __launch_bounds__(32 * kMergeChunks) merge_hist_kernel(const double* __restrict__ block_hist, int nblocks,
+                                                                       int nbins_total, double* __restrict__ out) {
+  __shared__ double s_part[kMergeChunks][33];
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  const int per = (nblocks + kMergeChunks - 1) / kMergeChunks;
+  const int b0 = c * per, b1 = min(nblocks, b0 + per);
+  double t = 0.0;
+  if (i < nbins_total && b0 < b1) {
+    t = block_hist[(size_t)b0 * nbins_total + i];
+    int b = b0 + 1;
+    for (; b + 8 <= b1; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = block_hist[(size_t)(b + k) * nbins_total + i];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t = t + v[k];
+    }
+    for (; b < b1; ++b) t = t + block_hist[(size_t)b * nbins_total + i];
+  }
+  s_part[c][lane] = t;
+  __syncthreads();
+  if (c == 0 && i < nbins_total) {
+    double r = s_part[0][lane];
+    const int used = (nblocks + per - 1) / per;
+    for (int k = 1; k < used; ++k) r = r + s_part[k][lane];
+    out[i] = r;
+  }
+}
+
+// final reduction of the per-work-group (I, E) pairs in group order with the pair tree of engine.tree_sum
+// (mcubes.py:292-293), for up to 1024 groups in one CTA; out[0] = integral, out[1] = variance sum
+__global__ void __launch_bounds__(512) group_pairs_tree_kernel(const double* __restrict__ pairs, int n, double* __restrict__ out) {
+  __shared__ double s[2][1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    s[0][i] = i < n ? pairs[2 * i] : 0.0;
+    s[1][i] = i < n ? pairs[2 * i + 1] : 0.0;
+  }
+  __syncthreads();
+  for (int half = 512; half >= 1; half >>= 1) {
+    double e = 0.0, v = 0.0;
+    const bool act = threadIdx.x < half;
+    if (act) { e = s[0][2 * threadIdx.x] + s[0][2 * threadIdx.x + 1]; v = s[1][2 * threadIdx.x] + s[1][2 * threadIdx.x + 1]; }
+    __syncthreads();
+    if (act) { s[0][threadIdx.x] = e; s[1][threadIdx.x] = v; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[0] = s[0][0]; out[1] = s[1][0]; }
 }
 
 // per logical thread: serial sum of its segment partials; then one CTA per work-group reduces the
@@ -236,12 +282,18 @@ __global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant_
   if (tid == 0) {
     const double wsum = np_pairwise_sum(w, n);
     s_wsum = wsum;
-    double run = 0.0;
+    double run = w[0];
     cw[0] = 0.0;
-    for (int i = 0; i < n; ++i) {  // np.cumsum: serial
-      run = (i == 0) ? w[0] : run + w[i];
-      cw[i + 1] = run;
+    cw[1] = run;
+    int i = 1;
+    for (; i + 8 <= n; i += 8) {  // np.cumsum: serial adds, loads batched so only the DADD chain is exposed
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = w[i + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) { run = run + v[k]; cw[i + k + 1] = run; }
     }
+    for (; i < n; ++i) { run = run + w[i]; cw[i + 1] = run; }
     cw[n] = wsum;
   }
   __syncthreads();
@@ -266,7 +318,11 @@ __global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant_
   }
   if (tid == 0) { row[0] = 0.0; row[n] = 1.0; }
   __syncthreads();
-  if (tid == 0) {  // restore strict monotonicity (vegas_grid.py:183-192)
+  // the serial repair below is a no-op unless some boundary collapsed: test that in parallel first
+  int broken = 0;
+  for (int k = tid + 1; k <= n; k += blockDim.x) broken |= (row[k] <= row[k - 1]);
+  broken = __syncthreads_or(broken);
+  if (broken && tid == 0) {  // restore strict monotonicity (vegas_grid.py:183-192)
     for (int k = 1; k <= n; ++k)
       if (row[k] <= row[k - 1]) row[k] = nextafter(row[k - 1], 2.0);
     if (row[n] != 1.0) {

@@ -47,7 +47,7 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
   const long long n_lw = (n_local_threads + 31) / 32;
   out->smem = bounds_bytes;
   // accumulation CTA: d warps (one per axis) per record stream, as many streams as fit in 32 warps / shared memory
-  const int streams = (int)std::max<size_t>(1, std::min<size_t>(32 / plan->d, avail / (per_warp * plan->d)));
+  const int streams = (int)std::max<size_t>(1, std::min<size_t>(16 / plan->d, avail / (per_warp * plan->d)));
   out->bin_warps = streams * plan->d;
   out->bin_smem = (size_t)out->bin_warps * per_warp + 16;
   // work units = logical warps x segments; aim at >= 8 units per resident warp for balance
@@ -99,7 +99,7 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
 
   // record buffer: one contribution (8 B) + d bin ids (2 B each) per sample slot, chunked over work units
   const long long n_lw = (nt + 31) / 32, units = n_lw * L.nseg;
-  const long long rec_per_unit = L.seg_len * plan->p * 32;
+  const long long rec_per_unit = round_up(L.seg_len * plan->p, 2) * 32;  // even number of 32-record groups
   const size_t rec_bytes = 8 + 2 * (size_t)d;
   size_t budget = (size_t)24 << 30;
   if (const char* env = std::getenv("PCB_MCUBES_RECORD_BYTES")) budget = (size_t)std::max(1LL, std::atoll(env));
@@ -109,7 +109,10 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   const long long rec_capacity = round_up(chunk_units * rec_per_unit, 64);
   PCB_CUDA_TRY(ctx, ctx->mc_rec.ensure((size_t)rec_capacity * rec_bytes));
 
-  const int bin_blocks = ctx->sm_count;
+  // accumulation grid: three 16-warp CTAs per SM (48 resident warps) for big passes, fewer for small ones
+  const long long total_pairs = std::min(units, chunk_units) * rec_per_unit / 64;
+  const int bin_streams = L.bin_warps / d;
+  const int bin_blocks = (int)std::max<long long>(1, std::min<long long>(3LL * ctx->sm_count, total_pairs / (32LL * bin_streams)));
   PCB_CUDA_TRY(ctx, ctx->mc_seg.ensure((size_t)nt * L.nseg * 2 * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)bin_blocks * d * nb * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure((size_t)d * nb * sizeof(double)));
@@ -182,20 +185,27 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
       ctx->launches++;
     }
   }
-  merge_hist_kernel<<<(d * nb + 255) / 256, 256, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), bin_blocks, d * nb,
-                                                                     ctx->mc_contrib.as<double>());
+  merge_hist_kernel<<<(d * nb + 31) / 32, 32 * kMergeChunks, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), bin_blocks, d * nb,
+                                                                                ctx->mc_contrib.as<double>());
   int pow2 = 1;
   while (pow2 < plan->group_size) pow2 <<= 1;
   const int gt_threads = std::max(32, std::min(256, pow2 / 2));
   group_tree_kernel<<<(unsigned)n_groups, gt_threads, 2 * pow2 * sizeof(double), ctx->stream>>>(
       ctx->mc_seg.as<double>(), L.nseg, nt, plan->group_size, pow2, ctx->mc_group.as<double>());
-  double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
-  double* ge = gi + n_groups;
-  deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
-  ctx->launches += 3;
-  PCB_CUDA_TRY(ctx, cudaGetLastError());
-  PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));   // engine.reduce in group order (mcubes.py:292-293)
-  PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
+  ctx->launches += 2;
+  if (n_groups <= 1024) {  // engine.reduce in group order (mcubes.py:292-293), both sums in one small CTA
+    group_pairs_tree_kernel<<<1, 512, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, sc + M_INTEGRAL);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+  } else {
+    double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
+    double* ge = gi + n_groups;
+    deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+    PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));
+    PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
+  }
   if (n_groups_out) *n_groups_out = n_groups;
   return PCB_OK;
 }

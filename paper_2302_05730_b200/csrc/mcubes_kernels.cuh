@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
         coord[j] = 0.0;
       }
     }
+    if ((a.seg_len * p) & 1) {  // units hold an even number of 32-record groups: blank the padding group
+      const long long r = a.seg_len * p * 32;
+      rw[r] = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = 0;
+    }
     if (T < a.t_end) {
       double* out = a.seg_partials + ((T - a.t_begin) * a.nseg + q) * 2;
       out[0] = sum_est;
