@@ -166,6 +166,15 @@ def b200_step(w, pb, comm=None):
 
     d = w["d"]
     f = pb.get_integrand(w["family"], d)
+    if w["kind"] == "pagani" and comm is not None and comm.world > 1:
+        # region list sharded over the ranks, per-iteration rebalancing (sharded.py)
+        t0 = time.perf_counter()
+        res = sharded.pagani_refine_sharded(f, pb.PaganiConfig(rel_tol=w["rel_tol"]), comm)
+        secs = time.perf_counter() - t0
+        evals = int(res.regions_processed) * F_EVAL[d]
+        info = dict(estimate=res.estimate, errorest=res.errorest, iterations=res.iterations,
+                    regions_processed=int(res.regions_processed), reason=res.reason)
+        return evals, secs, info, 312 + 352 + 40, 40 * (res.iterations + 1) + 56
     if w["kind"] == "pagani":
         cfg = pb.PaganiConfig(rel_tol=w["rel_tol"])
         res, history = _native.pagani_refine(f.device_spec(), pb.rules.orbit_form(pb.build_rule(d)), cfg)

@@ -218,6 +218,35 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
                              pcb_pagani_progress* records, pcb_pagani_progress_fn progress, void* user,
                              pcb_nonfinite* bad);
 
+/* ---- PAGANI on a shard of the region list (multi-GPU; one context per rank) ------------------
+ * The ordered global region list is the concatenation of the ranks' slices.  These calls run one
+ * step of refine (pagani.py:300-391) on the local slice and leave the collectives to the host
+ * (paper_2302_05730_b200/sharded.py: torch.distributed over NCCL).
+ *   init      local slice [first, first+count) of the g^d uniform tiling (core.py:250-269), then evaluate
+ *   reduce    `which` 0/1 = active integrals/errors, 2/3 = integrals/errors retired by the last split.
+ *             With `head` = number of local elements before the first 1024-aligned GLOBAL index it returns
+ *             the raw head elements, the sums of the full aligned 1024-blocks (pair tree, engine.py:69-86)
+ *             and the raw tail elements, so every rank can finish the global tree bit-identically.
+ *   classify  split mask (pagani.py:361-365): mode 0 err > budget*vol, mode 1 err >= emax; returns the count
+ *   split     stable compaction + bisection of the marked regions (pagani.py:282-297, 371-377); the children
+ *             become the local list (not yet evaluated), the rest is retired
+ *   export    rows [begin, end) of the local list in the reference's (n,d) row-major layout
+ *   rebuild   new local list = front rows ++ local[keep_begin, keep_end) ++ back rows  (rebalancing)
+ *   evaluate  evaluate the local list                                                                  */
+pcb_status pcb_pagani_shard_init(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                                 int32_t g, int64_t first, int64_t count, pcb_nonfinite* bad);
+pcb_status pcb_pagani_shard_count(pcb_ctx* ctx, int64_t* n_active, int64_t* n_retired);
+pcb_status pcb_pagani_shard_reduce(pcb_ctx* ctx, int32_t which, int64_t head, double* head_vals, int64_t* n_blocks,
+                                   double* block_sums, double* tail_vals, int64_t* n_tail);
+pcb_status pcb_pagani_shard_max_error(pcb_ctx* ctx, double* emax);
+pcb_status pcb_pagani_shard_classify(pcb_ctx* ctx, double budget, int32_t mode, double emax, int64_t* n_split);
+pcb_status pcb_pagani_shard_split(pcb_ctx* ctx);
+pcb_status pcb_pagani_shard_export(pcb_ctx* ctx, int64_t begin, int64_t end, double* lefts_rows, double* lengths_rows);
+pcb_status pcb_pagani_shard_rebuild(pcb_ctx* ctx, int64_t keep_begin, int64_t keep_end, int64_t n_front,
+                                    const double* front_lefts, const double* front_lengths, int64_t n_back,
+                                    const double* back_lefts, const double* back_lengths);
+pcb_status pcb_pagani_shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad);
+
 /* ---- fixed-shape reductions: replaces engine.tree_sum (engine.py:69-86) --------------- */
 pcb_status pcb_tree_sum(pcb_ctx* ctx, int64_t n, const double* values, double* out);
 

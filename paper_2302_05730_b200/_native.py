@@ -116,6 +116,18 @@ SIGNATURES = {
                                     C.POINTER(PaganiResultC), C.POINTER(PaganiProgressC), PAGANI_PROGRESS_FN, C.c_void_p,
                                     C.POINTER(NonFiniteC)]),
     "pcb_tree_sum": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, _DP]),
+    "pcb_pagani_shard_init": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
+                                        C.c_int32, C.c_int64, C.c_int64, C.POINTER(NonFiniteC)]),
+    "pcb_pagani_shard_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pcb_pagani_shard_reduce": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                                          C.c_void_p, C.POINTER(C.c_int64)]),
+    "pcb_pagani_shard_max_error": (C.c_int, [C.c_void_p, _DP]),
+    "pcb_pagani_shard_classify": (C.c_int, [C.c_void_p, C.c_double, C.c_int32, C.c_double, C.POINTER(C.c_int64)]),
+    "pcb_pagani_shard_split": (C.c_int, [C.c_void_p]),
+    "pcb_pagani_shard_export": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "pcb_pagani_shard_rebuild": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                           C.c_void_p, C.c_void_p]),
+    "pcb_pagani_shard_evaluate": (C.c_int, [C.c_void_p, C.POINTER(NonFiniteC)]),
     "pcb_mcubes_sample": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_void_p, C.c_uint64,
                                     C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(McubesIterationC),
                                     C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
@@ -481,3 +493,74 @@ def debug_divide(x: np.ndarray, g: int, device=None) -> np.ndarray:
     with ctx.call_lock:
         ctx.check(ctx.lib.pcb_debug_divide(ctx.handle, xx.size, _ptr(xx), int(g), _ptr(out)))
     return out
+
+
+class PaganiShard:
+    """The local slice of a sharded PAGANI refinement, resident on one device (pcb_pagani_shard_*)."""
+
+    TREE_SPAN = 1024
+
+    def __init__(self, spec: DeviceSpec, orbit, cfg, device=None, ctx: "Context | None" = None):
+        self.ctx = ctx or context(device)  # the shard state lives in the context: one shard per context
+        self.d = spec.d
+        self._f, self._r, self._c = spec.to_c(), rule_to_c(orbit), pagani_config_to_c(cfg)
+
+    def _call(self, fn, *args, bad=None):
+        with self.ctx.call_lock:
+            self.ctx.check(fn(self.ctx.handle, *args), bad, self.d)
+
+    def init(self, g: int, first: int, count: int):
+        bad = NonFiniteC()
+        self._call(self.ctx.lib.pcb_pagani_shard_init, C.byref(self._f), C.byref(self._r), C.byref(self._c), int(g),
+                   int(first), int(count), C.byref(bad), bad=bad)
+
+    def counts(self):
+        a, r = C.c_int64(), C.c_int64()
+        self._call(self.ctx.lib.pcb_pagani_shard_count, C.byref(a), C.byref(r))
+        return a.value, r.value
+
+    def reduce(self, which: int, head: int):
+        n_active, n_ret = self.counts()
+        n = n_active if which < 2 else n_ret
+        head_vals, tail_vals = np.empty(self.TREE_SPAN), np.empty(self.TREE_SPAN)
+        blocks = np.empty(n // self.TREE_SPAN + 1)
+        nb, nt = C.c_int64(), C.c_int64()
+        self._call(self.ctx.lib.pcb_pagani_shard_reduce, int(which), int(head), _ptr(head_vals), C.byref(nb), _ptr(blocks),
+                   _ptr(tail_vals), C.byref(nt))
+        return head_vals[: min(head, n)].copy(), blocks[: nb.value].copy(), tail_vals[: nt.value].copy()
+
+    def max_error(self) -> float:
+        out = C.c_double()
+        self._call(self.ctx.lib.pcb_pagani_shard_max_error, C.byref(out))
+        return out.value
+
+    def classify(self, budget: float, mode: int, emax: float) -> int:
+        out = C.c_int64()
+        self._call(self.ctx.lib.pcb_pagani_shard_classify, float(budget), int(mode), float(emax), C.byref(out))
+        return out.value
+
+    def split(self):
+        self._call(self.ctx.lib.pcb_pagani_shard_split)
+
+    def export(self, begin: int, end: int):
+        n = end - begin
+        lefts, lengths = np.empty((n, self.d)), np.empty((n, self.d))
+        self._call(self.ctx.lib.pcb_pagani_shard_export, int(begin), int(end), _ptr(lefts), _ptr(lengths))
+        return lefts, lengths
+
+    def rebuild(self, keep_begin, keep_end, front, back):
+        fl, fh = (_f64(front[0]), _f64(front[1])) if front is not None and len(front[0]) else (None, None)
+        bl, bh = (_f64(back[0]), _f64(back[1])) if back is not None and len(back[0]) else (None, None)
+        self._call(self.ctx.lib.pcb_pagani_shard_rebuild, int(keep_begin), int(keep_end),
+                   0 if fl is None else fl.shape[0], None if fl is None else _ptr(fl), None if fh is None else _ptr(fh),
+                   0 if bl is None else bl.shape[0], None if bl is None else _ptr(bl), None if bh is None else _ptr(bh))
+
+    def evaluate(self):
+        bad = NonFiniteC()
+        self._call(self.ctx.lib.pcb_pagani_shard_evaluate, C.byref(bad), bad=bad)
+
+    def tree_sum(self, values) -> float:
+        v = _f64(values).ravel()
+        out = C.c_double()
+        self._call(self.ctx.lib.pcb_tree_sum, v.size, _ptr(v), C.byref(out))
+        return out.value

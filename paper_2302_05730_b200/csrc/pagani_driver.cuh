@@ -191,9 +191,9 @@ __global__ void __launch_bounds__(kScanBlock) split_kernel(const __grid_constant
 }
 
 // lexicographic uniform tiling, axis 0 slowest: left = idx * (1/g), length = 1/g (core.py:265-268)
-__global__ void tiling_kernel(int d, int g, long long n, long long ld, double h, double* lefts, double* lengths) {
+__global__ void tiling_kernel(int d, int g, long long first, long long n, long long ld, double h, double* lefts, double* lengths) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
-    long long rem = r;
+    long long rem = first + r;  // global tile index
     for (int j = d - 1; j >= 0; --j) {
       lefts[j * ld + r] = (double)(rem % g) * h;
       lengths[j * ld + r] = h;
@@ -206,6 +206,23 @@ __global__ void tiling_kernel(int d, int g, long long n, long long ld, double h,
 __global__ void rows_to_soa_kernel(int d, long long n, long long ld, const double* __restrict__ rows, double* __restrict__ soa) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
     for (int j = 0; j < d; ++j) soa[j * ld + r] = rows[r * d + j];
+}
+
+__global__ void soa_to_rows_kernel(int d, long long begin, long long n, long long ld, const double* __restrict__ soa, double* __restrict__ rows) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    for (int j = 0; j < d; ++j) rows[r * d + j] = soa[j * ld + begin + r];
+}
+
+// dst[j][dst_off + r] = src[j][src_off + r]
+__global__ void soa_copy_kernel(int d, long long n, long long ld_src, long long src_off, const double* __restrict__ src,
+                                long long ld_dst, long long dst_off, double* __restrict__ dst) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    for (int j = 0; j < d; ++j) dst[j * ld_dst + dst_off + r] = src[j * ld_src + src_off + r];
+}
+
+__global__ void rows_to_soa_at_kernel(int d, long long n, long long ld, long long off, const double* __restrict__ rows, double* __restrict__ soa) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x)
+    for (int j = 0; j < d; ++j) soa[j * ld + off + r] = rows[r * d + j];
 }
 
 __global__ void widen_axes_kernel(long long n, const int32_t* __restrict__ in, long long* __restrict__ out) {

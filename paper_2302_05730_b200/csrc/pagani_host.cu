@@ -256,7 +256,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   PCB_CUDA_TRY(ctx, ctx->lefts[cur].ensure((size_t)ld * d * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->lengths[cur].ensure((size_t)ld * d * sizeof(double)));
   tiling_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-      d, (int)g, n, ld, 1.0 / (double)g, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>());
+      d, (int)g, 0LL, n, ld, 1.0 / (double)g, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>());
   ctx->launches++;
 
   double* sc = ctx->scalars.as<double>();
@@ -390,6 +390,239 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   result->seconds_device = ms * 1e-3;
   result->kernel_launches = ctx->launches - launches0;
   return PCB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// PAGANI on a shard of the region list: one refine step at a time, collectives left to the host.
+// ------------------------------------------------------------------------------------------------
+static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 4096)); }
+
+static pcb_status shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad) {
+  auto& S = ctx->shard;
+  S.classified = false;
+  if (S.n == 0) return PCB_OK;
+  PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)S.n * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)S.n * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)S.n * sizeof(int32_t)));
+  unsigned long long* bad_dev = ctx->scalars.as<unsigned long long>() + S_BAD;
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xFF, sizeof(unsigned long long), ctx->stream));
+  PCB_TRY(evaluate_launch(ctx, &S.f, &S.rule, &S.cfg, S.n, S.ld, ctx->lefts[S.cur].as<double>(), ctx->lengths[S.cur].as<double>(),
+                          ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), bad_dev));
+  PCB_TRY(read_scalars(ctx, S_BAD, 1));
+  const unsigned long long flat = ((unsigned long long*)ctx->pinned)[S_BAD];
+  if (flat != ~0ULL)
+    return fetch_nonfinite_pagani(ctx, &S.f, &S.rule, S.ld, ctx->lefts[S.cur].as<double>(), ctx->lengths[S.cur].as<double>(), flat, bad);
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_init(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
+                                 int32_t g, int64_t first, int64_t count, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_rule(ctx, f, rule, cfg));
+  if (g < 1 || first < 0 || count < 0) return fail(ctx, PCB_INVALID, "shard_init: bad tiling slice");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  S = pcb_ctx::Shard();
+  S.live = true;
+  S.f = *f; S.rule = *rule; S.cfg = *cfg;
+  S.n = count;
+  S.ld = round_up(std::max<long long>(count, 1), 32);
+  const int d = f->d;
+  PCB_CUDA_TRY(ctx, ctx->lefts[0].ensure((size_t)S.ld * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[0].ensure((size_t)S.ld * d * sizeof(double)));
+  if (count > 0) {
+    tiling_kernel<<<grid_for(count), 256, 0, ctx->stream>>>(d, g, (long long)first, (long long)count, S.ld, 1.0 / (double)g,
+                                                            ctx->lefts[0].as<double>(), ctx->lengths[0].as<double>());
+    ctx->launches++;
+  }
+  return shard_evaluate(ctx, bad);
+}
+
+pcb_status pcb_pagani_shard_count(pcb_ctx* ctx, int64_t* n_active, int64_t* n_retired) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  if (n_active) *n_active = ctx->shard.n;
+  if (n_retired) *n_retired = ctx->shard.n_ret;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_reduce(pcb_ctx* ctx, int32_t which, int64_t head, double* head_vals, int64_t* n_blocks,
+                                   double* block_sums, double* tail_vals, int64_t* n_tail) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  if (which < 0 || which > 3 || head < 0 || head >= kTreeSpan || !n_blocks || !n_tail)
+    return fail(ctx, PCB_INVALID, "shard_reduce: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  const long long n = which < 2 ? S.n : S.n_ret;
+  const double* src = (which == 0 ? ctx->est_i : which == 1 ? ctx->est_e : which == 2 ? ctx->ret_i : ctx->ret_e).as<double>();
+  const long long h = std::min<long long>(head, n);
+  const long long nb = (n - h) / kTreeSpan, tail = n - h - nb * kTreeSpan;
+  if (h > 0) PCB_CUDA_TRY(ctx, cudaMemcpyAsync(head_vals, src, (size_t)h * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (nb > 0) {
+    PCB_CUDA_TRY(ctx, ctx->tree[0].ensure((size_t)nb * sizeof(double)));
+    tree_level_kernel<<<(unsigned)nb, kTreeBlock, 0, ctx->stream>>>(src + h, nb * kTreeSpan, ctx->tree[0].as<double>());
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(block_sums, ctx->tree[0].p, (size_t)nb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (tail > 0)
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(tail_vals, src + h + nb * kTreeSpan, (size_t)tail * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  *n_blocks = nb;
+  *n_tail = tail;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_max_error(pcb_ctx* ctx, double* emax) {
+  if (!ctx || !ctx->shard.live || !emax) return fail(ctx, PCB_INVALID, "no live shard");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  double* sc = ctx->scalars.as<double>();
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc + S_EMAX, 0, sizeof(double), ctx->stream));
+  if (S.n > 0) {
+    max_kernel<<<(unsigned)std::min<long long>((S.n + 255) / 256, 1024), 256, 0, ctx->stream>>>(ctx->est_e.as<double>(), S.n, sc + S_EMAX);
+    ctx->launches++;
+  }
+  PCB_TRY(read_scalars(ctx, S_EMAX, 1));
+  *emax = ((double*)ctx->pinned)[S_EMAX];
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_classify(pcb_ctx* ctx, double budget, int32_t mode, double emax, int64_t* n_split) {
+  if (!ctx || !ctx->shard.live || !n_split) return fail(ctx, PCB_INVALID, "no live shard");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  S.n_split = 0;
+  S.classified = true;
+  *n_split = 0;
+  if (S.n == 0) return PCB_OK;
+  const long long nblk = (S.n + kScanBlock - 1) / kScanBlock;
+  PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)S.n));
+  PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));
+  PCB_CUDA_TRY(ctx, ctx->offsets.ensure((size_t)nblk * sizeof(unsigned long long)));
+  ClassifyArgs ca;
+  ca.n = S.n; ca.ld = S.ld; ca.d = S.f.d; ca.mode = mode; ca.budget = budget; ca.emax = emax;
+  ca.lengths = ctx->lengths[S.cur].as<double>();
+  ca.errors = ctx->est_e.as<double>();
+  ca.flags = ctx->flags.as<unsigned char>();
+  ca.block_counts = ctx->counts.as<unsigned int>();
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>();
+  classify_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(ca);
+  scan_counts_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->counts.as<unsigned int>(), (int)nblk, ctx->offsets.as<unsigned long long>(),
+                                                  sc_u + S_NSPLIT);
+  ctx->launches += 2;
+  PCB_TRY(read_scalars(ctx, S_NSPLIT, 1));
+  S.n_split = (long long)((unsigned long long*)ctx->pinned)[S_NSPLIT];
+  *n_split = S.n_split;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_split(pcb_ctx* ctx) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  if (!S.classified) return fail(ctx, PCB_INVALID, "shard_split needs a preceding shard_classify");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = S.f.d, nxt = S.cur ^ 1;
+  const long long n_child = 2 * S.n_split, n_ret = S.n - S.n_split, ld_out = round_up(std::max<long long>(n_child, 1), 32);
+  PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_out * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_out * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->ret_i.ensure((size_t)std::max<long long>(n_ret, 1) * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->ret_e.ensure((size_t)std::max<long long>(n_ret, 1) * sizeof(double)));
+  if (S.n > 0) {
+    SplitArgs sa;
+    sa.n = S.n; sa.ld_in = S.ld; sa.ld_out = ld_out; sa.d = d;
+    sa.lefts = ctx->lefts[S.cur].as<double>();
+    sa.lengths = ctx->lengths[S.cur].as<double>();
+    sa.integrals = ctx->est_i.as<double>();
+    sa.errors = ctx->est_e.as<double>();
+    sa.axes = ctx->est_k.as<int32_t>();
+    sa.flags = ctx->flags.as<unsigned char>();
+    sa.block_offsets = ctx->offsets.as<unsigned long long>();
+    sa.out_lefts = ctx->lefts[nxt].as<double>();
+    sa.out_lengths = ctx->lengths[nxt].as<double>();
+    sa.retired_i = ctx->ret_i.as<double>();
+    sa.retired_e = ctx->ret_e.as<double>();
+    split_kernel<<<(unsigned)((S.n + kScanBlock - 1) / kScanBlock), kScanBlock, 0, ctx->stream>>>(sa);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+  }
+  S.n_ret = n_ret;
+  S.n = n_child;
+  S.ld = ld_out;
+  S.cur = nxt;
+  S.classified = false;
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_export(pcb_ctx* ctx, int64_t begin, int64_t end, double* lefts_rows, double* lengths_rows) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  if (begin < 0 || end > S.n || begin > end) return fail(ctx, PCB_INVALID, "shard_export: range outside the local list");
+  const long long n = end - begin;
+  if (n == 0) return PCB_OK;
+  if (!lefts_rows || !lengths_rows) return fail(ctx, PCB_INVALID, "shard_export: NULL buffer");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = S.f.d;
+  const size_t bytes = (size_t)n * d * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->rows_a.ensure(bytes));
+  PCB_CUDA_TRY(ctx, ctx->rows_b.ensure(bytes));
+  soa_to_rows_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, begin, n, S.ld, ctx->lefts[S.cur].as<double>(), ctx->rows_a.as<double>());
+  soa_to_rows_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, begin, n, S.ld, ctx->lengths[S.cur].as<double>(), ctx->rows_b.as<double>());
+  ctx->launches += 2;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(lefts_rows, ctx->rows_a.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(lengths_rows, ctx->rows_b.p, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_rebuild(pcb_ctx* ctx, int64_t keep_begin, int64_t keep_end, int64_t n_front, const double* front_lefts,
+                                    const double* front_lengths, int64_t n_back, const double* back_lefts, const double* back_lengths) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  if (keep_begin < 0 || keep_end > S.n || keep_begin > keep_end || n_front < 0 || n_back < 0)
+    return fail(ctx, PCB_INVALID, "shard_rebuild: bad ranges");
+  if ((n_front > 0 && (!front_lefts || !front_lengths)) || (n_back > 0 && (!back_lefts || !back_lengths)))
+    return fail(ctx, PCB_INVALID, "shard_rebuild: NULL rows");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = S.f.d, nxt = S.cur ^ 1;
+  const long long keep = keep_end - keep_begin, n_new = n_front + keep + n_back;
+  if (n_front == 0 && n_back == 0 && keep_begin == 0 && keep_end == S.n) return PCB_OK;  // nothing moves
+  const long long ld_new = round_up(std::max<long long>(n_new, 1), 32);
+  PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_new * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_new * d * sizeof(double)));
+  if (keep > 0) {
+    soa_copy_kernel<<<grid_for(keep), 256, 0, ctx->stream>>>(d, keep, S.ld, keep_begin, ctx->lefts[S.cur].as<double>(), ld_new, n_front,
+                                                             ctx->lefts[nxt].as<double>());
+    soa_copy_kernel<<<grid_for(keep), 256, 0, ctx->stream>>>(d, keep, S.ld, keep_begin, ctx->lengths[S.cur].as<double>(), ld_new, n_front,
+                                                             ctx->lengths[nxt].as<double>());
+    ctx->launches += 2;
+  }
+  auto upload = [&](long long n, const double* l_rows, const double* h_rows, long long off) -> pcb_status {
+    if (n == 0) return PCB_OK;
+    const size_t bytes = (size_t)n * d * sizeof(double);
+    PCB_CUDA_TRY(ctx, ctx->rows_a.ensure(bytes));
+    PCB_CUDA_TRY(ctx, ctx->rows_b.ensure(bytes));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_a.p, l_rows, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_b.p, h_rows, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    rows_to_soa_at_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, n, ld_new, off, ctx->rows_a.as<double>(), ctx->lefts[nxt].as<double>());
+    rows_to_soa_at_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, n, ld_new, off, ctx->rows_b.as<double>(), ctx->lengths[nxt].as<double>());
+    ctx->launches += 2;
+    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // rows_a/rows_b are reused by the next upload
+    return PCB_OK;
+  };
+  PCB_TRY(upload(n_front, front_lefts, front_lengths, 0));
+  PCB_TRY(upload(n_back, back_lefts, back_lengths, n_front + keep));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  S.cur = nxt;
+  S.n = n_new;
+  S.ld = ld_new;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  return shard_evaluate(ctx, bad);
 }
 
 // quadrature.apply_rules for a single region: generic table, plain pair tree over all points.

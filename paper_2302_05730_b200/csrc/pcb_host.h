@@ -59,6 +59,16 @@ struct pcb_ctx {
   // scratch device buffers, grown on demand and reused across calls
   pcb::DevBuf lefts[2], lengths[2], est_i, est_e, est_k, flags, counts, offsets, ret_i, ret_e, tree[2], scalars;
   pcb::DevBuf rows_a, rows_b, k64;
+  // PAGANI shard state (pcb_pagani_shard_*)
+  struct Shard {
+    bool live = false;
+    pcb_integrand f;
+    pcb_rule rule;
+    pcb_pagani_config cfg;
+    int cur = 0;
+    long long n = 0, ld = 0, n_ret = 0, n_split = 0;
+    bool classified = false;
+  } shard;
   // roofline profiling (pcb_profile_begin/end)
   bool profiling = false;
   struct Span { cudaEvent_t a, b; };

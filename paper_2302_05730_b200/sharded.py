@@ -1,5 +1,15 @@
 """Multi-GPU drivers: one process per GPU, torch.distributed for the plumbing.
 
+PAGANI shards the ordered region list in contiguous slices.  Per iteration the ranks exchange
+  * tree-sum pieces of the active (and just-retired) integrals/errors: each rank reduces the
+    1024-aligned blocks of the GLOBAL index space that lie inside its slice and ships the ragged
+    head/tail elements raw, so every rank finishes engine.tree_sum's pair tree bit-identically
+    for any GPU count (estimate and errorest drive the classification, pagani.py:336-365);
+  * the split counts (region-cap test is global, pagani.py:367) and, only when nothing exceeds
+    its budget, the maximum error;
+  * region rows that change owner when the children are rebalanced to equal contiguous slices
+    (only rows that move travel; config 3 doubles every slice uniformly and moves nothing).
+
 m-Cubes shards the logical threads (hence the sub-cubes) across ranks on work-group
 boundaries.  Every draw is uniform(seed, thread, counter) (mcubes.py:224-232), so any
 partition reproduces the reference's sample set.  Per iteration the ranks exchange
@@ -74,6 +84,22 @@ class Comm:
     def barrier(self):
         self._dist.barrier(group=self.group)
 
+    def exchange_rows(self, sends: dict, recvs: dict, d: int) -> dict:
+        """Point-to-point exchange of region rows: sends[r] = (lefts, lengths) for rank r, recvs[r] = row
+        count expected from rank r.  Returns {r: (lefts, lengths)}.  (NCCL send/recv on GPUs, gloo on CPU.)"""
+        torch, dist = self._torch, self._dist
+        ops, bufs = [], {}
+        for r, (lefts, lengths) in sends.items():
+            t = self._to(np.stack([lefts, lengths]))
+            ops.append(dist.P2POp(dist.isend, t, r, group=self.group))
+        for r, n in recvs.items():
+            bufs[r] = torch.empty((2, n, d), dtype=torch.float64, device=self.device)
+            ops.append(dist.P2POp(dist.irecv, bufs[r], r, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return {r: (b[0].cpu().numpy(), b[1].cpu().numpy()) for r, b in bufs.items()}
+
 
 def group_shards(n_groups: int, world: int) -> list:
     """Contiguous, near-equal ranges of work-groups per rank: [(g0, g1), ...]."""
@@ -131,3 +157,155 @@ def mcubes_run_sharded(f, n, d, iterations, comm, backend=None, params=None, see
             break
     est, err, chi2 = combine_iterations(history)
     return MonteCarloResult(est, err, chi2, history, plan)
+
+
+# =============================================================================== PAGANI
+TREE_SPAN = 1024
+
+
+def global_tree_sum(comm, backend_tree_sum, pieces, counts):
+    """Finish engine.tree_sum over the concatenation of all ranks' arrays.
+
+    `pieces` = (head_vals, block_sums, tail_vals) of this rank for head = (-offset) mod 1024;
+    `counts` = element count of every rank.  Every rank returns the same float, bit-identical to a
+    single-device tree over the concatenated array (blocks of 2^10, then a pair tree over the block sums).
+    """
+    head, blocks, tail = pieces
+    width = max(1, max(c // TREE_SPAN + 1 for c in counts))
+    packed = np.zeros(3 + 2 * TREE_SPAN + width)
+    packed[0], packed[1], packed[2] = len(head), len(blocks), len(tail)
+    packed[3:3 + len(head)] = head
+    packed[3 + TREE_SPAN:3 + TREE_SPAN + len(tail)] = tail
+    packed[3 + 2 * TREE_SPAN:3 + 2 * TREE_SPAN + len(blocks)] = blocks
+    sums, carry = [], []
+    for part in comm.allgather(packed):
+        nh, nb, nt = int(part[0]), int(part[1]), int(part[2])
+        carry.extend(part[3:3 + nh])
+        if len(carry) == TREE_SPAN:
+            sums.append(backend_tree_sum(np.array(carry)))
+            carry = []
+        sums.extend(part[3 + 2 * TREE_SPAN:3 + 2 * TREE_SPAN + nb])
+        if nt:
+            assert not carry, "a tail can only follow a completed block"
+            carry = list(part[3 + TREE_SPAN:3 + TREE_SPAN + nt])
+    if carry:
+        sums.append(backend_tree_sum(np.array(carry)))   # last, zero-padded block
+    return backend_tree_sum(np.array(sums)) if sums else 0.0
+
+
+def _offsets(counts):
+    out, run = [], 0
+    for c in counts:
+        out.append(run)
+        run += c
+    return out, run
+
+
+def _even_ranges(total, world):
+    return [(total * r // world, total * (r + 1) // world) for r in range(world)]
+
+
+def rebalance(comm, shard, counts):
+    """Move region rows so that rank r owns global indices [N*r/W, N*(r+1)/W) of the ordered list."""
+    offsets, total = _offsets(counts)
+    me, world = comm.rank, comm.world
+    target = _even_ranges(total, world)
+    my0, my1 = offsets[me], offsets[me] + counts[me]
+    t0, t1 = target[me]
+    if all(offsets[r] == target[r][0] and counts[r] == target[r][1] - target[r][0] for r in range(world)):
+        return counts
+    d = shard.d
+    sends = {}
+    for r in range(world):           # my rows that belong to rank r
+        a, b = max(my0, target[r][0]), min(my1, target[r][1])
+        if r != me and a < b:
+            sends[r] = shard.export(a - my0, b - my0)
+    recvs = {}
+    for r in range(world):           # rows of rank r that belong to me
+        a, b = max(offsets[r], t0), min(offsets[r] + counts[r], t1)
+        if r != me and a < b:
+            recvs[r] = b - a
+    got = comm.exchange_rows(sends, recvs, d)
+    keep0, keep1 = max(my0, t0), min(my1, t1)
+    front = [got[r] for r in sorted(got) if r < me]
+    back = [got[r] for r in sorted(got) if r > me]
+    cat = lambda parts: (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts])) if parts else None
+    if keep0 < keep1:
+        shard.rebuild(keep0 - my0, keep1 - my0, cat(front), cat(back))
+    else:
+        shard.rebuild(0, 0, cat(front), cat(back))
+    return [b - a for a, b in target]
+
+
+def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None):
+    """refine (pagani.py:300-391) with the region list sharded over comm.world GPUs.
+
+    Every rank returns the same IntegralResult; histories are bit-identical to the single-GPU run
+    for any world size (same per-region values, same global pair trees, same classification).
+    """
+    from .cubature import IntegralResult, PaganiConfig
+    from .rules import build_rule, orbit_form
+
+    cfg = cfg or PaganiConfig()
+    if shard is None:
+        shard = _native.PaganiShard(f.device_spec(), orbit_form(rule or build_rule(f.d)), cfg)
+    d = shard.d
+    g = 1
+    while g**d < cfg.initial_regions:
+        g += 1
+    n0 = g**d
+    if n0 > cfg.region_cap:
+        from .domain import BudgetExceededError
+        raise BudgetExceededError(f"uniform split needs {n0} regions, cap is {cfg.region_cap}")
+    first, last = _even_ranges(n0, comm.world)[comm.rank]
+    shard.init(g, first, last - first)
+    counts = [b - a for a, b in _even_ranges(n0, comm.world)]
+    fin_i = fin_e = 0.0
+    fin_count, processed = 0, n0
+    history, converged, reason = [], False, ""
+    ret_counts = None
+
+    def tree(which, cnts):
+        offs, _ = _offsets(cnts)
+        head = (-offs[comm.rank]) % TREE_SPAN
+        return global_tree_sum(comm, shard.tree_sum, shard.reduce(which, head), cnts)
+
+    for iteration in range(cfg.max_iterations + 1):
+        if ret_counts is not None:                      # fin += tree_sum(act[~mask]) of the last split
+            fin_i += tree(2, ret_counts)
+            fin_e += tree(3, ret_counts)
+            ret_counts = None
+        n_active = sum(counts)
+        estimate = fin_i + tree(0, counts)
+        errorest = fin_e + tree(1, counts)
+        history.append((estimate, errorest, fin_count + n_active))
+        if progress is not None:
+            progress({"iteration": iteration, "n_regions": fin_count + n_active, "active": n_active,
+                      "estimate": estimate, "errorest": errorest})
+        if errorest <= cfg.rel_tol * abs(estimate):
+            converged, reason = True, "tolerance met"
+            break
+        if iteration == cfg.max_iterations:
+            reason = "max iterations reached"
+            break
+        if n_active == 0:
+            reason = "no active regions left"
+            break
+        budget = 0.8 * cfg.rel_tol * abs(estimate)
+        local_split = shard.classify(budget, 0, 0.0)
+        split_counts = [int(round(v[0])) for v in comm.allgather(np.array([float(local_split)]))]
+        if sum(split_counts) == 0:                      # force progress on the globally worst regions
+            emax = max(float(v[0]) for v in comm.allgather(np.array([shard.max_error()])))
+            local_split = shard.classify(budget, 1, emax)
+            split_counts = [int(round(v[0])) for v in comm.allgather(np.array([float(local_split)]))]
+        n_split = sum(split_counts)
+        if processed + 2 * n_split > cfg.region_cap:
+            reason = "region cap reached"
+            break
+        shard.split()
+        ret_counts = [c - s for c, s in zip(counts, split_counts)]
+        fin_count += n_active - n_split
+        processed += 2 * n_split
+        counts = rebalance(comm, shard, [2 * s for s in split_counts])
+        shard.evaluate()
+    return IntegralResult(estimate, errorest, len(history) - 1, processed, converged, history, reason)

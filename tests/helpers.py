@@ -20,3 +20,75 @@ def ulp_diff(a, b):
     a = np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
     b = np.ascontiguousarray(b, dtype=np.float64).view(np.int64)
     return np.abs(a - b)
+
+
+class ThreadComm:
+    """In-process stand-in for sharded.Comm: `world` threads exchange through shared slots.
+    Lets one GPU (or the CPU) run the SPMD drivers with several ranks."""
+
+    class _Shared:
+        def __init__(self, world):
+            import threading
+            self.world = world
+            self.barrier = threading.Barrier(world)
+            self.slots = [None] * world
+            self.mail = {}
+
+    def __init__(self, shared, rank):
+        self._s, self.rank, self.world = shared, rank, shared.world
+
+    @classmethod
+    def make(cls, world):
+        shared = cls._Shared(world)
+        return [cls(shared, r) for r in range(world)]
+
+    def allgather(self, a):
+        self._s.slots[self.rank] = np.array(a, dtype=np.float64)
+        self._s.barrier.wait()
+        out = [x.copy() for x in self._s.slots]
+        self._s.barrier.wait()
+        return out
+
+    def allreduce_sum(self, a):
+        parts = self.allgather(a)
+        total = parts[0].copy()
+        for p in parts[1:]:
+            total = total + p
+        return total
+
+    def barrier(self):
+        self._s.barrier.wait()
+
+    def exchange_rows(self, sends, recvs, d):
+        for r, (lefts, lengths) in sends.items():
+            self._s.mail[(self.rank, r)] = (np.array(lefts), np.array(lengths))
+        self._s.barrier.wait()
+        got = {r: self._s.mail[(r, self.rank)] for r in recvs}
+        self._s.barrier.wait()
+        for r in sends:
+            self._s.mail.pop((self.rank, r), None)
+        self._s.barrier.wait()
+        return got
+
+
+def run_ranks(world, fn):
+    """Run fn(rank, comm) on `world` threads; returns the list of results, re-raising the first failure."""
+    import threading
+    comms = ThreadComm.make(world)
+    out, err = [None] * world, []
+
+    def body(r):
+        try:
+            out[r] = fn(r, comms[r])
+        except BaseException as exc:  # noqa: BLE001
+            err.append(exc)
+            comms[r]._s.barrier.abort()
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if err:
+        raise err[0]
+    return out

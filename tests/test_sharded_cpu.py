@@ -82,3 +82,123 @@ def test_group_shards_cover_everything():
             assert shards[0][0] == 0 and shards[-1][1] == n_groups
             assert all(a[1] == b[0] for a, b in zip(shards, shards[1:]))
             assert max(b - a for a, b in shards) - min(b - a for a, b in shards) <= 1
+
+
+# ================================================================================ PAGANI
+class OraclePaganiShard:
+    """The shard-step interface of _native.PaganiShard, computed by the CPU oracle (test only)."""
+
+    def __init__(self, family, d, rule, cfg):
+        self.family, self.d, self.rule, self.cfg = family, d, rule, cfg
+        self.ret_i = self.ret_e = np.empty(0)
+
+    def init(self, g, first, count):
+        lefts, lengths = po.uniform_tiling(self.d, g)
+        self.lefts, self.lengths = lefts[first:first + count].copy(), lengths[first:first + count].copy()
+        self.evaluate()
+
+    def evaluate(self):
+        if len(self.lefts):
+            self.i, self.e, self.k = po.pagani_evaluate(self.family, self.lefts, self.lengths, self.rule)
+        else:
+            self.i, self.e, self.k = np.empty(0), np.empty(0), np.empty(0, dtype=np.int64)
+
+    def counts(self):
+        return len(self.lefts), len(self.ret_i)
+
+    def reduce(self, which, head):
+        a = (self.i, self.e, self.ret_i, self.ret_e)[which]
+        h = min(head, len(a))
+        nb = (len(a) - h) // 1024
+        blocks = np.array([po.tree_sum(a[h + 1024 * b:h + 1024 * (b + 1)]) for b in range(nb)])
+        return a[:h].copy(), blocks, a[h + 1024 * nb:].copy()
+
+    def max_error(self):
+        return float(self.e.max()) if len(self.e) else 0.0
+
+    def classify(self, budget, mode, emax):
+        if mode == 0:
+            self.mask = self.e > budget * np.prod(self.lengths, axis=1) if len(self.e) else np.zeros(0, dtype=bool)
+        else:
+            self.mask = self.e >= emax
+        return int(np.count_nonzero(self.mask))
+
+    def split(self):
+        m = self.mask
+        self.ret_i, self.ret_e = self.i[~m], self.e[~m]
+        if m.any():
+            self.lefts, self.lengths = po.bisect(self.lefts[m], self.lengths[m], self.k[m])
+        else:
+            self.lefts, self.lengths = np.empty((0, self.d)), np.empty((0, self.d))
+
+    def export(self, begin, end):
+        return self.lefts[begin:end].copy(), self.lengths[begin:end].copy()
+
+    def rebuild(self, keep_begin, keep_end, front, back):
+        parts_l, parts_h = [], []
+        for rows in (front, (self.lefts[keep_begin:keep_end], self.lengths[keep_begin:keep_end]), back):
+            if rows is not None and len(rows[0]):
+                parts_l.append(rows[0])
+                parts_h.append(rows[1])
+        self.lefts = np.concatenate(parts_l) if parts_l else np.empty((0, self.d))
+        self.lengths = np.concatenate(parts_h) if parts_h else np.empty((0, self.d))
+
+    def tree_sum(self, values):
+        return po.tree_sum(values)
+
+
+def _rule_from_golden(d):
+    import json
+
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "rules.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "golden.json")))["rules"][str(d)]
+    return dict(generators=z[f"gen{d}"], weights=z[f"w{d}"], axial_indices=z[f"ax{d}"],
+                split_weights=np.array([float.fromhex(v) for v in meta["split"]]),
+                null_degrees=tuple(meta["null_degrees"]), null_scales=tuple(meta["null_scales"]))
+
+
+def _pagani_worker(rank, world, port, family, d, cfg_kw, out_dir):
+    import torch.distributed as dist
+
+    from paper_2302_05730_b200 import sharded
+    from paper_2302_05730_b200.cubature import PaganiConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    sys_path_root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import sys
+    sys.path.insert(0, os.path.join(sys_path_root, "tests"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = sharded.Comm()
+        cfg = PaganiConfig(**cfg_kw)
+        shard = OraclePaganiShard(family, d, _rule_from_golden(d), cfg)
+        recs = []
+        res = sharded.pagani_refine_sharded(None, cfg, comm, shard=shard, progress=recs.append)
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), history=np.array(res.history), iterations=res.iterations,
+                 processed=res.regions_processed, converged=res.converged, reason=res.reason,
+                 active=[r["active"] for r in recs], final_local=len(shard.lefts))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("family,d,cfg_kw,world", [
+    ("f2", 3, dict(rel_tol=1e-5), 2),                                   # peaked: survivors concentrate -> rebalancing
+    ("f2", 3, dict(rel_tol=1e-3, max_iterations=20, initial_regions=16), 3),  # tiny lists, empty shards, forced progress
+    ("f4", 4, dict(rel_tol=1e-4), 3),
+    ("sum", 2, dict(rel_tol=1e-16, max_iterations=3), 2),               # everything splits: ragged 1024-block edges
+    ("f1", 5, dict(rel_tol=1e-6, region_cap=20000), 2),                 # region cap
+])
+def test_sharded_pagani_is_bit_identical_to_single_process(tmp_path, family, d, cfg_kw, world):
+    mp.spawn(_pagani_worker, args=(world, _free_port(), family, d, cfg_kw, str(tmp_path)), nprocs=world, join=True)
+    want = po.pagani_refine(family, d, _rule_from_golden(d), **cfg_kw)
+    ranks = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    for r in ranks:
+        assert str(r["reason"]) == want["reason"] and bool(r["converged"]) == want["converged"]
+        assert int(r["iterations"]) == want["iterations"] and int(r["processed"]) == want["regions_processed"]
+        assert list(r["active"]) == want["active_counts"]
+        got = [(float(a), float(b), int(c)) for a, b, c in r["history"]]
+        assert got == [(a, b, int(c)) for a, b, c in want["history"]]     # bit-identical estimates and errors
+    # the final lists are balanced to within one region
+    sizes = [int(r["final_local"]) for r in ranks]
+    assert max(sizes) - min(sizes) <= 1
