@@ -193,6 +193,12 @@ pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_
 pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points /* (n,d) */,
                            double* values /* (n) */);
 
+/* ---- serial integrand invocation micro-benchmark: replaces cli.cmd_bench_invoke's loop (cli.py:134-142;
+ * PAPER.md:451-455): blocks*threads device threads each evaluate all n points serially, keeping a running
+ * sum; ms_out[repetitions] are CUDA-event times, *accumulator is thread 0's sum (the reference's `acc`). */
+pcb_status pcb_bench_invoke(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points, int32_t blocks,
+                            int32_t threads, int32_t repetitions, double* ms_out, double* accumulator);
+
 /* ---- PAGANI evaluate: replaces pagani_kernel (pagani.py:227-257) ------------------------
  * lefts/lengths: (n,d) row-major as in RegionList (core.py:187-207); outputs as in
  * RegionEstimates (core.py:224-247): integrals, errors float64, split_axes int64.            */

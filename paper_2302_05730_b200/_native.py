@@ -104,6 +104,8 @@ SIGNATURES = {
     "pcb_profile_begin": (C.c_int, [C.c_void_p]),
     "pcb_profile_end": (C.c_int, [C.c_void_p, C.c_int32, _DP, C.POINTER(C.c_int64), _DP]),
     "pcb_eval_points": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_void_p]),
+    "pcb_bench_invoke": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                   C.c_void_p, _DP]),
     "pcb_pagani_evaluate": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
                                       C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(NonFiniteC)]),
@@ -564,3 +566,15 @@ class PaganiShard:
         out = C.c_double()
         self._call(self.ctx.lib.pcb_tree_sum, v.size, _ptr(v), C.byref(out))
         return out.value
+
+
+def bench_invoke(spec: DeviceSpec, points: np.ndarray, blocks: int, threads: int, repetitions: int, device=None):
+    ctx = context(device)
+    pts = _f64(points)
+    fc = spec.to_c()
+    ms = np.empty(repetitions)
+    acc = C.c_double()
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_bench_invoke(ctx.handle, C.byref(fc), pts.shape[0], _ptr(pts), int(blocks), int(threads),
+                                           int(repetitions), _ptr(ms), C.byref(acc)))
+    return ms, acc.value

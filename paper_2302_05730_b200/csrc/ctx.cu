@@ -11,6 +11,7 @@ namespace pcb {
 #define PCB_DECL(F, _) \
   const void* eval_kernel_fam##F(int d); \
   const void* points_kernel_fam##F(int d); \
+  const void* invoke_kernel_fam##F(int d); \
   const void* vsample_kernel_fam##F(int d, int rng);
 PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5, ) PCB_DECL(6, ) PCB_DECL(7, )
 #undef PCB_DECL
@@ -23,6 +24,8 @@ typedef const void* (*sample_getter)(int d, int rng);
 static const sample_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsample_kernel_fam1, vsample_kernel_fam2, vsample_kernel_fam3,
                                                       vsample_kernel_fam4, vsample_kernel_fam5, vsample_kernel_fam6, vsample_kernel_fam7};
 
+static const kernel_getter kInvoke[PCB_N_FAMILIES] = {invoke_kernel_fam0, invoke_kernel_fam1, invoke_kernel_fam2, invoke_kernel_fam3,
+                                                      invoke_kernel_fam4, invoke_kernel_fam5, invoke_kernel_fam6, invoke_kernel_fam7};
 const void* eval_kernel(int family, int d) { return kEval[family](d); }
 const void* points_kernel(int family, int d) { return kPoints[family](d); }
 const void* vsample_kernel_ptr(int family, int d, int rng) { return kSample[family](d, rng); }
@@ -186,6 +189,44 @@ pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, cons
   PCB_CUDA_TRY(ctx, cudaLaunchKernel(points_kernel(f->family, f->d), dim3(blocks), dim3(256), args, 0, ctx->stream));
   ctx->launches++;
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(values, out, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+pcb_status pcb_bench_invoke(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points, int32_t blocks,
+                            int32_t threads, int32_t repetitions, double* ms_out, double* accumulator) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  if (n < 1 || !points || blocks < 1 || threads < 1 || threads > 1024 || repetitions < 1 || !ms_out || !accumulator)
+    return fail(ctx, PCB_INVALID, "bench_invoke: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, ctx->rows_a.ensure((size_t)n * f->d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->rows_b.ensure((size_t)blocks * threads * sizeof(double)));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->rows_a.p, points, (size_t)n * f->d * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  const double* pts = ctx->rows_a.as<double>();
+  double* out = ctx->rows_b.as<double>();
+  long long nn = n;
+  pcb_integrand fv = *f;
+  void* args[] = {&fv, &nn, &pts, &out};
+  cudaEvent_t e0, e1;
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&e0));
+  PCB_CUDA_TRY(ctx, cudaEventCreate(&e1));
+  pcb_status st = PCB_OK;
+  for (int r = 0; r < repetitions && st == PCB_OK; ++r) {
+    cudaEventRecord(e0, ctx->stream);
+    cudaError_t err = cudaLaunchKernel(kInvoke[f->family](f->d), dim3(blocks), dim3(threads), args, 0, ctx->stream);
+    cudaEventRecord(e1, ctx->stream);
+    ctx->launches++;
+    if (err == cudaSuccess) err = cudaEventSynchronize(e1);
+    if (err != cudaSuccess) { st = fail(ctx, PCB_CUDA, "bench_invoke: %s", cudaGetErrorString(err)); break; }
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms_out[r] = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != PCB_OK) return st;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(accumulator, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return PCB_OK;
 }

@@ -362,4 +362,20 @@ __global__ void eval_points_kernel(const __grid_constant__ pcb_integrand f, long
   }
 }
 
+// Serial integrand invocation micro-benchmark (reference: cli.py:123-153): every
+// thread evaluates all n points one after the other and keeps a running sum.
+template <int FAM, int D>
+__global__ void invoke_kernel(const __grid_constant__ pcb_integrand f, long long n, const double* __restrict__ pts,
+                              double* __restrict__ acc_out) {
+  using F = Family<FAM>;
+  double acc = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    double x[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) x[j] = pts[i * D + j];
+    acc = acc + eval_at<F, D>(x, f);
+  }
+  acc_out[blockIdx.x * (long long)blockDim.x + threadIdx.x] = acc;
+}
+
 }  // namespace pcb

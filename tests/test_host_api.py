@@ -135,3 +135,24 @@ def test_no_cpu_fallback_and_no_oracle_in_product():
                 for line in text.splitlines():  # citations are fine, reading the tree at run time is not
                     if "/root/reference" in line:
                         assert not any(tok in line for tok in ("sys.path", "open(", "import ", "PYTHONPATH")), (name, line)
+
+
+def test_cli_argument_handling_matches_reference(capsys):
+    from paper_2302_05730_b200 import harness
+
+    assert harness.COMPARE_HEADER == "id,mean_a_ms,mean_b_ms,std_a,std_b,ratio"          # cli.py:33
+    assert harness.main(["integrate", "--integrator", "pagani", "--integrand", "f9", "-d", "5"]) == 2
+    assert harness.main(["integrate", "--integrator", "nope", "--integrand", "f1", "-d", "5"]) == 2
+    assert harness.main(["compare", "--config-a", "workers=1", "--config-b", "workers=8"]) == 2
+    assert harness.main(["bench-invoke", "--integrand", "f1", "-d", "3", "--points", "0"]) == 2
+    sc = harness.parse_scenario("pagani:f4:d=8:g=4:reps=5")
+    assert (sc["integrator"], sc["integrand"], sc["d"], sc["g"], sc["reps"]) == ("pagani", "f4", 8, 4, 5)
+    assert harness.parse_scenario("mcubes:f5:d=5:n=1e5:reps=5")["n"] == 100000
+    for bad in ("pagani:f4", "vegas:f4:d=3", "pagani:f9:d=3", "pagani:f4:g=3", "pagani:f4:d=3:zz=1", "pagani:f4:d=3:reps=0"):
+        with pytest.raises(harness.CliError):
+            harness.parse_scenario(bad)
+    cfg = harness.parse_config("workers=8,deterministic=false")
+    assert cfg.workers == 8 and cfg.deterministic is False
+    with pytest.raises(harness.CliError):
+        harness.parse_config("threads=8")
+    capsys.readouterr()
