@@ -439,7 +439,7 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
     fc, pc, bad = spec.to_c(), plan_to_c(plan, n_bins), NonFiniteC()
     its = (McubesIterationC * iterations)()
     n_done, seconds = C.c_int32(), C.c_double()
-    contribs = np.zeros((iterations, d, n_bins)) if keep_contributions else None
+    contribs = np.empty((iterations, d, n_bins)) if keep_contributions else None
     final_b = np.empty((d, n_bins + 1))
     failure = []
 

@@ -94,6 +94,8 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
     cudaStreamDestroy(ctx->stream);
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
+  for (auto ev : ctx->mc_events) cudaEventDestroy(ev);
   for (int k = 0; k < 3; ++k)
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
   for (auto& sp : ctx->span_pool) {
@@ -148,7 +150,6 @@ pcb_status pcb_profile_begin(pcb_ctx* ctx) {
   for (int k = 0; k < 3; ++k) {
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);
     ctx->spans[k].clear();
-    ctx->span_units[k] = 0;
   }
   ctx->profiling = true;
   return PCB_OK;
@@ -159,15 +160,16 @@ pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_
   ctx->profiling = false;
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  double total = 0;
+  double total = 0, total_units = 0;
   for (auto& sp : ctx->spans[kind]) {
     float ms = 0;
     PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, sp.a, sp.b));
     total += ms;
+    total_units += sp.units;
   }
   if (kernel_ms) *kernel_ms = total;
   if (launches) *launches = (int64_t)ctx->spans[kind].size();
-  if (units) *units = ctx->span_units[kind];
+  if (units) *units = total_units;
   return PCB_OK;
 }
 

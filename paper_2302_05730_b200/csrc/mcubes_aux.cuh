@@ -13,6 +13,7 @@ namespace pcb {
 // warp.  The d warps of a stream read the same records (L1/L2 hits on the contributions), two
 // records per lane and round.  Tables are merged stream -> CTA here, CTA -> grid by merge_hist_kernel.
 __global__ void __launch_bounds__(512, 3) bin_kernel(const __grid_constant__ BinArgs a, int d, int streams) {
+  if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb;
   const int W = blockDim.x >> 5;                                  // = d * streams
@@ -46,16 +47,19 @@ __global__ void __launch_bounds__(512, 3) bin_kernel(const __grid_constant__ Bin
     const bool same = b0 == b1;
     const double add0 = same ? w0 + w1 : w0, add1 = w1;
     unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
-#pragma unroll
+    // Arbitration rounds.  Only lanes that still have an update pending touch shared memory: the table is
+    // bound by shared-memory wavefronts (random 64-bit read-modify-write = ~10 wavefronts per warp), so the
+    // second round -- a handful of collision losers -- must not replay the loads of the whole warp.
+#pragma unroll 1
     for (int round = 0; round < 2; ++round) {
       if (want & 1u) tags[b0] = (unsigned char)lane;
       if (want & 2u) tags[b1] = (unsigned char)lane;
       __syncwarp();
-      const unsigned char t0 = tags[b0], t1 = tags[b1];
-      const double o0 = hist[b0], o1 = hist[b1];
-      const bool win0 = (want & 1u) && t0 == lane, win1 = (want & 2u) && t1 == lane;
-      if (win0) hist[b0] = o0 + add0;
-      if (win1) hist[b1] = o1 + add1;
+      bool win0 = false, win1 = false;
+      if (want & 1u) win0 = tags[b0] == lane;
+      if (want & 2u) win1 = tags[b1] == lane;
+      if (win0) hist[b0] = hist[b0] + add0;
+      if (win1) hist[b1] = hist[b1] + add1;
       want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
       __syncwarp();
       if (!__any_sync(PCB_FULL_MASK, want)) break;
@@ -79,13 +83,13 @@ __global__ void __launch_bounds__(512, 3) bin_kernel(const __grid_constant__ Bin
 
 
 // CTA tables -> contribution table in a fixed order: a CTA owns 32 bins; thread (chunk c, bin i) adds the
-// tables of blocks [c*per, (c+1)*per) serially, then the 32 chunk sums of a bin are added in chunk order.
-constexpr int kMergeChunks = 32;
-__global__ void __launch_bounds__(32 * kMergeChunks) merge_hist_kernel(const double* __restrict__ block_hist, int nblocks,
-                                                                       int nbins_total, double* __restrict__ out) {
-  __shared__ double s_part[kMergeChunks][33];
+// tables of blocks [c*per, (c+1)*per) serially, then the chunk sums of a bin are added in chunk order.
+constexpr int kReduceThreads = 256;
+constexpr int kMergeChunks = kReduceThreads / 32;
+__device__ __forceinline__ void merge_hist_cta(int cta, const double* __restrict__ block_hist, int nblocks, int nbins_total,
+                                               double* __restrict__ out, double* __restrict__ out_copy, double* s_part /* [kMergeChunks][33] */) {
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
+  const int i = cta * 32 + lane;
   const int per = (nblocks + kMergeChunks - 1) / kMergeChunks;
   const int b0 = c * per, b1 = min(nblocks, b0 + per);
   double t = 0.0;
@@ -101,42 +105,22 @@ __global__ void __launch_bounds__(32 * kMergeChunks) merge_hist_kernel(const dou
     }
     for (; b < b1; ++b) t = t + block_hist[(size_t)b * nbins_total + i];
   }
-  s_part[c][lane] = t;
+  s_part[c * 33 + lane] = t;
   __syncthreads();
   if (c == 0 && i < nbins_total) {
-    double r = s_part[0][lane];
+    double r = s_part[lane];
     const int used = (nblocks + per - 1) / per;
-    for (int k = 1; k < used; ++k) r = r + s_part[k][lane];
+    for (int k = 1; k < used; ++k) r = r + s_part[k * 33 + lane];
     out[i] = r;
+    if (out_copy) out_copy[i] = r;
   }
 }
 
-// final reduction of the per-work-group (I, E) pairs in group order with the pair tree of engine.tree_sum
-// (mcubes.py:292-293), for up to 1024 groups in one CTA; out[0] = integral, out[1] = variance sum
-__global__ void __launch_bounds__(512) group_pairs_tree_kernel(const double* __restrict__ pairs, int n, double* __restrict__ out) {
-  __shared__ double s[2][1024];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    s[0][i] = i < n ? pairs[2 * i] : 0.0;
-    s[1][i] = i < n ? pairs[2 * i + 1] : 0.0;
-  }
-  __syncthreads();
-  for (int half = 512; half >= 1; half >>= 1) {
-    double e = 0.0, v = 0.0;
-    const bool act = threadIdx.x < half;
-    if (act) { e = s[0][2 * threadIdx.x] + s[0][2 * threadIdx.x + 1]; v = s[1][2 * threadIdx.x] + s[1][2 * threadIdx.x + 1]; }
-    __syncthreads();
-    if (act) { s[0][threadIdx.x] = e; s[1][threadIdx.x] = v; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) { out[0] = s[0][0]; out[1] = s[1][0]; }
-}
-
-// per logical thread: serial sum of its segment partials; then one CTA per work-group reduces the
-// group's threads with the adjacent-pair tree (mcubes.py:255-259).  out[g][0..1] = (I_g, E_g).
-__global__ void group_tree_kernel(const double* __restrict__ seg_partials, int nseg, long long n_local_threads,
-                                  int group_size, int pow2, double* __restrict__ group_out) {
-  extern __shared__ double s[];  // [2][pow2]
-  const long long t0 = (long long)blockIdx.x * group_size;
+// per logical thread: serial sum of its segment partials; then the CTA reduces the work-group's threads with
+// the adjacent-pair tree (mcubes.py:255-259).  group_out[g][0..1] = (I_g, E_g).  s: [2][pow2] doubles.
+__device__ __forceinline__ void group_tree_cta(int group, const double* __restrict__ seg_partials, int nseg, long long n_local_threads,
+                                               int group_size, int pow2, double* __restrict__ group_out, double* s) {
+  const long long t0 = (long long)group * group_size;
   for (int i = threadIdx.x; i < pow2; i += blockDim.x) {
     double e = 0.0, v = 0.0;
     const long long t = t0 + i;
@@ -161,9 +145,54 @@ __global__ void group_tree_kernel(const double* __restrict__ seg_partials, int n
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    group_out[2 * blockIdx.x] = s[0];
-    group_out[2 * blockIdx.x + 1] = s[pow2];
+    group_out[2 * group] = s[0];
+    group_out[2 * group + 1] = s[pow2];
   }
+}
+
+// One launch after the accumulation: CTAs [0, merge_ctas) merge the per-CTA tables into the contribution
+// table (and into the run's per-iteration history slot), CTAs [merge_ctas, merge_ctas + n_groups) reduce one
+// work-group each.
+struct ReduceArgs {
+  const int* stop;               // iteration at which the run stopped (INT_MAX while running); may be NULL
+  int iteration;
+  const double* block_hist;
+  int nblocks, nbins_total, merge_ctas;
+  double* contrib;
+  double* contrib_copy;          // optional
+  const double* seg_partials;
+  int nseg, group_size, pow2;
+  long long n_local_threads;
+  double* group_out;
+};
+__global__ void __launch_bounds__(kReduceThreads) reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  if (a.stop && a.iteration > *a.stop) return;
+  extern __shared__ double s_dyn[];  // max(kMergeChunks*33, 2*pow2) doubles
+  if ((int)blockIdx.x < a.merge_ctas)
+    merge_hist_cta(blockIdx.x, a.block_hist, a.nblocks, a.nbins_total, a.contrib, a.contrib_copy, s_dyn);
+  else
+    group_tree_cta(blockIdx.x - a.merge_ctas, a.seg_partials, a.nseg, a.n_local_threads, a.group_size, a.pow2, a.group_out, s_dyn);
+}
+
+// final reduction of the per-work-group (I, E) pairs in group order with the pair tree of engine.tree_sum
+// (mcubes.py:292-293), for up to 1024 groups in one CTA; returns (integral, variance sum) on thread 0.
+// s: [2][1024] doubles; blockDim.x >= 512.
+__device__ __forceinline__ void group_pairs_tree_cta(const double* __restrict__ pairs, int n, double* s, double& integral, double& variance) {
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
+    s[i] = i < n ? pairs[2 * i] : 0.0;
+    s[1024 + i] = i < n ? pairs[2 * i + 1] : 0.0;
+  }
+  __syncthreads();
+  for (int half = 512; half >= 1; half >>= 1) {
+    double e = 0.0, v = 0.0;
+    const bool act = threadIdx.x < half;
+    if (act) { e = s[2 * threadIdx.x] + s[2 * threadIdx.x + 1]; v = s[1024 + 2 * threadIdx.x] + s[1024 + 2 * threadIdx.x + 1]; }
+    __syncthreads();
+    if (act) { s[threadIdx.x] = e; s[1024 + threadIdx.x] = v; }
+    __syncthreads();
+  }
+  integral = s[0];
+  variance = s[1024];
 }
 
 // transform_many (vegas_grid.py:99-114) for caller-supplied points; flags[0] set on y outside [0,1)
@@ -201,27 +230,33 @@ __global__ void deinterleave2_kernel(const double* __restrict__ in, int n, doubl
 
 // ------------------------------------------------------------------------------------------
 // refine_grid (vegas_grid.py:142-193): one CTA per axis.
-// numpy's pairwise float sum of an n-vector (n <= 128*k blocks) restated serially.
+// numpy's pairwise float sum of an n-vector restated for ONE WARP (all 32 lanes call it with the same
+// arguments): numpy splits recursively down to blocks of <= 128 elements, sums a block with 8 strided
+// accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and adds the tail serially.  Lanes 0..7
+// play the 8 accumulators (their chains are independent), the combine is three xor-shuffles.
 // ------------------------------------------------------------------------------------------
-__device__ inline double np_pairwise_sum(const double* a, int n) {
+__device__ inline double np_pairwise_sum_warp(const double* a, int n) {
+  const int lane = threadIdx.x & 31;
   if (n < 8) {
     double r = 0.0;  // numpy starts from the first element; 0.0 + a[0] == a[0] for these inputs (a >= 0)
     for (int i = 0; i < n; ++i) r = (i == 0) ? a[0] : r + a[i];
     return r;
   }
   if (n <= 128) {
-    double r[8];
-    for (int k = 0; k < 8; ++k) r[k] = a[k];
-    int i;
-    for (i = 8; i < n - (n % 8); i += 8)
-      for (int k = 0; k < 8; ++k) r[k] = r[k] + a[i + k];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; ++i) res = res + a[i];
-    return res;
+    const int k = lane & 7, body = n - (n % 8);
+    double r = a[k];
+    for (int i = 8; i < body; i += 8) r = r + a[i + k];
+    r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 1);
+    r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 2);
+    r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 4);
+    for (int i = body; i < n; ++i) r = r + a[i];
+    return r;
   }
   int n2 = n / 2;
   n2 -= n2 % 8;
-  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+  const double lo = np_pairwise_sum_warp(a, n2);
+  const double hi = np_pairwise_sum_warp(a + n2, n - n2);
+  return lo + hi;
 }
 
 struct RefineArgs {
@@ -233,26 +268,21 @@ struct RefineArgs {
   double* new_boundaries;       // [d][n+1]
 };
 
-__global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant__ RefineArgs a) {
-  extern __shared__ double sh[];
-  const int n = a.n, j = blockIdx.x, tid = threadIdx.x;
+// sh: (4n + 4) doubles of shared memory; blockDim.x threads cooperate on axis j
+__device__ __forceinline__ void refine_axis_cta(const RefineArgs& a, int j, double* sh) {
+  const int n = a.n, tid = threadIdx.x;
   double* c = sh;              // [n]   smoothed contributions
   double* w = c + n;           // [n]   damped weights
   double* cw = w + n;          // [n+1] cumulative weights
   double* row = cw + n + 1;    // [n+1] new boundaries
-  __shared__ double s_total, s_wsum;
-  __shared__ int s_any;
+  double* s_scal = row + n + 1;  // [2] total, wsum
   const double* src = a.contrib + (size_t)j * n;
   const double* old = a.boundaries + (size_t)j * (n + 1);
   double* dst = a.new_boundaries + (size_t)j * (n + 1);
 
-  if (tid == 0) s_any = 0;
-  __syncthreads();
   int any = 0;
   for (int i = tid; i < n; i += blockDim.x) any |= (src[i] > 0.0);
-  if (any) atomicOr(&s_any, 1);
-  __syncthreads();
-  if (!s_any) {  // axis untouched (vegas_grid.py:156-157)
+  if (!__syncthreads_or(any)) {  // axis untouched (vegas_grid.py:156-157)
     for (int i = tid; i <= n; i += blockDim.x) dst[i] = old[i];
     return;
   }
@@ -268,9 +298,12 @@ __global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant_
     c[i] = v;
   }
   __syncthreads();
-  if (tid == 0) s_total = np_pairwise_sum(c, n);
+  if (tid < 32) {
+    const double t = np_pairwise_sum_warp(c, n);
+    if (tid == 0) s_scal[0] = t;
+  }
   __syncthreads();
-  const double total = s_total;
+  const double total = s_scal[0];
   for (int i = tid; i < n; i += blockDim.x) {
     const double r = c[i] / total;
     double ww = 0.0;
@@ -279,25 +312,27 @@ __global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant_
     w[i] = ww;
   }
   __syncthreads();
-  if (tid == 0) {
-    const double wsum = np_pairwise_sum(w, n);
-    s_wsum = wsum;
-    double run = w[0];
-    cw[0] = 0.0;
-    cw[1] = run;
-    int i = 1;
-    for (; i + 8 <= n; i += 8) {  // np.cumsum: serial adds, loads batched so only the DADD chain is exposed
-      double v[8];
+  if (tid < 32) {
+    const double wsum = np_pairwise_sum_warp(w, n);
+    if (tid == 0) {
+      s_scal[1] = wsum;
+      double run = w[0];
+      cw[0] = 0.0;
+      cw[1] = run;
+      int i = 1;
+      for (; i + 8 <= n; i += 8) {  // np.cumsum: serial adds, loads batched so only the DADD chain is exposed
+        double v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = w[i + k];
+        for (int k = 0; k < 8; ++k) v[k] = w[i + k];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) { run = run + v[k]; cw[i + k + 1] = run; }
+        for (int k = 0; k < 8; ++k) { run = run + v[k]; cw[i + k + 1] = run; }
+      }
+      for (; i < n; ++i) { run = run + w[i]; cw[i + 1] = run; }
+      cw[n] = wsum;
     }
-    for (; i < n; ++i) { run = run + w[i]; cw[i + 1] = run; }
-    cw[n] = wsum;
   }
   __syncthreads();
-  const double wsum = s_wsum;
+  const double wsum = s_scal[1];
   if (!(wsum > 0.0)) {
     for (int i = tid; i <= n; i += blockDim.x) dst[i] = old[i];
     return;
@@ -333,6 +368,94 @@ __global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant_
   }
   __syncthreads();
   for (int i = tid; i <= n; i += blockDim.x) dst[i] = row[i];
+}
+
+__global__ void __launch_bounds__(512) refine_grid_kernel(const __grid_constant__ RefineArgs a) {
+  extern __shared__ double sh[];
+  refine_axis_cta(a, blockIdx.x, sh);
+}
+
+// ------------------------------------------------------------------------------------------
+// End of an m-Cubes iteration, one launch: CTA j < n_refine refines axis j of the grid
+// (vegas_grid.py:142-193); the last CTA finishes the group-order pair tree (mcubes.py:292-293),
+// publishes the iteration record to pinned host memory, re-arms the pass scalars and decides
+// whether the run has reached its tolerance (combine_iterations, mcubes.py:311-329).
+// ------------------------------------------------------------------------------------------
+struct McRecord {               // host-visible (pinned) record of one iteration
+  double integral, variance;
+  unsigned long long clamps, bad;
+  int stop, pad;
+  volatile unsigned long long seq;  // written last: run token << 20 | (iteration + 1)
+};
+
+struct FinishArgs {
+  RefineArgs refine;
+  int n_refine;                 // d when the grid adapts, else 0
+  int* stop;                    // iteration at which the run stopped (INT_MAX while running); NULL outside pcb_mcubes_run
+  const double* group_pairs;    // [n_groups][2]
+  int n_groups;                 // <= 1024, or 0 when the sums are already in scalars[M_INTEGRAL..]
+  unsigned long long* scalars;  // pass scalars: bad, clamps, integral, variance
+  double* hist_i;               // run history of (integral, variance), capacity = iterations
+  double* hist_v;
+  int iteration;
+  double rel_tol;
+  McRecord* record;             // pinned host memory (nullptr: leave the results in scalars only)
+  unsigned long long seq;
+};
+
+__global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ FinishArgs a) {
+  // kernels of iteration `it` run iff it <= *stop, so the refinement CTAs of the stopping iteration itself are
+  // unaffected by the decision taken by the last CTA of this very launch
+  if (a.stop && a.iteration > *a.stop) return;
+  extern __shared__ double sh[];
+  if ((int)blockIdx.x < a.n_refine) {
+    refine_axis_cta(a.refine, blockIdx.x, sh);
+    return;
+  }
+  double integral, variance;
+  double* sc_d = reinterpret_cast<double*>(a.scalars);
+  if (a.n_groups > 0) {
+    group_pairs_tree_cta(a.group_pairs, a.n_groups, sh, integral, variance);
+  } else {
+    integral = sc_d[2];
+    variance = sc_d[3];
+  }
+  if (threadIdx.x != 0) return;
+  sc_d[2] = integral;
+  sc_d[3] = variance;
+  const unsigned long long bad = a.scalars[0], clamps = a.scalars[1];
+  int stop = bad != ~0ULL;
+  if (a.hist_i) {
+    const double var = fmax(variance, 0.0);
+    a.hist_i[a.iteration] = integral;
+    a.hist_v[a.iteration] = var;
+    if (a.rel_tol > 0.0) {
+      double wsum = 0.0, dot = 0.0;
+      for (int i = 0; i <= a.iteration; ++i) {
+        const double w = 1.0 / fmax(a.hist_v[i], 1e-30);
+        wsum = wsum + w;
+        dot = dot + w * a.hist_i[i];
+      }
+      const double est = dot / wsum, err = 1.0 / sqrt(wsum);
+      if (err <= a.rel_tol * fabs(est)) stop = 1;
+    }
+    // re-arm the scalars for the next pass of the run
+    a.scalars[0] = ~0ULL;
+    a.scalars[1] = 0ULL;
+  }
+  if (a.record) {
+    a.record->integral = integral;
+    a.record->variance = variance;
+    a.record->clamps = clamps;
+    a.record->bad = bad;
+    a.record->stop = stop;
+    __threadfence_system();
+    a.record->seq = a.seq;
+  }
+  if (a.stop && stop) {
+    __threadfence();
+    *a.stop = a.iteration;
+  }
 }
 
 }  // namespace pcb

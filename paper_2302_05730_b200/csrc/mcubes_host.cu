@@ -5,6 +5,7 @@
 #include "pcb_host.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -60,9 +61,61 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
   const long long seg_len = (plan->s + nseg - 1) / nseg;
   out->seg_len = seg_len;
   out->nseg = (int)((plan->s + seg_len - 1) / seg_len);
-  const long long units = n_lw * out->nseg;
+  const long long units = (n_local_threads * out->nseg + 31) / 32;
   out->blocks = (int)std::max<long long>(1, std::min<long long>(2LL * ctx->sm_count, (units + kSampleWarps - 1) / kSampleWarps));
   return PCB_OK;
+}
+
+// Multiplier A of the lane -> segment map sigma = ((u*32 + lane) * A) mod N (mcubes_kernels.cuh).  Lane-to-lane
+// offset in sub-cubes is ~A*seg_len; the ideal offset is (1,1,...,1) in base g, which gives the 32 lanes of a warp
+// different coordinates -- hence different importance-grid windows -- on every axis.  Candidates around that
+// value (coprime to N) are scored by counting equal-coordinate lane pairs over a few sample units.
+static unsigned long long choose_segment_multiplier(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long long t_begin, long long nt,
+                                                    int nseg, long long seg_len) {
+  const long long N = nt * nseg;
+  if (N <= 1 || N >= (1LL << 31)) return 1;  // (u*32+lane)*A must stay below 2^63
+  const std::array<long long, 6> key = {plan->g * 100 + plan->d, plan->s, t_begin, nt, nseg, seg_len};
+  auto hit = ctx->mc_multipliers.find(key);
+  if (hit != ctx->mc_multipliers.end()) return hit->second;
+  const int d = plan->d;
+  const long long g = plan->g;
+  auto gcd = [](long long a, long long b) { while (b) { long long t = a % b; a = b; b = t; } return a; };
+  auto score = [&](long long A) {
+    long long total = 0;
+    const long long units = (N + 31) / 32;
+    for (int smp = 0; smp < 8; ++smp) {
+      const long long u = units * smp / 8;
+      int coords[32][PCB_MAX_DIM];
+      int live = 0;
+      for (int lane = 0; lane < 32; ++lane) {
+        const long long sin = u * 32 + lane;
+        if (sin >= N) break;
+        const long long sigma = (long long)(((unsigned __int128)sin * (unsigned __int128)A) % (unsigned __int128)N);
+        long long cube = (t_begin + sigma / nseg) * plan->s + (sigma % nseg) * seg_len;
+        for (int j = d - 1; j >= 0; --j) { coords[lane][j] = (int)(cube % g); cube /= g; }
+        ++live;
+      }
+      for (int j = 0; j < d; ++j)
+        for (int x = 0; x < live; ++x)
+          for (int y = x + 1; y < live; ++y) total += coords[x][j] == coords[y][j];
+    }
+    return total;
+  };
+  long long delta = 0;  // (1,1,...,1) in base g
+  for (int j = 0; j < d; ++j) delta = delta * g + 1;
+  std::vector<long long> cands = {1};
+  const long long base = std::max<long long>(1, delta / std::max<long long>(1, seg_len));
+  for (long long k = -48; k <= 48; ++k) cands.push_back(base + k);
+  for (long long k = -8; k <= 8; ++k) { cands.push_back((long long)(N * 0.6180339887) + k); cands.push_back((long long)(N * 0.3819660113) + k); }
+  long long best = 1, best_score = -1;
+  for (long long c : cands) {
+    long long A = ((c % N) + N) % N;
+    if (A < 1 || gcd(A, N) != 1) continue;
+    const long long sc = score(A);
+    if (best_score < 0 || sc < best_score) { best = A; best_score = sc; }
+  }
+  ctx->mc_multipliers[key] = (unsigned long long)best;
+  return (unsigned long long)best;
 }
 
 static pcb_status read_mc_scalars(pcb_ctx* ctx) {
@@ -72,12 +125,40 @@ static pcb_status read_mc_scalars(pcb_ctx* ctx) {
   return PCB_OK;
 }
 
-// One V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries.
-// Leaves: contributions in ctx->mc_contrib (d*nb), per-group (I, Var) in ctx->mc_group,
-// scalars (bad, clamps, integral, variance) in ctx->scalars[kMcSlot..].
-static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, const double* bounds_dev,
-                             unsigned long long seed, int rng_kind, const double* injected_dev, int squared_weighted,
-                             long long t_begin, long long t_end, long long* n_groups_out) {
+static pcb_status grant_smem(pcb_ctx* ctx, const void* fn, size_t bytes) {
+  size_t& have = ctx->smem_attr[fn];  // cudaFuncSetAttribute is not free: once per kernel and size
+  if (have < bytes) {
+    PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
+  return PCB_OK;
+}
+
+// What the end-of-pass launch does besides the group-order tree: grid refinement, the iteration record
+// and the stop decision of pcb_mcubes_run.
+struct PassTail {
+  int iteration = 0;
+  int* stop = nullptr;                 // device; run only
+  bool refine = false;
+  double alpha = 1.5;
+  int smoothing = 1;
+  const double* bounds_in = nullptr;   // device
+  double* bounds_out = nullptr;        // device
+  double* contrib_copy = nullptr;      // device slot of the run's per-iteration tables (optional)
+  double* hist_i = nullptr;            // device run history
+  double* hist_v = nullptr;
+  double rel_tol = 0.0;
+  McRecord* record = nullptr;          // pinned
+  unsigned long long seq = 0;
+};
+
+// Enqueue one V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries; nothing
+// here waits for the device.  Leaves: contributions in ctx->mc_contrib (d*nb), per-group (I, Var) in
+// ctx->mc_group, scalars (bad, clamps, integral, variance) in ctx->scalars[kMcSlot..]; with tail.hist_i set
+// the scalars bad/clamps are re-armed by the device for the next pass.
+static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, const double* bounds_dev,
+                               unsigned long long seed, int rng_kind, const double* injected_dev, int squared_weighted,
+                               long long t_begin, long long t_end, const PassTail& tail, long long* n_groups_out) {
   const int d = plan->d, nb = plan->n_bins;
   const long long n_threads = (plan->m + plan->s - 1) / plan->s;
   if (t_begin < 0 || t_end > n_threads || t_begin >= t_end)
@@ -89,16 +170,11 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   PCB_TRY(plan_launch(ctx, plan, nt, &L));
   const void* fn = vsample_kernel_ptr(f->family, d, rng_kind);
   const void* bin_fn = (const void*)&bin_kernel;
-  for (auto kv : {std::make_pair(fn, L.smem), std::make_pair(bin_fn, L.bin_smem)}) {
-    size_t& have = ctx->smem_attr[kv.first];  // cudaFuncSetAttribute is not free: once per kernel and size
-    if (have < kv.second) {
-      PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(kv.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kv.second));
-      have = kv.second;
-    }
-  }
+  PCB_TRY(grant_smem(ctx, fn, L.smem));
+  PCB_TRY(grant_smem(ctx, bin_fn, L.bin_smem));
 
   // record buffer: one contribution (8 B) + d bin ids (2 B each) per sample slot, chunked over work units
-  const long long n_lw = (nt + 31) / 32, units = n_lw * L.nseg;
+  const long long n_segments = nt * L.nseg, units = (n_segments + 31) / 32;
   const long long rec_per_unit = round_up(L.seg_len * plan->p, 2) * 32;  // even number of 32-record groups
   const size_t rec_bytes = 8 + 2 * (size_t)d;
   size_t budget = (size_t)24 << 30;
@@ -120,8 +196,6 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   PCB_CUDA_TRY(ctx, ctx->mc_group.ensure((size_t)n_groups * 4 * sizeof(double)));
   unsigned long long* sc_u = ctx->scalars.as<unsigned long long>() + kMcSlot;
   double* sc = ctx->scalars.as<double>() + kMcSlot;
-  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
-  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_CLAMPS, 0, sizeof(unsigned long long), ctx->stream));
 
   SampleArgs a;
   a.f = *f;
@@ -129,7 +203,11 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   a.m = plan->m; a.s = plan->s;
   a.n_threads = n_threads;
   a.t_begin = t_begin; a.t_end = t_end;
-  a.n_lw = n_lw;
+  a.n_segments = n_segments;
+  a.seg_mul = choose_segment_multiplier(ctx, plan, t_begin, nt, L.nseg, L.seg_len);
+  a.div_segments = make_fastdiv((unsigned long long)n_segments);
+  a.div_nseg = make_fastdiv((unsigned long long)L.nseg);
+  a.div_g = make_fastdiv((unsigned long long)plan->g);
   a.nseg = L.nseg;
   a.rng_kind = rng_kind;
   a.seg_len = L.seg_len;
@@ -153,6 +231,8 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   a.rec_capacity = rec_capacity;
   a.rec_w = ctx->mc_rec.as<double>();
   a.rec_b = reinterpret_cast<unsigned short*>(ctx->mc_rec.as<double>() + rec_capacity);
+  a.stop = tail.stop;
+  a.iteration = tail.iteration;
 
   BinArgs b;
   b.nb = nb;
@@ -160,6 +240,8 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   b.rec_w = a.rec_w;
   b.rec_b = a.rec_b;
   b.block_hist = ctx->mc_hist.as<double>();
+  b.stop = tail.stop;
+  b.iteration = tail.iteration;
 
   for (long long u0 = 0, chunk = 0; u0 < units; u0 += chunk_units, ++chunk) {
     a.unit_begin = u0;
@@ -171,7 +253,7 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
       // units of work for the roofline: the samples actually drawn (active lanes) in this chunk
       const double frac = (double)n_units / (double)units;
       const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
-      ProfileSpan span(ctx, 1, frac * (double)(c1 - c0) * plan->p);
+      ProfileSpan span(ctx, 1, frac * (double)(c1 - c0) * plan->p, tail.iteration);
       PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
       ctx->launches++;
     }
@@ -180,24 +262,40 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
     int d_arg = d, streams_arg = L.bin_warps / d;
     void* bargs[] = {&b, &d_arg, &streams_arg};
     {
-      ProfileSpan span(ctx, 2, (double)b.n_groups * 32.0);
+      ProfileSpan span(ctx, 2, (double)b.n_groups * 32.0, tail.iteration);
       PCB_CUDA_TRY(ctx, cudaLaunchKernel(bin_fn, dim3(bin_blocks), dim3(L.bin_warps * 32), bargs, L.bin_smem, ctx->stream));
       ctx->launches++;
     }
   }
-  merge_hist_kernel<<<(d * nb + 31) / 32, 32 * kMergeChunks, 0, ctx->stream>>>(ctx->mc_hist.as<double>(), bin_blocks, d * nb,
-                                                                                ctx->mc_contrib.as<double>());
+
+  // table merge + work-group trees in one launch
   int pow2 = 1;
   while (pow2 < plan->group_size) pow2 <<= 1;
-  const int gt_threads = std::max(32, std::min(256, pow2 / 2));
-  group_tree_kernel<<<(unsigned)n_groups, gt_threads, 2 * pow2 * sizeof(double), ctx->stream>>>(
-      ctx->mc_seg.as<double>(), L.nseg, nt, plan->group_size, pow2, ctx->mc_group.as<double>());
-  ctx->launches += 2;
-  if (n_groups <= 1024) {  // engine.reduce in group order (mcubes.py:292-293), both sums in one small CTA
-    group_pairs_tree_kernel<<<1, 512, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, sc + M_INTEGRAL);
-    ctx->launches++;
-    PCB_CUDA_TRY(ctx, cudaGetLastError());
-  } else {
+  ReduceArgs r;
+  r.stop = tail.stop;
+  r.iteration = tail.iteration;
+  r.block_hist = ctx->mc_hist.as<double>();
+  r.nblocks = bin_blocks;
+  r.nbins_total = d * nb;
+  r.merge_ctas = (d * nb + 31) / 32;
+  r.contrib = ctx->mc_contrib.as<double>();
+  r.contrib_copy = tail.contrib_copy;
+  r.seg_partials = ctx->mc_seg.as<double>();
+  r.nseg = L.nseg;
+  r.group_size = plan->group_size;
+  r.pow2 = pow2;
+  r.n_local_threads = nt;
+  r.group_out = ctx->mc_group.as<double>();
+  const size_t reduce_smem = std::max<size_t>((size_t)kMergeChunks * 33, (size_t)2 * pow2) * sizeof(double);
+  PCB_TRY(grant_smem(ctx, (const void*)&reduce_kernel, reduce_smem));
+  reduce_kernel<<<(unsigned)(r.merge_ctas + n_groups), kReduceThreads, reduce_smem, ctx->stream>>>(r);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+
+  FinishArgs fa;
+  fa.n_groups = (int)n_groups;
+  if (n_groups > 1024) {  // engine.reduce in group order over more groups than one CTA holds (never with the default plans)
+    if (tail.stop) return fail(ctx, PCB_INVALID, "mcubes_run supports at most 1024 work-groups (%lld requested)", n_groups);
     double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
     double* ge = gi + n_groups;
     deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
@@ -205,8 +303,34 @@ static pcb_status sample_dev(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
     PCB_CUDA_TRY(ctx, cudaGetLastError());
     PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));
     PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
+    fa.n_groups = 0;
   }
+  fa.refine.d = d; fa.refine.n = nb; fa.refine.alpha = tail.alpha; fa.refine.smoothing = tail.smoothing;
+  fa.refine.boundaries = tail.bounds_in; fa.refine.contrib = ctx->mc_contrib.as<double>(); fa.refine.new_boundaries = tail.bounds_out;
+  fa.n_refine = tail.refine ? d : 0;
+  fa.stop = tail.stop;
+  fa.group_pairs = ctx->mc_group.as<double>();
+  fa.scalars = sc_u;
+  fa.hist_i = tail.hist_i;
+  fa.hist_v = tail.hist_v;
+  fa.iteration = tail.iteration;
+  fa.rel_tol = tail.rel_tol;
+  fa.record = tail.record;
+  fa.seq = tail.seq;
+  const size_t finish_smem = std::max<size_t>((size_t)(4 * nb + 4), 2048) * sizeof(double);
+  if (finish_smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
+  PCB_TRY(grant_smem(ctx, (const void*)&finish_kernel, finish_smem));
+  finish_kernel<<<fa.n_refine + 1, 512, finish_smem, ctx->stream>>>(fa);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
   if (n_groups_out) *n_groups_out = n_groups;
+  return PCB_OK;
+}
+
+static pcb_status arm_pass_scalars(pcb_ctx* ctx) {
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>() + kMcSlot;
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + M_CLAMPS, 0, sizeof(unsigned long long), ctx->stream));
   return PCB_OK;
 }
 
@@ -228,9 +352,9 @@ static pcb_status refine_dev(pcb_ctx* ctx, int d, int nb, const double* bounds_d
   RefineArgs r;
   r.d = d; r.n = nb; r.alpha = alpha; r.smoothing = smoothing;
   r.boundaries = bounds_dev; r.contrib = contrib_dev; r.new_boundaries = out_dev;
-  const size_t smem = (size_t)(4 * nb + 2) * sizeof(double);
+  const size_t smem = (size_t)(4 * nb + 4) * sizeof(double);
   if (smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
-  PCB_CUDA_TRY(ctx, cudaFuncSetAttribute((const void*)refine_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PCB_TRY(grant_smem(ctx, (const void*)&refine_grid_kernel, smem));
   refine_grid_kernel<<<d, 512, smem, ctx->stream>>>(r);
   ctx->launches++;
   PCB_CUDA_TRY(ctx, cudaGetLastError());
@@ -266,8 +390,9 @@ pcb_status pcb_mcubes_sample(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
     inj = ctx->mc_inject.as<double>();
   }
   long long n_groups = 0;
-  PCB_TRY(sample_dev(ctx, f, plan, ctx->mc_bounds[0].as<double>(), seed, rng_kind, inj, squared_weighted, thread_begin,
-                     thread_end, &n_groups));
+  PCB_TRY(arm_pass_scalars(ctx));
+  PCB_TRY(enqueue_pass(ctx, f, plan, ctx->mc_bounds[0].as<double>(), seed, rng_kind, inj, squared_weighted, thread_begin,
+                       thread_end, PassTail{}, &n_groups));
   PCB_TRY(read_mc_scalars(ctx));
   const unsigned long long* hu = (const unsigned long long*)ctx->pinned + kMcSlot;
   const double* hd = (const double*)ctx->pinned + kMcSlot;
@@ -363,90 +488,164 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   if (alpha < 0) return fail(ctx, PCB_INVALID, "alpha must be >= 0");
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int d = plan->d, nb = plan->n_bins;
-  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double);
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double), tbytes = (size_t)d * nb * sizeof(double);
   PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
   PCB_CUDA_TRY(ctx, ctx->mc_bounds[1].ensure(bbytes));
-  {  // init_grid: k / n_bins on every axis (vegas_grid.py:77-84)
-    std::vector<double> b((size_t)d * (nb + 1));
+  // run state on the device: [0] stop iteration (int), then the (integral, variance) history
+  PCB_CUDA_TRY(ctx, ctx->mc_state.ensure(16 + 2 * (size_t)iterations * sizeof(double)));
+  int* stop_dev = ctx->mc_state.as<int>();
+  double* hist_i = reinterpret_cast<double*>(ctx->mc_state.as<char>() + 16);
+  double* hist_v = hist_i + iterations;
+  if (contributions_out) PCB_CUDA_TRY(ctx, ctx->mc_tables.ensure((size_t)iterations * tbytes));
+  if (ctx->mc_records_cap < (size_t)iterations) {
+    if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
+    ctx->mc_records = nullptr;
+    ctx->mc_records_cap = 0;
+    const size_t cap = std::max<size_t>(64, (size_t)iterations);
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->mc_records, cap * sizeof(McRecord)));
+    std::memset(ctx->mc_records, 0, cap * sizeof(McRecord));
+    ctx->mc_records_cap = cap;
+  }
+  McRecord* records = static_cast<McRecord*>(ctx->mc_records);
+  while (ctx->mc_events.size() < (size_t)iterations + 1) {
+    cudaEvent_t ev;
+    PCB_CUDA_TRY(ctx, cudaEventCreate(&ev));
+    ctx->mc_events.push_back(ev);
+  }
+  const unsigned long long token = ++ctx->mc_run_token;
+  {  // init_grid: k / n_bins on every axis (vegas_grid.py:77-84); stop iteration = "never"
+    double* b = static_cast<double*>(ctx->pinned) + 64;  // 64-KiB staging block, first 512 B hold the scalar slots
+    std::vector<double> big;
+    if ((64 + (size_t)d * (nb + 1)) * sizeof(double) > (1u << 16)) { big.resize((size_t)d * (nb + 1)); b = big.data(); }
     for (int j = 0; j < d; ++j)
       for (int k = 0; k <= nb; ++k) b[(size_t)j * (nb + 1) + k] = (double)k / (double)nb;
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, b.data(), bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, b, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+    static const int never = 0x7fffffff;
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(stop_dev, &never, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    PCB_TRY(arm_pass_scalars(ctx));
     PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   }
-  cudaEvent_t ev0, ev1;
-  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev0));
-  PCB_CUDA_TRY(ctx, cudaEventCreate(&ev1));
-  struct EventGuard {
-    cudaEvent_t a, b;
-    ~EventGuard() { cudaEventDestroy(a); cudaEventDestroy(b); }
-  } guard{ev0, ev1};
-  cudaEventRecord(ev0, ctx->stream);
+  const size_t span_mark[3] = {ctx->spans[0].size(), ctx->spans[1].size(), ctx->spans[2].size()};
+  PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[0], ctx->stream));
 
+  // The loop is device-resident: every kernel of iteration `it` is a no-op once the device has decided to
+  // stop at an earlier iteration, so the host enqueues iteration it+1 BEFORE it waits for the record of
+  // iteration it -- the device never idles on the host round trip.
   const long long n_threads = (plan->m + plan->s - 1) / plan->s;
-  int cur = 0, done = 0;
-  std::vector<double> ivals, ivars;
-  for (int it = 0; it < iterations; ++it) {
+  auto enqueue = [&](int it) -> pcb_status {
+    PassTail tail;
+    tail.iteration = it;
+    tail.stop = stop_dev;
+    tail.refine = adapt != 0;
+    tail.alpha = alpha;
+    tail.smoothing = smoothing;
+    const int cur = adapt ? (it & 1) : 0;
+    tail.bounds_in = ctx->mc_bounds[cur].as<double>();
+    tail.bounds_out = ctx->mc_bounds[cur ^ 1].as<double>();
+    tail.contrib_copy = contributions_out ? ctx->mc_tables.as<double>() + (size_t)it * d * nb : nullptr;
+    tail.hist_i = hist_i;
+    tail.hist_v = hist_v;
+    tail.rel_tol = rel_tol;
+    tail.record = records + it;
+    tail.seq = (token << 20) | (unsigned long long)(it + 1);
     const unsigned long long it_seed = derive_seed(seed, (unsigned long long)it);  // mcubes.py:58-60, 359
-    PCB_TRY(sample_dev(ctx, f, plan, ctx->mc_bounds[cur].as<double>(), it_seed, rng_kind, nullptr, 1, 0, n_threads, nullptr));
-    if (contributions_out)
-      PCB_CUDA_TRY(ctx, cudaMemcpyAsync(contributions_out + (size_t)it * d * nb, ctx->mc_contrib.p, (size_t)d * nb * sizeof(double),
-                                        cudaMemcpyDeviceToHost, ctx->stream));
-    if (adapt) {
-      PCB_TRY(refine_dev(ctx, d, nb, ctx->mc_bounds[cur].as<double>(), ctx->mc_contrib.as<double>(), alpha, smoothing,
-                         ctx->mc_bounds[cur ^ 1].as<double>()));
-      cur ^= 1;
+    PCB_TRY(enqueue_pass(ctx, f, plan, tail.bounds_in, it_seed, rng_kind, nullptr, 1, 0, n_threads, tail, nullptr));
+    PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[it + 1], ctx->stream));
+    return PCB_OK;
+  };
+  auto wait_record = [&](int it) -> pcb_status {
+    const unsigned long long want = (token << 20) | (unsigned long long)(it + 1);
+    const McRecord* r = records + it;
+    for (unsigned spin = 0; r->seq != want; ++spin) {
+      if ((spin & 0xfff) == 0xfff) {  // the record never arrives if a kernel faulted: look at the stream now and then
+        cudaError_t e = cudaStreamQuery(ctx->stream);
+        if (e != cudaErrorNotReady && r->seq != want) {
+          if (e == cudaSuccess) return fail(ctx, PCB_CUDA, "mcubes_run: iteration %d finished without publishing its record", it);
+          (void)cudaGetLastError();
+          return fail(ctx, PCB_CUDA, "mcubes_run: %s", cudaGetErrorString(e));
+        }
+      }
     }
-    PCB_TRY(read_mc_scalars(ctx));
-    const unsigned long long* hu = (const unsigned long long*)ctx->pinned + kMcSlot;
-    const double* hd = (const double*)ctx->pinned + kMcSlot;
-    if (hu[M_BAD] != ~0ULL) return report_bad_sample(ctx, plan, hu[M_BAD], bad);
+    return PCB_OK;
+  };
+
+  int done = 0, enqueued = 0;
+  std::vector<double> ivals, ivars;
+  pcb_status st = enqueue(enqueued++);
+  for (int it = 0; st == PCB_OK && it < iterations; ++it) {
+    if (enqueued < iterations) {
+      st = enqueue(enqueued++);
+      if (st != PCB_OK) break;
+    }
+    st = wait_record(it);
+    if (st != PCB_OK) break;
+    const McRecord rec = {records[it].integral, records[it].variance, records[it].clamps, records[it].bad, records[it].stop, 0, 0};
+    if (rec.bad != ~0ULL) {
+      cudaStreamSynchronize(ctx->stream);
+      return report_bad_sample(ctx, plan, rec.bad, bad);
+    }
     pcb_mcubes_iteration& o = iterations_out[it];
-    o.integral = hd[M_INTEGRAL];
-    o.variance = std::fmax(hd[M_VARIANCE], 0.0);
+    o.integral = rec.integral;
+    o.variance = std::fmax(rec.variance, 0.0);
     o.n_samples = plan->m * plan->p;
-    o.clamp_events = (int64_t)hu[M_CLAMPS];
+    o.clamp_events = (int64_t)rec.clamps;
     done = it + 1;
     ivals.push_back(o.integral);
     ivars.push_back(o.variance);
-    // combine_iterations (mcubes.py:311-329): inverse-variance weights, variances floored at 1e-30
-    double wsum = 0.0, dot = 0.0;
-    for (int i = 0; i < done; ++i) {
-      const double w = 1.0 / std::fmax(ivars[i], 1e-30);
-      wsum += w;
-      dot += w * ivals[i];
-    }
-    const double est = dot / wsum, err = std::pow(wsum, -0.5);
-    double chi2 = 0.0;
-    if (done > 1) {
-      for (int i = 0; i < done; ++i) {
-        const double w = 1.0 / std::fmax(ivars[i], 1e-30), dv = ivals[i] - est;
-        chi2 += w * (dv * dv);
-      }
-      chi2 /= (double)(done - 1);
-    }
     if (progress) {
-      pcb_mcubes_progress rec;
-      rec.iteration = it;
-      rec.reserved = 0;
-      rec.estimate = est;
-      rec.errorest = err;
-      rec.chi2_per_dof = chi2;
-      rec.iter_integral = o.integral;
-      rec.iter_variance = o.variance;
-      progress(user, &rec);
+      // combine_iterations (mcubes.py:311-329): inverse-variance weights, variances floored at 1e-30
+      double wsum = 0.0, dot = 0.0;
+      for (int i = 0; i < done; ++i) {
+        const double w = 1.0 / std::fmax(ivars[i], 1e-30);
+        wsum += w;
+        dot += w * ivals[i];
+      }
+      const double est = dot / wsum, err = std::pow(wsum, -0.5);
+      double chi2 = 0.0;
+      if (done > 1) {
+        for (int i = 0; i < done; ++i) {
+          const double w = 1.0 / std::fmax(ivars[i], 1e-30), dv = ivals[i] - est;
+          chi2 += w * (dv * dv);
+        }
+        chi2 /= (double)(done - 1);
+      }
+      pcb_mcubes_progress rec_out;
+      rec_out.iteration = it;
+      rec_out.reserved = 0;
+      rec_out.estimate = est;
+      rec_out.errorest = err;
+      rec_out.chi2_per_dof = chi2;
+      rec_out.iter_integral = o.integral;
+      rec_out.iter_variance = o.variance;
+      progress(user, &rec_out);
     }
-    if (rel_tol > 0 && err <= rel_tol * std::fabs(est)) break;
+    if (rec.stop) break;
   }
-  cudaEventRecord(ev1, ctx->stream);
-  PCB_CUDA_TRY(ctx, cudaEventSynchronize(ev1));
+  // drain the (at most one) speculative no-op pass before anything is read back or reused
+  cudaError_t drain = cudaStreamSynchronize(ctx->stream);
+  if (st != PCB_OK) return st;
+  PCB_CUDA_TRY(ctx, drain);
+  // profiling spans of passes that never ran are not launches of the hot kernel
+  for (int k = 0; k < 3; ++k) {
+    auto& v = ctx->spans[k];
+    size_t keep = span_mark[k];
+    for (size_t i = span_mark[k]; i < v.size(); ++i) {
+      if (v[i].tag < done) v[keep++] = v[i];
+      else ctx->span_pool.push_back(v[i]);
+    }
+    v.resize(keep);
+  }
   float ms = 0;
-  cudaEventElapsedTime(&ms, ev0, ev1);
+  PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[done]));
   if (seconds_device) *seconds_device = ms * 1e-3;
   *n_done = done;
+  if (contributions_out)
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(contributions_out, ctx->mc_tables.p, (size_t)done * tbytes, cudaMemcpyDeviceToHost, ctx->stream));
   if (final_boundaries) {
+    const int cur = adapt ? (done & 1) : 0;
     PCB_CUDA_TRY(ctx, cudaMemcpyAsync(final_boundaries, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
-    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   }
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return PCB_OK;
 }
 

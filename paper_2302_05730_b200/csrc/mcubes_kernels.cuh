@@ -23,13 +23,39 @@
 
 namespace pcb {
 
+// x / d and x % d for a loop-invariant d by one multiply-high (m = floor(2^64 / d)): the quotient estimate is
+// at most 2 short, fixed by the loop.  64-bit division is ~100 instructions on this part and the per-unit
+// setup of a small pass would otherwise cost as much as one sample.
+struct FastDiv {
+  unsigned long long d, m;
+};
+__host__ inline FastDiv make_fastdiv(unsigned long long d) {
+  FastDiv f;
+  f.d = d;
+  f.m = d <= 1 ? ~0ULL : (unsigned long long)((((unsigned __int128)1) << 64) / d);
+  return f;
+}
+__device__ __forceinline__ unsigned long long fast_divmod(unsigned long long x, const FastDiv& f, unsigned long long& rem) {
+  unsigned long long q = __umul64hi(x, f.m);
+  unsigned long long r = x - q * f.d;
+  while (r >= f.d) { r -= f.d; ++q; }
+  rem = r;
+  return q;
+}
+
 struct SampleArgs {
   pcb_integrand f;
   int g, p, nb, squared_weighted;
   long long m, s;
   long long n_threads;          // logical threads of the whole plan
   long long t_begin, t_end;     // this launch's shard of logical threads
-  long long n_lw;               // logical warps in the shard = ceil((t_end - t_begin) / 32)
+  // Work item = segment sigma = (T - t_begin) * nseg + q of seg_len sub-cubes; lane l of unit u takes
+  // sigma = ((u * 32 + l) * seg_mul) mod n_segments.  The multiplier spreads the 32 lanes of a warp over
+  // different sub-cube coordinates on EVERY axis (lane-to-lane offset ~ (1,1,...,1) in base g), so their
+  // samples fall into different windows of the importance grid and rarely collide in the accumulation.
+  long long n_segments;         // (t_end - t_begin) * nseg
+  unsigned long long seg_mul;   // coprime to n_segments
+  FastDiv div_segments, div_nseg, div_g;
   int nseg;                     // segments per logical thread
   int rng_kind;
   long long seg_len;
@@ -46,6 +72,8 @@ struct SampleArgs {
   long long unit_begin, unit_end, rec_per_unit, rec_capacity;
   double* rec_w;                // [rec_capacity] contribution (v^2, or f^2 when not squared_weighted)
   unsigned short* rec_b;        // [d][rec_capacity] bin ids
+  const int* stop;              // iteration at which the run stopped (INT_MAX while running); may be NULL
+  int iteration;
 };
 
 struct BinArgs {
@@ -56,6 +84,8 @@ struct BinArgs {
   const unsigned short* rec_b;
   double* block_hist;           // [gridDim.x][d*nb], accumulated across launches
   int accumulate;               // 0: overwrite block_hist, 1: add to it
+  const int* stop;
+  int iteration;
 };
 
 // One sample: draw u per axis, stratify, push through the grid, evaluate (mcubes.py:224-243).
@@ -99,6 +129,7 @@ constexpr int kSampleWarps = 8;  // warps per sampling CTA; two CTAs per SM at 1
 template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
+  if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb1 = a.nb + 1;
   double* s_b = reinterpret_cast<double*>(smem_raw);            // [D][nb+1]
@@ -112,11 +143,14 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
 
   for (long long u = a.unit_begin + (long long)blockIdx.x * kSampleWarps + wib; u < a.unit_end;
        u += (long long)gridDim.x * kSampleWarps) {
-    const long long lw = u % a.n_lw;
-    const int q = (int)(u / a.n_lw);
-    const long long T = a.t_begin + lw + (long long)lane * a.n_lw;
+    const unsigned long long sin = (unsigned long long)u * 32ULL + (unsigned long long)lane;
+    const bool live = sin < (unsigned long long)a.n_segments;
+    unsigned long long sigma = 0, qq_seg = 0;
+    if (live) fast_divmod(sin * a.seg_mul, a.div_segments, sigma);
+    const long long T = a.t_begin + (long long)fast_divmod(sigma, a.div_nseg, qq_seg);
+    const int q = (int)qq_seg;
     long long c_begin = 0, count = 0;
-    if (T < a.t_end) {
+    if (live) {
       const long long l0 = (long long)q * a.seg_len;
       long long l1 = l0 + a.seg_len;
       if (l1 > a.s) l1 = a.s;
@@ -128,12 +162,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
     // sub-cube coordinates (axis 0 most significant, mcubes.py:132-140), kept as doubles
     double coord[D];
     {
-      long long rem = c_begin;
+      unsigned long long rem = (unsigned long long)c_begin;
 #pragma unroll
       for (int j = D - 1; j >= 0; --j) {
-        long long qq = rem / a.g;
-        coord[j] = (double)(rem - qq * a.g);
-        rem = qq;
+        unsigned long long digit;
+        rem = fast_divmod(rem, a.div_g, digit);
+        coord[j] = (double)(int)digit;
       }
     }
     const unsigned long long key = stream_key(a.seed, (unsigned long long)T);
@@ -213,8 +247,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
 #pragma unroll
       for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = 0;
     }
-    if (T < a.t_end) {
-      double* out = a.seg_partials + ((T - a.t_begin) * a.nseg + q) * 2;
+    if (live) {
+      double* out = a.seg_partials + sigma * 2;
       out[0] = sum_est;
       out[1] = sum_var;
     }

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdarg>
 #include <cstdio>
 #include <map>
@@ -71,11 +72,17 @@ struct pcb_ctx {
   } shard;
   // roofline profiling (pcb_profile_begin/end)
   bool profiling = false;
-  struct Span { cudaEvent_t a, b; };
+  struct Span { cudaEvent_t a, b; double units; int tag; };
   std::vector<Span> spans[3];
   std::vector<Span> span_pool;
-  double span_units[3] = {0, 0, 0};
   pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject, mc_rec;
+  // pcb_mcubes_run: device run state (stop iteration, history), per-iteration tables, pinned iteration records
+  pcb::DevBuf mc_state, mc_tables;
+  void* mc_records = nullptr;
+  size_t mc_records_cap = 0;
+  unsigned long long mc_run_token = 0;
+  std::vector<cudaEvent_t> mc_events;
+  std::map<std::array<long long, 6>, unsigned long long> mc_multipliers;  // lane -> segment map, per plan
 };
 
 namespace pcb {
@@ -117,7 +124,8 @@ struct ProfileSpan {
   int kind;
   pcb_ctx::Span span{};
   bool on;
-  ProfileSpan(pcb_ctx* c, int k, double units) : ctx(c), kind(k), on(c->profiling) {
+  // `tag` lets a driver that enqueues speculatively (pcb_mcubes_run) discard the spans of passes that never ran
+  ProfileSpan(pcb_ctx* c, int k, double units, int tag = 0) : ctx(c), kind(k), on(c->profiling) {
     if (!on) return;
     if (!ctx->span_pool.empty()) {
       span = ctx->span_pool.back();
@@ -126,7 +134,8 @@ struct ProfileSpan {
       cudaEventCreate(&span.a);
       cudaEventCreate(&span.b);
     }
-    ctx->span_units[kind] += units;
+    span.units = units;
+    span.tag = tag;
     cudaEventRecord(span.a, ctx->stream);
   }
   ~ProfileSpan() {
