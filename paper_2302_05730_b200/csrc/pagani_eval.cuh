@@ -68,6 +68,48 @@ __device__ __forceinline__ double region_error(const double (&v)[5], const pcb_r
 __device__ __forceinline__ double shfl_xor_d(double v, int m) { return __shfl_xor_sync(PCB_FULL_MASK, v, m); }
 __device__ __forceinline__ double shfl_idx_d(double v, int l) { return __shfl_sync(PCB_FULL_MASK, v, l); }
 
+// region_error with the divisions of the two-level mode spread over the lanes: every lane holds v[0..4];
+// lane k < 4 forms nul[k] / scale[k] (x / 1.0 == x, so unit scales skip the ~25-instruction division), the
+// maxima are gathered with shuffles.  Same operations and roundings as region_error, a third of the issue slots.
+__device__ __forceinline__ double region_error_warp(const double (&v)[5], const pcb_rule& rule, int mode, double rel_floor,
+                                                    int lane) {
+  if (mode != PCB_ERR_TWO_LEVEL) return region_error(v, rule, mode, rel_floor);
+  const int k = lane & 3;
+  const double mine = fabs(k == 0 ? v[1] : k == 1 ? v[2] : k == 2 ? v[3] : v[4]);
+  const bool high = rule.null_high[k] != 0;
+  const double scale = rule.null_scale[k];
+  double hi = high ? mine : -1.0;
+  double lo = high ? -1.0 : (scale == 1.0 ? mine : mine / scale);
+  hi = fmax(hi, shfl_xor_d(hi, 1));
+  lo = fmax(lo, shfl_xor_d(lo, 1));
+  hi = fmax(hi, shfl_xor_d(hi, 2));
+  lo = fmax(lo, shfl_xor_d(lo, 2));
+  const double corr = (lo > 0.0) ? (10.0 * hi) / lo : 1.0;
+  const double err = hi * fmin(1.0, corr);
+  return fmax(err, rel_floor * fabs(v[0]));
+}
+
+// split axis (pagani.py:215-223): argmax_j |c0 * d2(l2, j) - c1 * d2(l3, j)| over the stored centre/axial
+// evaluations, first maximum wins.  All lanes return the axis.
+template <int D>
+__device__ __forceinline__ int split_axis_warp(const double* store, const pcb_rule& rule, int lane) {
+  double ind = -1.0;
+  if (lane < D) {
+    double two_f0 = 2.0 * store[0];
+    double d2a = (store[1 + 2 * lane] + store[2 + 2 * lane]) - two_f0;
+    double d2b = (store[1 + 2 * D + 2 * lane] + store[2 + 2 * D + 2 * lane]) - two_f0;
+    ind = fabs(rule.split_weights[0] * d2a - rule.split_weights[1] * d2b);
+  }
+  int idx = lane;
+#pragma unroll
+  for (int m = 8; m >= 1; m >>= 1) {  // argmax over lanes 0..15, lowest index wins ties
+    double o = shfl_xor_d(ind, m);
+    int oi = __shfl_xor_sync(PCB_FULL_MASK, idx, m);
+    if (o > ind || (o == ind && oi < idx)) { ind = o; idx = oi; }
+  }
+  return __shfl_sync(PCB_FULL_MASK, idx, 0);
+}
+
 // Reduce 2 sets x 5 columns over the 32 lanes with the adjacent-pair tree, then add the two sets.
 // On return every lane holds all five sums.
 __device__ __forceinline__ void schedule_tree(const double (&a)[5], const double (&b)[5], int lane,
@@ -172,7 +214,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
   __shared__ __align__(16) double s_term[kEvalWarps][D * 8];
   __shared__ double s_store[kEvalWarps][kStore + 1];
   __shared__ double s_geo[kEvalWarps][2][2 * D];   // double-buffered left[0..D), length[0..D)
-  __shared__ __align__(16) double s_w[6][6];   // orbit weights (+pad); rows 4/5 = corners with even/odd bit count
+  __shared__ __align__(16) double s_w[6][8];   // orbit weights (+pad); rows 4/5 = corners with even/odd bit count
   __shared__ double s_off[8];
   __shared__ unsigned long long s_code[kCorner0][kWords];  // byte j: candidate byte offset on axis j; bits 6-7 of byte 0: orbit
 
@@ -210,6 +252,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
   __syncthreads();
 
   const int fe = rule.f_eval, G = args.group;
+  const double jac = args.f.bounded ? args.f.jac : 1.0;   // x * 1.0 == x: no branch per point
   const char* term_b = reinterpret_cast<const char*>(s_term[wib]);
   double* term = s_term[wib];
   double* store = s_store[wib];
@@ -242,16 +285,19 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
     for (int j = 1; j < D; ++j) vol = vol * geo[D + j];  // np.prod, left to right
     __syncwarp();
 
-    // ---- 2. rule points of my two virtual threads
+    // ---- 2. rule points of my two virtual threads.  Partial sums start from -0.0: (-0.0) + x == x for every
+    //         x, so "first product, then adds" (pagani.py:189-191) needs no special case; a virtual thread
+    //         without points keeps the +0.0 of the reference's zero padding.
     double acc[2][5];
+    unsigned badpt = 0xffffffffu;
 #pragma unroll
     for (int set = 0; set < 2; ++set) {
-#pragma unroll
-      for (int k = 0; k < 5; ++k) acc[set][k] = 0.0;
       const int vt = lane + 32 * set;
+      const double init = (vt < G && vt < fe) ? -0.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) acc[set][k] = init;
       if (vt >= G) continue;
       int i = vt;
-      bool first = true;
       // centre, axial and pair points
       for (; i < kCorner0; i += G) {
         unsigned long long code[kWords];
@@ -265,18 +311,12 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
           const unsigned half = (unsigned)(code[j >> 3] >> (32 * ((j >> 2) & 1)));
           t[j] = term_at<D>(term_b, j, __byte_perm(half, 0, 0x4440 + (j & 3)));
         }
-        const double fx = finish_value<F, D>(combine_terms<F, D>(t), args.f);
-        if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+        const double fx = F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
+        if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
         if (i < kStore) store[i] = fx;
         const double* w = s_w[orbit];
-        if (first) {
 #pragma unroll
-          for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
-          first = false;
-        } else {
-#pragma unroll
-          for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
-        }
+        for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
       }
       // corner points: bit j of (i - kCorner0) set => abscissa candidate 6 (minus), else 5 (plus)
       if (G == 64) {
@@ -284,35 +324,26 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
         if (i < fe) cc.head(term_b, (unsigned)(i - kCorner0));
         for (; i < fe; i += 64) {
           const unsigned bits = (unsigned)(i - kCorner0);
-          const double fx = finish_value<F, D>(cc.tail(term_b, bits), args.f);
-          if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+          const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
+          if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
           const double* w = s_w[4 + (__popc(bits) & 1)];
-          if (first) {
 #pragma unroll
-            for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
-            first = false;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
-          }
+          for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
         }
       } else {
         CornerCombine<F, D, 0> cc;
         for (; i < fe; i += G) {
           const unsigned bits = (unsigned)(i - kCorner0);
-          const double fx = finish_value<F, D>(cc.tail(term_b, bits), args.f);
-          if (!isfinite(fx)) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)i);
+          const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
+          if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
           const double* w = s_w[4 + (__popc(bits) & 1)];
-          if (first) {
 #pragma unroll
-            for (int k = 0; k < 5; ++k) acc[set][k] = w[k] * fx;
-            first = false;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
-          }
+          for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
         }
       }
+    }
+    if (__any_sync(PCB_FULL_MASK, badpt != 0xffffffffu)) {
+      if (badpt != 0xffffffffu) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)badpt);
     }
 
     // ---- 3. schedule tree, 4. volume scaling / error / split axis
@@ -323,26 +354,11 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
     for (int k = 0; k < 5; ++k) v[k] = vol * sums[k];
     __syncwarp();
     int axis = 0;
-    if constexpr (D > 1) {
-      double ind = -1.0;
-      if (lane < D) {
-        double two_f0 = 2.0 * store[0];
-        double d2a = (store[1 + 2 * lane] + store[2 + 2 * lane]) - two_f0;
-        double d2b = (store[1 + 2 * D + 2 * lane] + store[2 + 2 * D + 2 * lane]) - two_f0;
-        ind = fabs(rule.split_weights[0] * d2a - rule.split_weights[1] * d2b);
-      }
-      int idx = lane;
-#pragma unroll
-      for (int m = 8; m >= 1; m >>= 1) {  // argmax over lanes 0..15, lowest index wins ties
-        double o = shfl_xor_d(ind, m);
-        int oi = __shfl_xor_sync(PCB_FULL_MASK, idx, m);
-        if (o > ind || (o == ind && oi < idx)) { ind = o; idx = oi; }
-      }
-      axis = __shfl_sync(PCB_FULL_MASK, idx, 0);
-    }
+    if constexpr (D > 1) axis = split_axis_warp<D>(store, rule, lane);
+    const double err = region_error_warp(v, rule, args.err_mode, args.rel_floor, lane);
     if (lane == 0) {
       args.integrals[r] = v[0];
-      args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
+      args.errors[r] = err;
       args.split_axes[r] = axis;
     }
     if (lane < 2 * D) s_geo[wib][buf ^ 1][lane] = next_geo;

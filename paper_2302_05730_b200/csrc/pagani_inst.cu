@@ -1,6 +1,7 @@
 // Instantiations of the PAGANI evaluate / eval_points kernels for ONE integrand family
 // (compiled once per family with -DPCB_FAM=<pcb_family>, so the families build in parallel).
 #include "pagani_eval.cuh"
+#include "pagani_eval_mult.cuh"
 
 #ifndef PCB_FAM
 #error "compile with -DPCB_FAM=<family id>"
@@ -11,9 +12,17 @@
 
 namespace pcb {
 
+// multiplicative families (f1, f4, f5, f6) evaluate rule points as products of tabulated per-axis factors;
+// the others keep the exact-order kernel
+template <int D>
+static const void* eval_kernel_for() {
+  if constexpr (MultFamily<PCB_FAM>::enabled) return (const void*)&pagani_eval_mult_kernel<PCB_FAM, D>;
+  else return (const void*)&pagani_eval_kernel<PCB_FAM, D>;
+}
+
 const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
   switch (d) {
-#define X(D) case D: return (const void*)&pagani_eval_kernel<PCB_FAM, D>;
+#define X(D) case D: return (const void*)eval_kernel_for<D>();
     PCB_DIMS(X)
 #undef X
   }
