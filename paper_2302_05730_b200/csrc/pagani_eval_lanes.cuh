@@ -1,0 +1,339 @@
+// PAGANI region evaluation, ONE REGION PER LANE, for the multiplicative families (f1, f4, f5, f6) and the
+// default schedule width G = 64 (reference: pagani.py:195-224; arithmetic as in pagani_eval_mult.cuh).
+//
+// The Genz-Malik point set is the same for every region, so the natural SIMD axis on a GPU is the REGION:
+// the 32 lanes of a warp walk the F rule points in lock-step, each on its own region.  Which point comes
+// next, which axes it moves, which orbit weights apply -- all of that is warp-uniform and costs (almost)
+// nothing per region; what is left per lane and point is three shared-memory gathers from the lane's own
+// factor tables, two multiplies and the five weighted accumulations the reference schedule prescribes.
+// The warp-per-region kernels spend ~1500 issue slots per region, 3/4 of them on index arithmetic and
+// shuffles; this one spends ~500 and is bound by the FP64 pipe.
+//
+// Per lane (= region):
+//   tables     phi[j][c] = factor_j(left_j + length_j * offset_c) for c in {0,3,4,5,6}; from them
+//              Rab[a<b] = everything of a pair point but its two moved axes, Grp[g][combo] = corner
+//              products over groups of three axes (same association as pagani_eval_mult.cuh, so the
+//              two kernels agree bit for bit and a sharded list does not depend on who evaluates it);
+//              term[j][c] for c in 0..4: the generic per-axis terms of the 4D+1 centre/axial points,
+//              which are evaluated in the reference's own association (split-axis inputs).
+//   points     virtual thread vt = 0..63 outer, step s inner (point i = vt + 64 s), five partial sums
+//              per virtual thread started from -0.0 (see pagani_eval.cuh), merged by a binary counter
+//              whose add tree is the adjacent-pair tree of engine.tree_sum.
+//   finish     volume scaling, error estimate, split axis (running first-maximum), coalesced stores.
+// A non-finite evaluation poisons the sums; only then the points are walked again to find the first one.
+#pragma once
+
+#include "pagani_eval_mult.cuh"
+
+namespace pcb {
+
+template <int D>
+struct LaneLayout {
+  static constexpr int kFe = (1 << D) + 2 * D * D + 2 * D + 1;
+  static constexpr int kCorner0 = 2 * D * D + 2 * D + 1;
+  static constexpr int kPairs = D * (D - 1) / 2;
+  static constexpr int kGroups = (D + 2) / 3;
+  static constexpr int kSteps = (kFe + 63) / 64;
+  static constexpr int kP34 = 0;                                  // phi[j][3], phi[j][4] at 2j, 2j+1
+  static constexpr int kRab = 2 * D;
+  static constexpr int kGrp = kRab + (kPairs > 0 ? kPairs : 1);  // Grp[g][combo] at kGrp + 8g + combo
+  static constexpr int kTab = kGrp + 8 * kGroups;                 // V entries per lane
+  static constexpr int kTerm = 5 * D;                             // doubles per lane: term[j][c], c = 0..4
+  // stash: D doubles per lane (second differences at l2) during the point phase; while the tables are built the
+  // same bytes hold the D centre factors phi[j][0]
+  static constexpr int kDesc = 4 * (kPairs > 0 ? kPairs : 1);     // unsigned per CTA
+  static constexpr size_t smem_bytes(size_t vsize) {
+    return 32 * (kTab * vsize + (size_t)kTerm * 8 + D * vsize) + 6 * 8 * 8 + (size_t)kDesc * 4;
+  }
+};
+
+
+// level LEV of a binary counter over blocks: an odd index closes the pair (left + right) and carries upward
+template <int LEV, int NLEV>
+__device__ __forceinline__ void counter_merge(int blk, double (&cur)[5], double (&hold)[NLEV][5]) {
+  if constexpr (LEV < NLEV) {
+    if ((blk >> LEV) & 1) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) cur[k] = hold[LEV][k] + cur[k];
+      counter_merge<LEV + 1, NLEV>(blk, cur, hold);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) hold[LEV][k] = cur[k];
+    }
+  }
+}
+
+template <int FAM, int D>
+__global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
+  using F = Family<FAM>;
+  using MF = MultFamily<FAM>;
+  using V = MVal<MF::cplx>;
+  using L = LaneLayout<D>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x;
+  V* tab = reinterpret_cast<V*>(smem_raw) + lane;                                                   // entry e: tab[e * 32]
+  double* term = reinterpret_cast<double*>(smem_raw + sizeof(V) * 32 * L::kTab) + lane;             // term[(5j + c) * 32]
+  double* stash = term + 32 * L::kTerm;                                                             // stash[j * 32]
+  V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * L::kTerm) + lane;  // cen_s[j * 32], aliases stash
+  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * L::kTerm + sizeof(V) * D));   // [6][8]
+  unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                                          // [4 * kPairs]
+
+  const pcb_rule& rule = args.rule;
+  // pair point q = 4 * pair + signs -> entry indices of its three factors
+  for (int q = lane; q < 4 * L::kPairs; q += 32) {
+    const int e = q >> 2;
+    int a = 0, b = 0, idx = 0;
+    for (int j = 0; j < D; ++j)
+      for (int k = j + 1; k < D; ++k, ++idx)
+        if (idx == e) { a = j; b = k; }
+    desc[q] = (unsigned)(L::kRab + e) | ((unsigned)(L::kP34 + 2 * a + (q & 1)) << 10) | ((unsigned)(L::kP34 + 2 * b + ((q >> 1) & 1)) << 20);
+  }
+  if (lane < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
+    const int o = lane / 5, k = lane % 5;
+    double w = rule.weights[k][o < 5 ? o : 4];
+    if (o == 5 && rule.corner_parity[k]) w = -w;
+    s_w[o * 8 + k] = w;
+  }
+  __syncwarp();
+
+  const double jac = args.f.bounded ? args.f.jac : 1.0;   // x * 1.0 == x
+  const V one = mone(V{});
+
+  // value of pair / corner points from the lane's tables
+  auto pair_value = [&](int i) -> double {
+    const unsigned dsc = desc[i - 1 - 4 * D];
+    const V v = mmul(mmul(tab[(dsc & 1023u) * 32], tab[((dsc >> 10) & 1023u) * 32]), tab[(dsc >> 20) * 32]);
+    return v.re * jac;
+  };
+  auto corner_head = [&](unsigned bits) -> V {   // groups 0 and 1 (all groups when D < 6)
+    V h = tab[(L::kGrp + (bits & 7u)) * 32];
+    if constexpr (L::kGroups > 1) h = mmul(h, tab[(L::kGrp + 8 + ((bits >> 3) & 7u)) * 32]);
+    return h;
+  };
+  auto corner_value = [&](V head, unsigned bits) -> double {
+    V v = head;
+#pragma unroll
+    for (int g = 2; g < L::kGroups; ++g) v = mmul(v, tab[(L::kGrp + 8 * g + ((bits >> (3 * g)) & 7u)) * 32]);
+    return v.re * jac;
+  };
+  auto direct_value = [&](int i) -> double {   // centre / axial points in the reference's association
+    const int q = i - 1;
+    const int a = i == 0 ? -1 : ((q >= 2 * D ? q - 2 * D : q) >> 1);
+    const int cand = i == 0 ? 0 : 1 + (q & 1) + (q >= 2 * D ? 2 : 0);
+    double t[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t[j] = term[(5 * j + (j == a ? cand : 0)) * 32];
+    return F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
+  };
+
+  for (long long batch = blockIdx.x; batch * 32 < args.n; batch += gridDim.x) {
+    const long long r = batch * 32 + lane;
+    const bool live = r < args.n;
+    const long long rc = live ? r : args.n - 1;
+
+    // ---- tables (loops over the axis are rolled: the kernel must stay inside the instruction cache)
+    double vol = 1.0;
+    double next_left = args.lefts[rc], next_len = args.lengths[rc];
+#pragma unroll 1
+    for (int j = 0; j < D; ++j) {
+      const double left = next_left, len = next_len;
+      if (j + 1 < D) {   // the next axis' geometry travels while this axis' transcendentals are evaluated
+        next_left = args.lefts[(j + 1) * args.ld + rc];
+        next_len = args.lengths[(j + 1) * args.ld + rc];
+      }
+      vol = (j == 0) ? len : vol * len;   // np.prod, left to right
+      V cg[2];
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        double x = left + len * rule.offsets[c];   // quadrature.py:301-302: mul, then add
+        if (args.f.bounded) x = args.f.low[j] + args.f.width[j] * x;
+        if (c < 5) term[(5 * j + c) * 32] = F::term(j, x, args.f);
+        if (c == 1 || c == 2) continue;            // axial points never use a factor
+        const V v = MF::factor(j, x, args.f);
+        if (c == 0) cen_s[j * 32] = v;
+        else if (c < 5) tab[(L::kP34 + 2 * j + (c - 3)) * 32] = v;
+        else cg[c - 5] = v;
+      }
+      // corner group tables: Grp[g][combo] = phi[3g][.] * phi[3g+1][.] * phi[3g+2][.], left to right
+      const int g = j / 3, pos = j - 3 * g;
+      V* grp = tab + (L::kGrp + 8 * g) * 32;
+      if (pos == 0) {
+        grp[0] = cg[0];
+        grp[32] = cg[1];
+      } else {
+        const int half = 1 << pos;
+#pragma unroll
+        for (int combo = 0; combo < 4; ++combo) {
+          if (combo < half) {
+            const V lo = grp[combo * 32];
+            grp[combo * 32] = mmul(lo, cg[0]);
+            grp[(combo + half) * 32] = mmul(lo, cg[1]);
+          }
+        }
+      }
+    }
+    // Rab[a][b] = (E[0][a] * E[a+1][b]) * E[b+1][D] with E[x][y] = ((1 * c_x) * c_{x+1}) ... * c_{y-1}
+    if constexpr (L::kPairs > 0) {
+      V cen[D], tail[D];   // tail[b] = E[b+1][D]
+#pragma unroll
+      for (int j = 0; j < D; ++j) cen[j] = cen_s[j * 32];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        V run = one;
+#pragma unroll
+        for (int k = b + 1; k < D; ++k) run = mmul(run, cen[k]);
+        tail[b] = run;
+      }
+      V pre = one;   // E[0][a]
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        V mid = one;  // E[a+1][b]
+#pragma unroll
+        for (int b = a + 1; b < D; ++b) {
+          tab[(L::kRab + e) * 32] = mmul(mmul(pre, mid), tail[b]);
+          mid = mmul(mid, cen[b]);
+          ++e;
+        }
+        pre = mmul(pre, cen[a]);
+      }
+    }
+
+    // ---- rule points.  Virtual threads are taken W at a time (vt = W blk + v).  For a fixed step s the W points
+    //      vt + 64 s of a block almost always belong to one orbit class, so the block is straight-line code over W
+    //      independent dependency chains (that is what hides the FP64 latency with ~2 warps per scheduler); only
+    //      the three blocks that straddle a class boundary take the point-by-point path.  The first log2(W)
+    //      levels of the pair tree are fixed-register adds, the remaining ones a binary counter over the blocks.
+    constexpr int W = MF::cplx ? 4 : 8;
+    constexpr int kCounterLevels = MF::cplx ? 4 : 3;   // log2(64 / W)
+    double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
+    int axis = 0;
+    // split axis bookkeeping (pagani.py:215-223) for direct point i: running first maximum over the axes
+    auto split_note = [&](int i, double fx) {
+      if constexpr (D > 1) {
+        const int q = i - 1;
+        if (i == 0) two_f0 = 2.0 * fx;
+        else if (!(q & 1)) first_of_pair = fx;
+        else {
+          const double d2 = (first_of_pair + fx) - two_f0;
+          const int a = (q >= 2 * D ? q - 2 * D : q) >> 1;
+          if (q < 2 * D) stash[a * 32] = d2;
+          else {
+            const double ind = fabs(rule.split_weights[0] * stash[a * 32] - rule.split_weights[1] * d2);
+            if (ind > best) { best = ind; axis = a; }
+          }
+        }
+      }
+    };
+    double hold[kCounterLevels][5];
+    double cur[5];
+#pragma unroll 1
+    for (int blk = 0; blk < 64 / W; ++blk) {
+      const int vt0 = W * blk;
+      double acc[W][5];
+      V head[W];
+#pragma unroll
+      for (int v = 0; v < W; ++v) {
+        const double init = vt0 + v < L::kFe ? -0.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) acc[v][k] = init;
+        head[v] = corner_head((unsigned)(vt0 + v - L::kCorner0) & 63u);
+      }
+#pragma unroll 1
+      for (int s = 0; s < L::kSteps; ++s) {
+        const int lo = vt0 + 64 * s, hi = lo + W - 1;
+        if (hi <= 4 * D) {                                         // W centre / axial points
+          double fx[W];
+#pragma unroll
+          for (int v = 0; v < W; ++v) fx[v] = direct_value(lo + v);
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            split_note(lo + v, fx[v]);
+            const double* w = s_w + 8 * (lo + v == 0 ? 0 : (lo + v <= 2 * D ? 1 : 2));
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
+          }
+        } else if (lo > 4 * D && hi < L::kCorner0) {               // W pair points
+          if constexpr (L::kPairs > 0) {
+            double fx[W];
+#pragma unroll
+            for (int v = 0; v < W; ++v) fx[v] = pair_value(lo + v);
+#pragma unroll
+            for (int v = 0; v < W; ++v)
+#pragma unroll
+              for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + rule.weights[k][3] * fx[v];
+          }
+        } else if (lo >= L::kCorner0 && hi < L::kFe) {             // W corner points
+          double fx[W];
+#pragma unroll
+          for (int v = 0; v < W; ++v) fx[v] = corner_value(head[v], (unsigned)(lo + v - L::kCorner0));
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            const double* w = s_w + 8 * (4 + (__popc((unsigned)(lo + v - L::kCorner0)) & 1));
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
+          }
+        } else if (lo < L::kFe) {                                  // the block straddles a class boundary
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            const int i = lo + v;
+            double fx;
+            int row;   // orbit weights: centre, l2, l3, pairs, corners with even / odd bit count
+            if (i <= 4 * D) {
+              fx = direct_value(i);
+              row = i == 0 ? 0 : (i <= 2 * D ? 1 : 2);
+              split_note(i, fx);
+            } else if (i < L::kCorner0) {
+              fx = L::kPairs > 0 ? pair_value(i) : 0.0;
+              row = 3;
+            } else if (i < L::kFe) {
+              const unsigned bits = (unsigned)(i - L::kCorner0);
+              fx = corner_value(head[v], bits);
+              row = 4 + (__popc(bits) & 1);
+            } else {
+              continue;
+            }
+            const double* w = s_w + 8 * row;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx;
+          }
+        }
+      }
+      // pair tree inside the block: (v, v+1), then (v, v+2), ... always left + right (engine.py:80-84)
+#pragma unroll
+      for (int span = 1; span < W; span *= 2)
+#pragma unroll
+        for (int v = 0; v < W; v += 2 * span)
+#pragma unroll
+          for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + acc[v + span][k];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) cur[k] = acc[0][k];
+      // remaining levels: binary counter over the blocks
+      counter_merge<0, kCounterLevels>(blk, cur, hold);
+    }
+
+    double v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = vol * cur[k];
+    if (live) {
+      if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]) && isfinite(v[3]) && isfinite(v[4]))) {
+        // rare: find the first non-finite evaluation of this region (pagani.py:206-209)
+        for (int i = 0; i < L::kFe; ++i) {
+          double fx;
+          if (i <= 4 * D) fx = direct_value(i);
+          else if (i < L::kCorner0) fx = L::kPairs > 0 ? pair_value(i) : 0.0;
+          else fx = corner_value(corner_head((unsigned)(i - L::kCorner0)), (unsigned)(i - L::kCorner0));
+          if (!isfinite(fx)) {
+            atomicMin(args.bad, (unsigned long long)r * (unsigned long long)L::kFe + (unsigned long long)i);
+            break;
+          }
+        }
+      }
+      args.integrals[r] = v[0];
+      args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
+      args.split_axes[r] = axis;
+    }
+  }
+}
+
+}  // namespace pcb

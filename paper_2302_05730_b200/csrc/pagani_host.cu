@@ -5,6 +5,7 @@
 #include "pcb_host.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 
@@ -54,6 +55,26 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   a.group = cfg->group_size;
   a.err_mode = cfg->err_mode;
   a.rel_floor = cfg->rel_floor;
+  // Long lists of a multiplicative family at the default schedule width go to the one-region-per-lane kernel
+  // (FP64-bound); short lists keep one warp per region (more parallelism per region).  The two agree bit for
+  // bit (tests/test_gpu_pagani.py), so the choice never shows in the results.
+  size_t lanes_smem = 0;
+  const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem) : nullptr;
+  long long lanes_min = 8192;
+  if (const char* env = std::getenv("PCB_PAGANI_LANES_MIN")) lanes_min = std::atoll(env);
+  if (lanes_fn && lanes_smem <= ctx->smem_optin && n >= lanes_min) {
+    size_t& have = ctx->smem_attr[lanes_fn];
+    if (have < lanes_smem) {
+      PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(lanes_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lanes_smem));
+      have = lanes_smem;
+    }
+    int per_sm = (int)std::min<size_t>(32, (ctx->smem_per_sm - 1024) / (lanes_smem + 1024));
+    if (per_sm < 1) per_sm = 1;
+    const long long want = (n + 31) / 32;
+    ProfileSpan span(ctx, 0, (double)n);
+    PCB_CUDA_TRY(ctx, launch(ctx, lanes_fn, dim3((unsigned)std::min<long long>(want, (long long)per_sm * ctx->sm_count)), dim3(32), lanes_smem, a));
+    return PCB_OK;
+  }
   const void* fn = eval_kernel(f->family, f->d);
   ProfileSpan span(ctx, 0, (double)n);
   PCB_CUDA_TRY(ctx, launch(ctx, fn, dim3(eval_grid(ctx, fn, n)), dim3(kEvalWarps * 32), 0, a));

@@ -2,6 +2,7 @@
 // (compiled once per family with -DPCB_FAM=<pcb_family>, so the families build in parallel).
 #include "pagani_eval.cuh"
 #include "pagani_eval_mult.cuh"
+#include "pagani_eval_lanes.cuh"
 
 #ifndef PCB_FAM
 #error "compile with -DPCB_FAM=<family id>"
@@ -26,6 +27,28 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
     PCB_DIMS(X)
 #undef X
   }
+  return nullptr;
+}
+
+// one-region-per-lane kernel (multiplicative families only) and its dynamic shared memory
+template <int D>
+static const void* lanes_kernel_for(size_t* smem) {
+  if constexpr (MultFamily<PCB_FAM>::enabled) {
+    *smem = LaneLayout<D>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
+    return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
+  } else {
+    *smem = 0;
+    return nullptr;
+  }
+}
+
+const void* PCB_CAT(lanes_kernel_fam, PCB_FAM)(int d, size_t* smem) {
+  switch (d) {
+#define X(D) case D: return lanes_kernel_for<D>(smem);
+    PCB_DIMS(X)
+#undef X
+  }
+  *smem = 0;
   return nullptr;
 }
 

@@ -290,3 +290,42 @@ def test_apply_rules_single_region(golden):
     assert np.array_equal(est.values, want)
     assert pb.compute_split_axis(fx, rule, 5) in range(5)
     assert pb.find_max_err(est, 1.0, rule=rule) >= 0
+
+
+# ------------------------------------------------------------------ one-region-per-lane kernel
+@pytest.mark.parametrize("fam", ["f1", "f4", "f5", "f6"])
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 7, 8, 10])
+def test_lane_kernel_equals_warp_kernel_bit_for_bit(fam, d, monkeypatch):
+    """Long lists of the multiplicative families run one region per lane, short ones one warp per
+    region (pagani_eval_lanes.cuh / pagani_eval_mult.cuh).  The results must not depend on which
+    kernel evaluated a region -- otherwise a sharded list would not reproduce the single-GPU tree."""
+    n = {1: 1000, 2: 999, 3: 777, 5: 555, 6: 333, 7: 200, 8: 130, 10: 70}[d]
+    lefts, lengths = random_boxes(d, n, 1234 + d)
+    regions, rule = pb.RegionList(lefts, lengths), pb.build_rule(d)
+    for wrap in (False, True):
+        f = pb.get_integrand(fam, d)
+        if wrap:
+            f = pb.scale_to_bounds(f, pb.IntegrationBounds([0.1] * d, [0.9 + 0.01 * j for j in range(d)]))
+        monkeypatch.setenv("PCB_PAGANI_LANES_MIN", "1")
+        lanes = pb.pagani_kernel(f, regions, rule)
+        monkeypatch.setenv("PCB_PAGANI_LANES_MIN", str(10**12))
+        warps = pb.pagani_kernel(f, regions, rule)
+        assert np.array_equal(lanes.integrals, warps.integrals), (fam, d, wrap)
+        assert np.array_equal(lanes.errors, warps.errors), (fam, d, wrap)
+        assert np.array_equal(lanes.split_axes, warps.split_axes), (fam, d, wrap)
+
+
+def test_lane_kernel_reports_first_nonfinite(monkeypatch):
+    """A non-finite evaluation surfaces exactly as in the warp kernels (pagani.py:206-209)."""
+    d = 3
+    # the Jacobian 1e160^3 overflows: every evaluation is 0 * inf or finite * inf
+    f = pb.scale_to_bounds(pb.get_integrand("f4", d), pb.IntegrationBounds([0.0] * d, [1e160] * d))
+    rl = pb.uniform_split(d, 8)
+    errs = []
+    for lanes_min in ("1", str(10**12)):
+        monkeypatch.setenv("PCB_PAGANI_LANES_MIN", lanes_min)
+        with pytest.raises(pb.GroupTaskError) as exc:
+            pb.pagani_kernel(f, rl, pb.build_rule(d))
+        cause = exc.value.cause
+        errs.append((cause.region_index, tuple(np.asarray(cause.point).tolist())))
+    assert errs[0] == errs[1]
