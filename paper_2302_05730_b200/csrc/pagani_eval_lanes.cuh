@@ -336,4 +336,249 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
   }
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// One region per lane for the families WITHOUT a multiplicative form (f2, f3, sum, constant): every rule point
+// gathers its D per-axis terms from the lane's table term[j][c] (7 abscissae per axis) and combines them in
+// numpy's own order, exactly as pagani_eval_kernel does -- the two kernels agree bit for bit, and for the
+// families without a transcendental both agree bit for bit with the reference.
+// ------------------------------------------------------------------------------------------------------------
+template <int D>
+struct GenericLaneLayout {
+  static constexpr int kFe = (1 << D) + 2 * D * D + 2 * D + 1;
+  static constexpr int kCorner0 = 2 * D * D + 2 * D + 1;
+  static constexpr int kSteps = (kFe + 63) / 64;
+  static constexpr int kTerm = 7 * D;   // doubles per lane
+  static constexpr size_t smem_bytes() { return 32 * (size_t)(kTerm + D) * 8 + 6 * 8 * 8 + (size_t)kCorner0 * 4; }
+};
+
+// corner combine over the lane's table, same association as CornerCombine (pagani_eval.cuh)
+template <class F, int D>
+struct LaneCorner {
+  static constexpr int LO = D < 6 ? D : 6;
+  double p0, p1;
+  __device__ __forceinline__ static double at(const double* term, int j, unsigned bit) { return term[(7 * j + 5 + (int)bit) * 32]; }
+  __device__ __forceinline__ void head(const double* term, unsigned bits) {
+    double t[LO];
+#pragma unroll
+    for (int j = 0; j < LO; ++j) t[j] = at(term, j, (bits >> j) & 1u);
+    if constexpr (F::combine == kSumNumpy && D >= 8) {
+      p0 = (t[0] + t[1]) + (t[2] + t[3]);
+      p1 = t[4] + t[5];
+    } else {
+      double s = t[0];
+#pragma unroll
+      for (int j = 1; j < LO; ++j) s = (F::combine == kProdSeq) ? s * t[j] : s + t[j];
+      p0 = s; p1 = 0.0;
+    }
+  }
+  __device__ __forceinline__ double tail(const double* term, unsigned bits) const {
+    if constexpr (F::combine == kSumNumpy && D >= 8) {
+      const double a6 = at(term, 6, (bits >> 6) & 1u), a7 = at(term, 7, (bits >> 7) & 1u);
+      double s = p0 + (p1 + (a6 + a7));
+#pragma unroll
+      for (int j = 8; j < D; ++j) s = s + at(term, j, (bits >> j) & 1u);
+      return s;
+    } else {
+      double s = p0;
+#pragma unroll
+      for (int j = LO; j < D; ++j) {
+        const double t = at(term, j, (bits >> j) & 1u);
+        s = (F::combine == kProdSeq) ? s * t : s + t;
+      }
+      return s;
+    }
+  }
+};
+
+template <int FAM, int D>
+__global__ void __launch_bounds__(32) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
+  using F = Family<FAM>;
+  using L = GenericLaneLayout<D>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x;
+  double* term = reinterpret_cast<double*>(smem_raw) + lane;               // term[(7j + c) * 32]
+  double* stash = term + 32 * L::kTerm;                                    // stash[j * 32]
+  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (size_t)(L::kTerm + D) * 8);   // [6][8]
+  unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                  // [kCorner0]: a | ca << 4 | b << 8 | cb << 12 | orbit << 16
+
+  const pcb_rule& rule = args.rule;
+  for (int i = lane; i < L::kCorner0; i += 32) {
+    int a = 15, b = 15, ca = 0, cb = 0, orbit = 0;
+    if (i == 0) {
+    } else if (i <= 2 * D) {
+      int q = i - 1; a = q >> 1; ca = 1 + (q & 1); orbit = 1;
+    } else if (i <= 4 * D) {
+      int q = i - 1 - 2 * D; a = q >> 1; ca = 3 + (q & 1); orbit = 2;
+    } else {
+      int q = i - 1 - 4 * D, pr = q >> 2, sg = q & 3, idx = 0;
+      for (int j = 0; j < D; ++j)
+        for (int k = j + 1; k < D; ++k, ++idx)
+          if (idx == pr) { a = j; b = k; }
+      ca = 3 + (sg & 1); cb = 3 + (sg >> 1); orbit = 3;
+    }
+    desc[i] = (unsigned)a | ((unsigned)ca << 4) | ((unsigned)b << 8) | ((unsigned)cb << 12) | ((unsigned)orbit << 16);
+  }
+  if (lane < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
+    const int o = lane / 5, k = lane % 5;
+    double w = rule.weights[k][o < 5 ? o : 4];
+    if (o == 5 && rule.corner_parity[k]) w = -w;
+    s_w[o * 8 + k] = w;
+  }
+  __syncwarp();
+  const double jac = args.f.bounded ? args.f.jac : 1.0;   // x * 1.0 == x
+
+  // centre / axial / pair point i: its D terms in numpy's order
+  auto plain_value = [&](int i, int& row) -> double {
+    const unsigned dsc = desc[i];
+    const int a = dsc & 15u, ca = (dsc >> 4) & 15u, b = (dsc >> 8) & 15u, cb = (dsc >> 12) & 15u;
+    row = (int)(dsc >> 16);
+    double t[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t[j] = term[(7 * j + (j == a ? ca : (j == b ? cb : 0))) * 32];
+    return F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
+  };
+
+  for (long long batch = blockIdx.x; batch * 32 < args.n; batch += gridDim.x) {
+    const long long r = batch * 32 + lane;
+    const bool live = r < args.n;
+    const long long rc = live ? r : args.n - 1;
+    double vol = 1.0;
+    double next_left = args.lefts[rc], next_len = args.lengths[rc];
+#pragma unroll 1
+    for (int j = 0; j < D; ++j) {
+      const double left = next_left, len = next_len;
+      if (j + 1 < D) {
+        next_left = args.lefts[(j + 1) * args.ld + rc];
+        next_len = args.lengths[(j + 1) * args.ld + rc];
+      }
+      vol = (j == 0) ? len : vol * len;   // np.prod, left to right
+#pragma unroll
+      for (int c = 0; c < 7; ++c) {
+        const double x = left + len * rule.offsets[c];   // quadrature.py:301-302: mul, then add
+        term[(7 * j + c) * 32] = axis_term<F>(j, x, args.f);
+      }
+    }
+
+    constexpr int W = 8;
+    double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
+    int axis = 0;
+    auto split_note = [&](int i, double fx) {   // pagani.py:215-223: running first maximum over the axes
+      if constexpr (D > 1) {
+        if (i > 4 * D) return;
+        const int q = i - 1;
+        if (i == 0) two_f0 = 2.0 * fx;
+        else if (!(q & 1)) first_of_pair = fx;
+        else {
+          const double d2 = (first_of_pair + fx) - two_f0;
+          const int a = (q >= 2 * D ? q - 2 * D : q) >> 1;
+          if (q < 2 * D) stash[a * 32] = d2;
+          else {
+            const double ind = fabs(rule.split_weights[0] * stash[a * 32] - rule.split_weights[1] * d2);
+            if (ind > best) { best = ind; axis = a; }
+          }
+        }
+      }
+    };
+    double hold[3][5];
+    double cur[5];
+#pragma unroll 1
+    for (int blk = 0; blk < 64 / W; ++blk) {
+      const int vt0 = W * blk;
+      double acc[W][5];
+      LaneCorner<F, D> head[W];
+#pragma unroll
+      for (int v = 0; v < W; ++v) {
+        const double init = vt0 + v < L::kFe ? -0.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) acc[v][k] = init;
+        head[v].head(term, (unsigned)(vt0 + v - L::kCorner0) & 63u);
+      }
+#pragma unroll 1
+      for (int s = 0; s < L::kSteps; ++s) {
+        const int lo = vt0 + 64 * s, hi = lo + W - 1;
+        if (hi < L::kCorner0) {                                    // W centre / axial / pair points
+          double fx[W];
+          int row[W];
+#pragma unroll
+          for (int v = 0; v < W; ++v) fx[v] = plain_value(lo + v, row[v]);
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            split_note(lo + v, fx[v]);
+            const double* w = s_w + 8 * row[v];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
+          }
+        } else if (lo >= L::kCorner0 && hi < L::kFe) {             // W corner points
+          double fx[W];
+#pragma unroll
+          for (int v = 0; v < W; ++v)
+            fx[v] = F::template finish<D>(head[v].tail(term, (unsigned)(lo + v - L::kCorner0)), args.f) * jac;
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            const double* w = s_w + 8 * (4 + (__popc((unsigned)(lo + v - L::kCorner0)) & 1));
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
+          }
+        } else if (lo < L::kFe) {                                  // the block straddles a class boundary
+#pragma unroll
+          for (int v = 0; v < W; ++v) {
+            const int i = lo + v;
+            double fx;
+            int row;
+            if (i < L::kCorner0) {
+              fx = plain_value(i, row);
+              split_note(i, fx);
+            } else if (i < L::kFe) {
+              const unsigned bits = (unsigned)(i - L::kCorner0);
+              fx = F::template finish<D>(head[v].tail(term, bits), args.f) * jac;
+              row = 4 + (__popc(bits) & 1);
+            } else {
+              continue;
+            }
+            const double* w = s_w + 8 * row;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx;
+          }
+        }
+      }
+#pragma unroll
+      for (int span = 1; span < W; span *= 2)
+#pragma unroll
+        for (int v = 0; v < W; v += 2 * span)
+#pragma unroll
+          for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + acc[v + span][k];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) cur[k] = acc[0][k];
+      counter_merge<0, 3>(blk, cur, hold);
+    }
+
+    double v[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] = vol * cur[k];
+    if (live) {
+      if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]) && isfinite(v[3]) && isfinite(v[4]))) {
+        // rare: find the first non-finite evaluation of this region (pagani.py:206-209)
+        for (int i = 0; i < L::kFe; ++i) {
+          double fx;
+          int row;
+          if (i < L::kCorner0) fx = plain_value(i, row);
+          else {
+            LaneCorner<F, D> cc;
+            const unsigned bits = (unsigned)(i - L::kCorner0);
+            cc.head(term, bits & 63u);
+            fx = F::template finish<D>(cc.tail(term, bits), args.f) * jac;
+          }
+          if (!isfinite(fx)) {
+            atomicMin(args.bad, (unsigned long long)r * (unsigned long long)L::kFe + (unsigned long long)i);
+            break;
+          }
+        }
+      }
+      args.integrals[r] = v[0];
+      args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
+      args.split_axes[r] = axis;
+    }
+  }
+}
+
 }  // namespace pcb

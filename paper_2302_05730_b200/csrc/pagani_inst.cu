@@ -30,15 +30,20 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
   return nullptr;
 }
 
-// one-region-per-lane kernel (multiplicative families only) and its dynamic shared memory
+// one-region-per-lane kernel (multiplicative or generic form) and its dynamic shared memory
 template <int D>
 static const void* lanes_kernel_for(size_t* smem) {
   if constexpr (MultFamily<PCB_FAM>::enabled) {
     *smem = LaneLayout<D>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
     return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
-  } else {
+  } else if constexpr (PCB_FAM == PCB_F3_CORNER_PEAK) {
+    // the double-double power dominates f3 and the warp-per-region kernel hides its latency better (measured:
+    // 1.08 ms vs 1.67 ms for 390625 regions at d = 8)
     *smem = 0;
     return nullptr;
+  } else {
+    *smem = GenericLaneLayout<D>::smem_bytes();
+    return (const void*)&pagani_eval_lanes_generic_kernel<PCB_FAM, D>;
   }
 }
 

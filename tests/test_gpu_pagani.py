@@ -293,12 +293,12 @@ def test_apply_rules_single_region(golden):
 
 
 # ------------------------------------------------------------------ one-region-per-lane kernel
-@pytest.mark.parametrize("fam", ["f1", "f4", "f5", "f6"])
+@pytest.mark.parametrize("fam", FAMILIES)
 @pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 7, 8, 10])
 def test_lane_kernel_equals_warp_kernel_bit_for_bit(fam, d, monkeypatch):
-    """Long lists of the multiplicative families run one region per lane, short ones one warp per
-    region (pagani_eval_lanes.cuh / pagani_eval_mult.cuh).  The results must not depend on which
-    kernel evaluated a region -- otherwise a sharded list would not reproduce the single-GPU tree."""
+    """Long lists run one region per lane, short ones one warp per region (pagani_eval_lanes.cuh vs
+    pagani_eval.cuh / pagani_eval_mult.cuh).  The results must not depend on which kernel evaluated
+    a region -- otherwise a sharded list would not reproduce the single-GPU tree."""
     n = {1: 1000, 2: 999, 3: 777, 5: 555, 6: 333, 7: 200, 8: 130, 10: 70}[d]
     lefts, lengths = random_boxes(d, n, 1234 + d)
     regions, rule = pb.RegionList(lefts, lengths), pb.build_rule(d)
@@ -313,6 +313,9 @@ def test_lane_kernel_equals_warp_kernel_bit_for_bit(fam, d, monkeypatch):
         assert np.array_equal(lanes.integrals, warps.integrals), (fam, d, wrap)
         assert np.array_equal(lanes.errors, warps.errors), (fam, d, wrap)
         assert np.array_equal(lanes.split_axes, warps.split_axes), (fam, d, wrap)
+        if fam in EXACT and not wrap:   # and both are the reference, bit for bit
+            i, e, k = po.pagani_evaluate(fam, lefts, lengths, rule_dict(rule))
+            assert np.array_equal(lanes.integrals, i) and np.array_equal(lanes.errors, e) and np.array_equal(lanes.split_axes, k)
 
 
 def test_lane_kernel_reports_first_nonfinite(monkeypatch):
