@@ -50,6 +50,29 @@ WORKLOADS = {
 }
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, from the committed `ncu --set full` capture of
+# the same kernel at the same size (scripts/collect_profiles.sh writes profiles/<round>_ncu_*.txt)
+TRAFFIC_PROFILE = {"config2": "r1_ncu_vsample_config2.txt", "config4": "r1_ncu_vsample_config4.txt",
+                   "config3": "r1_ncu_pagani_lanes_f1_d8.txt", "config1": "r1_ncu_pagani_warp_f4_d5_small.txt"}
+
+
+def dram_traffic_bytes(workload):
+    """(bytes per launch, source file) of the dominant kernel, or (None, None) when no capture is committed."""
+    name = TRAFFIC_PROFILE.get(workload)
+    path = os.path.join(ROOT, "profiles", name) if name else None
+    if not path or not os.path.exists(path):
+        return None, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total, seen = 0.0, 0
+    for line in open(path):
+        line = line.strip()
+        if line.startswith(("dram__bytes_read.sum", "dram__bytes_write.sum")):
+            unit = line[line.index("[") + 1:line.index("]")]
+            total += float(line.split("=")[1]) * scale.get(unit, 1.0)
+            seen += 1
+    return (total, "profiles/" + name) if seen == 2 else (None, None)
+
+
 def flops_per_eval(w):
     d = w["d"]
     return FORMULA_FLOPS[w["family"]](d) + (2 * d + 10 if w["kind"] == "pagani" else 10 * d + 4)
@@ -278,7 +301,6 @@ def main():
         region_s = time.perf_counter() - t_region
     kind = 0 if w["kind"] == "pagani" else 1
     k_ms, k_launches, k_units = ctx.profile_end(kind)
-    bin_ms, bin_launches, _ = ctx.profile_end(2) if kind == 1 else (0.0, 0, 0.0)
     launches = ctx.launch_count() - launches0
 
     # max over ranks of the timed durations (device seconds and API wall-clock)
@@ -287,6 +309,7 @@ def main():
         dev_s, wall_s, k_ms = (float(x) for x in agg)
         k_units *= 1  # per-rank units; the roofline below is per GPU
     fpe = flops_per_eval(w)
+    traffic, traffic_src = dram_traffic_bytes(name)
     evals_per_unit = F_EVAL[w["d"]] if w["kind"] == "pagani" else 1
     achieved = (k_units * evals_per_unit * fpe) / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
 
@@ -301,12 +324,16 @@ def main():
         "e2e": {"value": evals / wall_s, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": 1e3 * wall_s / args.steps, "api": "refine()/mcubes_run() C-ABI call, host structs in, host records out"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "fp64", "kernel": "pagani_eval_kernel" if kind == 0 else "vsample_kernel",
+        "roofline": {"bound": "fp64",
+                     "bound_note": "FP64 vector pipe (DFMA): the path is ~100 flop per HBM byte and is no dense contraction, "
+                                   "so neither the HBM nor the tensor roofline binds it (BASELINE.json north_star)",
+                     "kernel": ("pagani_eval_lanes_kernel / pagani_eval_mult_kernel (one region per lane / per warp)" if kind == 0
+                                else "vsample_kernel"),
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                     "traffic": None, "launches": int(k_launches), "avg_launch_ms": k_ms / max(k_launches, 1),
+                     "traffic": traffic, "traffic_unit": "bytes of DRAM read+write per launch (ncu --set full capture)",
+                     "traffic_source": traffic_src, "launches": int(k_launches), "avg_launch_ms": k_ms / max(k_launches, 1),
                      "flops_per_eval": fpe, "evals_per_launch": k_units * evals_per_unit / max(k_launches, 1),
                      "kernel_share_of_step": k_ms * 1e-3 / dev_s if dev_s else None,
-                     "bin_kernel_avg_launch_ms": bin_ms / max(bin_launches, 1) if kind == 1 else None,
                      "peak_source": "DFMA micro-benchmark run live (MEASURED_PEAKS.json has no FP64 entry; nominal 37 TFLOP/s)"},
         "clocks": clocks.summary(),
         "timed_region_s": region_s,

@@ -7,81 +7,6 @@
 
 namespace pcb {
 
-// Accumulate sample records into the contribution table.  Each warp serves ONE axis: its private
-// table is a single row (n_bins doubles + n_bins tag bytes, 4.5 KB at 500 bins), so a CTA holds
-// d x R warps (up to 32) and the SM's latency is hidden by occupancy instead of by a 36 KB table per
-// warp.  The d warps of a stream read the same records (L1/L2 hits on the contributions), two
-// records per lane and round.  Tables are merged stream -> CTA here, CTA -> grid by merge_hist_kernel.
-__global__ void __launch_bounds__(512, 3) bin_kernel(const __grid_constant__ BinArgs a, int d, int streams) {
-  if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb = a.nb;
-  const int W = blockDim.x >> 5;                                  // = d * streams
-  double* s_hist = reinterpret_cast<double*>(smem_raw);           // [W][nb]
-  unsigned char* s_tag = reinterpret_cast<unsigned char*>(s_hist + (size_t)W * nb);  // [W][nb]
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int axis = wib % d, stream = wib / d;
-  for (int i = threadIdx.x; i < W * nb; i += blockDim.x) s_hist[i] = 0.0;
-  __syncthreads();
-  double* __restrict__ hist = s_hist + (size_t)wib * nb;
-  unsigned char* __restrict__ tags = s_tag + (size_t)wib * nb;
-  const unsigned short* __restrict__ bins = a.rec_b + (long long)axis * a.rec_capacity;
-
-  // record pairs (64 records) are dealt round-robin to the streams of the grid; n_groups is even (host pads)
-  const long long n_pairs = a.n_groups / 2, step = (long long)gridDim.x * streams;
-  long long pr = (long long)blockIdx.x * streams + stream;
-  const double* __restrict__ pw = a.rec_w + pr * 64 + lane;
-  const unsigned short* __restrict__ pb = bins + pr * 64 + lane;
-  const long long hop = step * 64;
-  double w0 = 0.0, w1 = 0.0;
-  int b0 = 0, b1 = 0;
-  if (pr < n_pairs) { w0 = pw[0]; w1 = pw[32]; b0 = pb[0]; b1 = pb[32]; }
-  for (; pr < n_pairs; pr += step) {
-    // prefetch the next pair while this one is applied
-    double nw0 = 0.0, nw1 = 0.0;
-    int nb0 = 0, nb1 = 0;
-    pw += hop; pb += hop;
-    if (pr + step < n_pairs) { nw0 = pw[0]; nw1 = pw[32]; nb0 = pb[0]; nb1 = pb[32]; }
-    // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
-    // two records of one lane in the same bin become one update
-    const bool same = b0 == b1;
-    const double add0 = same ? w0 + w1 : w0, add1 = w1;
-    unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
-    // Arbitration rounds.  Only lanes that still have an update pending touch shared memory: the table is
-    // bound by shared-memory wavefronts (random 64-bit read-modify-write = ~10 wavefronts per warp), so the
-    // second round -- a handful of collision losers -- must not replay the loads of the whole warp.
-#pragma unroll 1
-    for (int round = 0; round < 2; ++round) {
-      if (want & 1u) tags[b0] = (unsigned char)lane;
-      if (want & 2u) tags[b1] = (unsigned char)lane;
-      __syncwarp();
-      bool win0 = false, win1 = false;
-      if (want & 1u) win0 = tags[b0] == lane;
-      if (want & 2u) win1 = tags[b1] == lane;
-      if (win0) hist[b0] = hist[b0] + add0;
-      if (win1) hist[b1] = hist[b1] + add1;
-      want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
-      __syncwarp();
-      if (!__any_sync(PCB_FULL_MASK, want)) break;
-    }
-    if (__any_sync(PCB_FULL_MASK, want)) {  // triple collisions: shared-memory CAS atomic
-      if (want & 1u) atomicAdd(hist + b0, add0);
-      if (want & 2u) atomicAdd(hist + b1, add1);
-      __syncwarp();
-    }
-    w0 = nw0; w1 = nw1; b0 = nb0; b1 = nb1;
-  }
-  __syncthreads();
-  double* dst = a.block_hist + (size_t)blockIdx.x * d * nb;
-  for (int i = threadIdx.x; i < d * nb; i += blockDim.x) {
-    const int j = i / nb, k = i - j * nb;
-    double t = s_hist[(size_t)j * nb + k];
-    for (int q = 1; q < streams; ++q) t = t + s_hist[(size_t)(q * d + j) * nb + k];
-    dst[i] = a.accumulate ? dst[i] + t : t;
-  }
-}
-
-
 // CTA tables -> contribution table in a fixed order: a CTA owns 32 bins; thread (chunk c, bin i) adds the
 // tables of blocks [c*per, (c+1)*per) serially, then the chunk sums of a bin are added in chunk order.
 constexpr int kReduceThreads = 256;

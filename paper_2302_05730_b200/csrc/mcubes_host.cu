@@ -17,12 +17,10 @@ enum { M_BAD = 0, M_CLAMPS = 1, M_INTEGRAL = 2, M_VARIANCE = 3 };  // slots in c
 constexpr int kMcSlot = 40;
 
 struct SampleLaunch {
-  int blocks = 0;        // sampling CTAs (kSampleWarps warps each)
-  size_t smem = 0;       // boundaries table
+  int blocks = 0;        // CTAs (kSampleWarps warps each)
+  size_t smem = 0;       // boundaries + table rows + staged records
   int nseg = 1;
   long long seg_len = 0;
-  int bin_warps = 0;     // warps per accumulation CTA (one private table each)
-  size_t bin_smem = 0;
 };
 
 static pcb_status validate_plan(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan) {
@@ -39,19 +37,12 @@ static pcb_status validate_plan(pcb_ctx* ctx, const pcb_integrand* f, const pcb_
 }
 
 static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long long n_local_threads, SampleLaunch* out) {
-  const size_t bounds_bytes = (size_t)plan->d * (plan->n_bins + 1) * sizeof(double);
-  const size_t per_warp = (size_t)plan->n_bins * (sizeof(double) + 1);  // one axis row + its tag bytes
-  const size_t avail = ctx->smem_optin > 1024 ? ctx->smem_optin - 1024 : 0;
-  if (avail < bounds_bytes || avail < per_warp * plan->d)
+  out->smem = vsample_smem_bytes(plan->d, plan->n_bins);
+  if (out->smem > ctx->smem_optin)
     return fail(ctx, PCB_INVALID, "d=%d, n_bins=%d needs %zu B of shared memory per CTA, device offers %zu", plan->d,
-                plan->n_bins, std::max(bounds_bytes, per_warp * plan->d) + 1024, ctx->smem_optin);
+                plan->n_bins, out->smem, ctx->smem_optin);
   const long long n_lw = (n_local_threads + 31) / 32;
-  out->smem = bounds_bytes;
-  // accumulation CTA: d warps (one per axis) per record stream, as many streams as fit in 32 warps / shared memory
-  const int streams = (int)std::max<size_t>(1, std::min<size_t>(16 / plan->d, avail / (per_warp * plan->d)));
-  out->bin_warps = streams * plan->d;
-  out->bin_smem = (size_t)out->bin_warps * per_warp + 16;
-  // work units = logical warps x segments; aim at >= 8 units per resident warp for balance
+  // work units = 32 segments; aim at >= 8 units per resident warp for balance
   const long long resident = 2LL * ctx->sm_count * kSampleWarps;
   int nseg = (int)std::max<long long>(1, std::min<long long>(plan->s, (8 * resident + n_lw - 1) / n_lw));
   if (const char* env = std::getenv("PCB_MCUBES_SEGMENTS")) {
@@ -169,28 +160,12 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   SampleLaunch L;
   PCB_TRY(plan_launch(ctx, plan, nt, &L));
   const void* fn = vsample_kernel_ptr(f->family, d, rng_kind);
-  const void* bin_fn = (const void*)&bin_kernel;
   PCB_TRY(grant_smem(ctx, fn, L.smem));
-  PCB_TRY(grant_smem(ctx, bin_fn, L.bin_smem));
 
-  // record buffer: one contribution (8 B) + d bin ids (2 B each) per sample slot, chunked over work units
   const long long n_segments = nt * L.nseg, units = (n_segments + 31) / 32;
-  const long long rec_per_unit = round_up(L.seg_len * plan->p, 2) * 32;  // even number of 32-record groups
-  const size_t rec_bytes = 8 + 2 * (size_t)d;
-  size_t budget = (size_t)24 << 30;
-  if (const char* env = std::getenv("PCB_MCUBES_RECORD_BYTES")) budget = (size_t)std::max(1LL, std::atoll(env));
-  budget = std::min(budget, (size_t)(ctx->total_mem * 0.4));
-  long long chunk_units = (long long)std::max<size_t>(1, budget / ((size_t)rec_per_unit * rec_bytes));
-  chunk_units = std::min(chunk_units, units);
-  const long long rec_capacity = round_up(chunk_units * rec_per_unit, 64);
-  PCB_CUDA_TRY(ctx, ctx->mc_rec.ensure((size_t)rec_capacity * rec_bytes));
-
-  // accumulation grid: three 16-warp CTAs per SM (48 resident warps) for big passes, fewer for small ones
-  const long long total_pairs = std::min(units, chunk_units) * rec_per_unit / 64;
-  const int bin_streams = L.bin_warps / d;
-  const int bin_blocks = (int)std::max<long long>(1, std::min<long long>(3LL * ctx->sm_count, total_pairs / (32LL * bin_streams)));
+  const int vs_blocks = L.blocks;
   PCB_CUDA_TRY(ctx, ctx->mc_seg.ensure((size_t)nt * L.nseg * 2 * sizeof(double)));
-  PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)bin_blocks * d * nb * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->mc_hist.ensure((size_t)vs_blocks * d * nb * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure((size_t)d * nb * sizeof(double)));
   const long long n_groups = (nt + plan->group_size - 1) / plan->group_size;
   PCB_CUDA_TRY(ctx, ctx->mc_group.ensure((size_t)n_groups * 4 * sizeof(double)));
@@ -227,45 +202,17 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   a.seg_partials = ctx->mc_seg.as<double>();
   a.clamps = sc_u + M_CLAMPS;
   a.bad = sc_u + M_BAD;
-  a.rec_per_unit = rec_per_unit;
-  a.rec_capacity = rec_capacity;
-  a.rec_w = ctx->mc_rec.as<double>();
-  a.rec_b = reinterpret_cast<unsigned short*>(ctx->mc_rec.as<double>() + rec_capacity);
+  a.n_units = units;
+  a.block_hist = ctx->mc_hist.as<double>();
   a.stop = tail.stop;
   a.iteration = tail.iteration;
-
-  BinArgs b;
-  b.nb = nb;
-  b.rec_capacity = rec_capacity;
-  b.rec_w = a.rec_w;
-  b.rec_b = a.rec_b;
-  b.block_hist = ctx->mc_hist.as<double>();
-  b.stop = tail.stop;
-  b.iteration = tail.iteration;
-
-  for (long long u0 = 0, chunk = 0; u0 < units; u0 += chunk_units, ++chunk) {
-    a.unit_begin = u0;
-    a.unit_end = std::min(units, u0 + chunk_units);
-    const long long n_units = a.unit_end - a.unit_begin;
-    const int blocks = (int)std::max<long long>(1, std::min<long long>(L.blocks, (n_units + kSampleWarps - 1) / kSampleWarps));
+  {
+    // units of work for the roofline: the samples actually drawn (active lanes)
+    const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
+    ProfileSpan span(ctx, 1, (double)(c1 - c0) * plan->p, tail.iteration);
     void* args[] = {&a};
-    {
-      // units of work for the roofline: the samples actually drawn (active lanes) in this chunk
-      const double frac = (double)n_units / (double)units;
-      const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
-      ProfileSpan span(ctx, 1, frac * (double)(c1 - c0) * plan->p, tail.iteration);
-      PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
-      ctx->launches++;
-    }
-    b.n_groups = n_units * rec_per_unit / 32;
-    b.accumulate = chunk > 0;
-    int d_arg = d, streams_arg = L.bin_warps / d;
-    void* bargs[] = {&b, &d_arg, &streams_arg};
-    {
-      ProfileSpan span(ctx, 2, (double)b.n_groups * 32.0, tail.iteration);
-      PCB_CUDA_TRY(ctx, cudaLaunchKernel(bin_fn, dim3(bin_blocks), dim3(L.bin_warps * 32), bargs, L.bin_smem, ctx->stream));
-      ctx->launches++;
-    }
+    PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(vs_blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
+    ctx->launches++;
   }
 
   // table merge + work-group trees in one launch
@@ -275,7 +222,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   r.stop = tail.stop;
   r.iteration = tail.iteration;
   r.block_hist = ctx->mc_hist.as<double>();
-  r.nblocks = bin_blocks;
+  r.nblocks = vs_blocks;
   r.nbins_total = d * nb;
   r.merge_ctas = (d * nb + 31) / 32;
   r.contrib = ctx->mc_contrib.as<double>();

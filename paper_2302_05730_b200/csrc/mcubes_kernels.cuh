@@ -8,15 +8,16 @@
 // uniform(seed, T, (L*p + k)*d + j), so the sample set is identical to the reference's for any
 // partition of threads over warps, segments or GPUs.
 //
-// The pass is two kernels:
-//   vsample_kernel  pure compute at 16 warps/SM: hash -> stratified y -> grid transform -> f -> per-cube
-//                   (S1, S2, estimate, variance); it emits one compact record per sample
-//                   (contribution, d bin ids) to HBM instead of touching a histogram;
-//   bin_kernel      streams the records and accumulates the (d x n_bins) contribution table.
-// Shared-memory FP64 atomicAdd is a CAS loop on sm_100 (ATOMS.CAST.SPIN), so in bin_kernel each warp
-// owns a private table in shared memory, arbitrates intra-warp collisions with one tag round and lets
-// the few losers use the CAS atomic; tables are merged warp -> CTA -> grid in a fixed order.
-// Keeping the table out of the sampling kernel is what lifts it from 5 to 16 resident warps per SM.
+// The pass is ONE kernel.  A CTA (8 warps, two CTAs per SM) alternates two phases per round:
+//   sample    every warp draws two samples per lane (hash -> stratified y -> grid transform -> f -> per-cube S1, S2,
+//             estimate, variance) and stages one record per sample -- contribution and D bin ids -- in shared memory;
+//   bin       warp w serves axis w (w + 8 for D > 8): it adds the CTA's 512 staged records into ITS private row of
+//             the contribution table (n_bins doubles in shared memory).  Shared-memory FP64 atomicAdd is a CAS loop
+//             on sm_100 (ATOMS.CAST.SPIN), so same-bin lanes are arbitrated by a tag round (winner does a plain
+//             read-modify-write), losers take a second round, triple collisions use the CAS atomic.
+// The sample phase is bound by the FP64 / integer pipes, the bin phase by shared-memory wavefronts; with two CTAs
+// per SM out of phase the two overlap, and no sample record ever travels to HBM.  Rows are merged CTA -> grid in a
+// fixed order (reduce_kernel), so the table is deterministic.
 #pragma once
 
 #include "pcb_device.cuh"
@@ -67,24 +68,9 @@ struct SampleArgs {
   double* seg_partials;         // [(t - t_begin) * nseg + q][2]
   unsigned long long* clamps;
   unsigned long long* bad;      // min over non-finite samples of cube*p + k
-  // sample records of this launch's units [unit_begin, unit_end): record r of unit u sits at
-  // (u - unit_begin) * rec_per_unit + r with r = (cube_step * p + k) * 32 + lane
-  long long unit_begin, unit_end, rec_per_unit, rec_capacity;
-  double* rec_w;                // [rec_capacity] contribution (v^2, or f^2 when not squared_weighted)
-  unsigned short* rec_b;        // [d][rec_capacity] bin ids
+  long long n_units;            // work units (32 segments each)
+  double* block_hist;           // [gridDim.x][d*nb]: the CTA's rows of the contribution table
   const int* stop;              // iteration at which the run stopped (INT_MAX while running); may be NULL
-  int iteration;
-};
-
-struct BinArgs {
-  int nb;
-  long long n_groups;           // record groups of 32
-  long long rec_capacity;
-  const double* rec_w;
-  const unsigned short* rec_b;
-  double* block_hist;           // [gridDim.x][d*nb], accumulated across launches
-  int accumulate;               // 0: overwrite block_hist, 1: add to it
-  const int* stop;
   int iteration;
 };
 
@@ -124,27 +110,92 @@ __device__ __forceinline__ void draw_sample(const SampleArgs& a, const double* s
   v = fx * jac;
 }
 
-constexpr int kSampleWarps = 8;  // warps per sampling CTA; two CTAs per SM at 128 registers
+constexpr int kSampleWarps = 8;  // warps per CTA; two CTAs per SM at 128 registers
+
+// shared memory of one CTA: boundaries, one table row + tag bytes per axis, the staged records of one round
+__host__ __device__ inline size_t vsample_smem_bytes(int d, int nb) {
+  const size_t tags = (size_t)((nb + 15) & ~15);
+  return (size_t)d * (nb + 1) * 8 + 8 /* pad */ + (size_t)d * ((size_t)nb * 8 + tags) + 2 * kSampleWarps * 32 * 8 +
+         (size_t)d * 2 * kSampleWarps * 32 * 2;
+}
+
+// Add two staged records per lane into the warp's private row (see the header comment).
+__device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
+                                         double w1, int b1) {
+  // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
+  // two records of one lane in the same bin become one update
+  const bool same = b0 == b1;
+  const double add0 = same ? w0 + w1 : w0, add1 = w1;
+  unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
+  // Only lanes that still have an update pending touch shared memory: the table is bound by shared-memory
+  // wavefronts, so the second round -- a handful of collision losers -- must not replay the whole warp's loads.
+#pragma unroll 1
+  for (int round = 0; round < 2; ++round) {
+    if (!__any_sync(PCB_FULL_MASK, want)) return;
+    if (want & 1u) tags[b0] = (unsigned char)lane;
+    if (want & 2u) tags[b1] = (unsigned char)lane;
+    __syncwarp();
+    bool win0 = false, win1 = false;
+    if (want & 1u) win0 = tags[b0] == lane;
+    if (want & 2u) win1 = tags[b1] == lane;
+    if (win0) hist[b0] = hist[b0] + add0;
+    if (win1) hist[b1] = hist[b1] + add1;
+    want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
+    __syncwarp();
+  }
+  if (__any_sync(PCB_FULL_MASK, want)) {  // triple collisions: shared-memory CAS atomic
+    if (want & 1u) atomicAdd(hist + b0, add0);
+    if (want & 2u) atomicAdd(hist + b1, add1);
+    __syncwarp();
+  }
+}
 
 template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int nb1 = a.nb + 1;
-  double* s_b = reinterpret_cast<double*>(smem_raw);            // [D][nb+1]
+  const int nb = a.nb, nb1 = a.nb + 1;
+  const size_t tag_bytes = (size_t)((nb + 15) & ~15);
+  double* s_b = reinterpret_cast<double*>(smem_raw);                                   // [D][nb+1]
+  double* s_hist = s_b + (((size_t)D * nb1 + 1) & ~(size_t)1);                         // [D][nb]
+  unsigned char* s_tag = reinterpret_cast<unsigned char*>(s_hist + (size_t)D * nb);    // [D][tag_bytes]
+  double* s_rw = reinterpret_cast<double*>(s_tag + (size_t)D * tag_bytes);             // [2][kSampleWarps][32]
+  unsigned short* s_rb = reinterpret_cast<unsigned short*>(s_rw + 2 * kSampleWarps * 32);  // [D][2][kSampleWarps][32]
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
+  for (int i = threadIdx.x; i < D * nb; i += blockDim.x) s_hist[i] = 0.0;
   __syncthreads();
 
   const int p = a.p;
   const double pd = (double)p;
   unsigned long long clamp_count = 0;
+  constexpr int kSlot = kSampleWarps * 32;   // records per staged sample slot
+  // stage one sample of this lane: slot 0 or 1 of the round
+  auto stage = [&](int slot, double w, const int (&bin)[D]) {
+    s_rw[slot * kSlot + wib * 32 + lane] = w;
+#pragma unroll
+    for (int j = 0; j < D; ++j) s_rb[(j * 2 + slot) * kSlot + wib * 32 + lane] = (unsigned short)bin[j];
+  };
+  // all warps: the staged round is complete -> add it to the rows -> staging may be overwritten
+  auto bin_round = [&]() {
+    __syncthreads();
+    for (int j = wib; j < D; j += kSampleWarps) {
+      double* hist = s_hist + (size_t)j * nb;
+      unsigned char* tags = s_tag + (size_t)j * tag_bytes;
+#pragma unroll 2
+      for (int w = 0; w < kSampleWarps; ++w)
+        bin_pair(hist, tags, lane, s_rw[w * 32 + lane], s_rb[(j * 2) * kSlot + w * 32 + lane], s_rw[kSlot + w * 32 + lane],
+                 s_rb[(j * 2 + 1) * kSlot + w * 32 + lane]);
+    }
+    __syncthreads();
+  };
 
-  for (long long u = a.unit_begin + (long long)blockIdx.x * kSampleWarps + wib; u < a.unit_end;
-       u += (long long)gridDim.x * kSampleWarps) {
+  // the CTA takes kSampleWarps units at a time (one per warp); all units have the same number of rounds
+  for (long long ub = (long long)blockIdx.x * kSampleWarps; ub < a.n_units; ub += (long long)gridDim.x * kSampleWarps) {
+    const long long u = ub + wib;
     const unsigned long long sin = (unsigned long long)u * 32ULL + (unsigned long long)lane;
-    const bool live = sin < (unsigned long long)a.n_segments;
+    const bool live = u < a.n_units && sin < (unsigned long long)a.n_segments;
     unsigned long long sigma = 0, qq_seg = 0;
     if (live) fast_divmod(sin * a.seg_mul, a.div_segments, sigma);
     const long long T = a.t_begin + (long long)fast_divmod(sigma, a.div_nseg, qq_seg);
@@ -175,11 +226,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
     unsigned long long ctr = (unsigned long long)(q * a.seg_len) * (unsigned long long)p * D;
     unsigned long long kc = key + (ctr + 1ULL) * kGolden;
     double sum_est = 0.0, sum_var = 0.0;
-    double* rw = a.rec_w + (u - a.unit_begin) * a.rec_per_unit + lane;
-    unsigned short* rb = a.rec_b + (u - a.unit_begin) * a.rec_per_unit + lane;
 
-    // every lane walks the full segment so that the record block of the unit is completely written;
-    // lanes past their own cube range emit empty records
+    // every lane of every warp walks the full segment (the rounds are CTA-wide); lanes past their own cube
+    // range stage empty records
     for (long long i = 0; i < a.seg_len; ++i) {
       const bool active = i < count;
       const unsigned long long inj_cube = (unsigned long long)(c_begin + i) * (unsigned long long)p;
@@ -202,13 +251,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
         // 8-accumulator tree -- only the rounding differs)
         s1 = (k == 0) ? v[0] + v[1] : (s1 + v[0]) + v[1];
         s2 = (k == 0) ? v2[0] + v2[1] : (s2 + v2[0]) + v2[1];
-#pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2) {
-          const long long r = (i * p + k + q2) * 32;
-          rw[r] = active ? (a.squared_weighted ? v2[q2] : fx[q2] * fx[q2]) : 0.0;
-#pragma unroll
-          for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = (unsigned short)bin[q2][j];
-        }
+        stage(0, active ? (a.squared_weighted ? v2[0] : fx[0] * fx[0]) : 0.0, bin[0]);
+        stage(1, active ? (a.squared_weighted ? v2[1] : fx[1] * fx[1]) : 0.0, bin[1]);
+        bin_round();
       }
       for (; k < p; ++k) {
         int bin[D];
@@ -220,10 +265,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
         const double v2 = v * v;
         s1 = (k == 0) ? v : s1 + v;
         s2 = (k == 0) ? v2 : s2 + v2;
-        const long long r = (i * p + k) * 32;
-        rw[r] = active ? (a.squared_weighted ? v2 : fx * fx) : 0.0;
-#pragma unroll
-        for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = (unsigned short)bin[j];
+        stage(0, active ? (a.squared_weighted ? v2 : fx * fx) : 0.0, bin);
+        stage(1, 0.0, bin);
+        bin_round();
       }
       if (active) {
         const double est = s1 / a.den_est;
@@ -241,12 +285,6 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
         coord[j] = 0.0;
       }
     }
-    if ((a.seg_len * p) & 1) {  // units hold an even number of 32-record groups: blank the padding group
-      const long long r = a.seg_len * p * 32;
-      rw[r] = 0.0;
-#pragma unroll
-      for (int j = 0; j < D; ++j) rb[(long long)j * a.rec_capacity + r] = 0;
-    }
     if (live) {
       double* out = a.seg_partials + sigma * 2;
       out[0] = sum_est;
@@ -254,6 +292,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __g
     }
   }
   if (clamp_count) atomicAdd(a.clamps, clamp_count);
+  __syncthreads();
+  double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
+  for (int i = threadIdx.x; i < D * nb; i += blockDim.x) dst[i] = s_hist[i];
 }
 
 }  // namespace pcb
