@@ -12,7 +12,7 @@ namespace pcb {
   const void* eval_kernel_fam##F(int d); \
   const void* points_kernel_fam##F(int d); \
   const void* invoke_kernel_fam##F(int d); \
-  const void* lanes_kernel_fam##F(int d, size_t* smem); \
+  const void* lanes_kernel_fam##F(int d, size_t* smem, int* threads); \
   const void* vsample_kernel_fam##F(int d, int rng);
 PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5, ) PCB_DECL(6, ) PCB_DECL(7, )
 #undef PCB_DECL
@@ -27,10 +27,10 @@ static const sample_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsamp
 
 static const kernel_getter kInvoke[PCB_N_FAMILIES] = {invoke_kernel_fam0, invoke_kernel_fam1, invoke_kernel_fam2, invoke_kernel_fam3,
                                                       invoke_kernel_fam4, invoke_kernel_fam5, invoke_kernel_fam6, invoke_kernel_fam7};
-typedef const void* (*lanes_getter)(int d, size_t* smem);
+typedef const void* (*lanes_getter)(int d, size_t* smem, int* threads);
 static const lanes_getter kLanes[PCB_N_FAMILIES] = {lanes_kernel_fam0, lanes_kernel_fam1, lanes_kernel_fam2, lanes_kernel_fam3,
                                                     lanes_kernel_fam4, lanes_kernel_fam5, lanes_kernel_fam6, lanes_kernel_fam7};
-const void* eval_lanes_kernel(int family, int d, size_t* smem) { return kLanes[family](d, smem); }
+const void* eval_lanes_kernel(int family, int d, size_t* smem, int* threads) { return kLanes[family](d, smem, threads); }
 const void* eval_kernel(int family, int d) { return kEval[family](d); }
 const void* points_kernel(int family, int d) { return kPoints[family](d); }
 const void* vsample_kernel_ptr(int family, int d, int rng) { return kSample[family](d, rng); }

@@ -42,8 +42,12 @@ struct LaneLayout {
   // stash: D doubles per lane (second differences at l2) during the point phase; while the tables are built the
   // same bytes hold the D centre factors phi[j][0]
   static constexpr int kDesc = 4 * (kPairs > 0 ? kPairs : 1);     // unsigned per CTA
+  // the two warps of a CTA share the tables of 32 regions and take virtual threads 0..31 and 32..63; the second
+  // warp hands over its five sums and the centre/axial evaluations with index >= 32 (split-axis inputs)
+  static constexpr int kLate = 4 * D + 1 > 32 ? 4 * D + 1 - 32 : 0;
+  static constexpr int kXfer = 5 + kLate;                         // doubles per lane
   static constexpr size_t smem_bytes(size_t vsize) {
-    return 32 * (kTab * vsize + (size_t)kTerm * 8 + D * vsize) + 6 * 8 * 8 + (size_t)kDesc * 4;
+    return 32 * (kTab * vsize + (size_t)(kTerm + (vsize > 8 ? kXfer : 0)) * 8 + D * vsize) + 6 * 8 * 8 + (size_t)kDesc * 4;
   }
 };
 
@@ -64,23 +68,31 @@ __device__ __forceinline__ void counter_merge(int blk, double (&cur)[5], double 
 }
 
 template <int FAM, int D>
-__global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
+__global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;
   using L = LaneLayout<D>;
+  // Complex factors (f1) double the tables, and one warp per 48 KB of tables cannot hide the FP64 latency: there two
+  // warps ("halves") share the tables of 32 regions and take virtual threads 0..31 and 32..63.  Real families run
+  // one warp per CTA with twice the chains per lane (measured faster: no duplicated prologue, no CTA barriers).
+  constexpr int kHalves = MF::cplx ? 2 : 1;
+  constexpr int kVt = 64 / kHalves;   // virtual threads per half
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31, half = threadIdx.x >> 5;   // half h takes virtual threads kVt*h .. kVt*h + kVt - 1
+  auto cta_sync = [&]() { if constexpr (kHalves > 1) __syncthreads(); else __syncwarp(); };
   V* tab = reinterpret_cast<V*>(smem_raw) + lane;                                                   // entry e: tab[e * 32]
   double* term = reinterpret_cast<double*>(smem_raw + sizeof(V) * 32 * L::kTab) + lane;             // term[(5j + c) * 32]
-  double* stash = term + 32 * L::kTerm;                                                             // stash[j * 32]
-  V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * L::kTerm) + lane;  // cen_s[j * 32], aliases stash
-  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * L::kTerm + sizeof(V) * D));   // [6][8]
+  constexpr int kXferD = kHalves > 1 ? L::kXfer : 0;
+  double* xfer = term + 32 * L::kTerm;                                                              // xfer[k * 32]: sums, late evaluations
+  double* stash = xfer + 32 * kXferD;                                                               // stash[j * 32]
+  V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * (L::kTerm + kXferD)) + lane;  // aliases stash
+  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * (L::kTerm + kXferD) + sizeof(V) * D));   // [6][8]
   unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                                          // [4 * kPairs]
 
   const pcb_rule& rule = args.rule;
   // pair point q = 4 * pair + signs -> entry indices of its three factors
-  for (int q = lane; q < 4 * L::kPairs; q += 32) {
+  for (int q = threadIdx.x; q < 4 * L::kPairs; q += 32 * kHalves) {
     const int e = q >> 2;
     int a = 0, b = 0, idx = 0;
     for (int j = 0; j < D; ++j)
@@ -88,13 +100,13 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
         if (idx == e) { a = j; b = k; }
     desc[q] = (unsigned)(L::kRab + e) | ((unsigned)(L::kP34 + 2 * a + (q & 1)) << 10) | ((unsigned)(L::kP34 + 2 * b + ((q >> 1) & 1)) << 20);
   }
-  if (lane < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
-    const int o = lane / 5, k = lane % 5;
+  if (threadIdx.x < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
+    const int o = threadIdx.x / 5, k = threadIdx.x % 5;
     double w = rule.weights[k][o < 5 ? o : 4];
     if (o == 5 && rule.corner_parity[k]) w = -w;
     s_w[o * 8 + k] = w;
   }
-  __syncwarp();
+  cta_sync();
 
   const double jac = args.f.bounded ? args.f.jac : 1.0;   // x * 1.0 == x
   const V one = mone(V{});
@@ -132,6 +144,7 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
     const long long rc = live ? r : args.n - 1;
 
     // ---- tables (loops over the axis are rolled: the kernel must stay inside the instruction cache)
+    // the halves share the work by corner group (three consecutive axes): even groups to half 0, odd to half 1
     double vol = 1.0;
     double next_left = args.lefts[rc], next_len = args.lengths[rc];
 #pragma unroll 1
@@ -142,6 +155,7 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
         next_len = args.lengths[(j + 1) * args.ld + rc];
       }
       vol = (j == 0) ? len : vol * len;   // np.prod, left to right
+      if (kHalves > 1 && ((j / 3) & 1) != half) continue;
       V cg[2];
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
@@ -172,7 +186,9 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
         }
       }
     }
-    // Rab[a][b] = (E[0][a] * E[a+1][b]) * E[b+1][D] with E[x][y] = ((1 * c_x) * c_{x+1}) ... * c_{y-1}
+    cta_sync();
+    // Rab[a][b] = (E[0][a] * E[a+1][b]) * E[b+1][D] with E[x][y] = ((1 * c_x) * c_{x+1}) ... * c_{y-1}; half h
+    // stores the pairs with a = h (mod 2)
     if constexpr (L::kPairs > 0) {
       V cen[D], tail[D];   // tail[b] = E[b+1][D]
 #pragma unroll
@@ -191,13 +207,16 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
         V mid = one;  // E[a+1][b]
 #pragma unroll
         for (int b = a + 1; b < D; ++b) {
-          tab[(L::kRab + e) * 32] = mmul(mmul(pre, mid), tail[b]);
-          mid = mmul(mid, cen[b]);
+          if (kHalves == 1 || (a & 1) == half) {
+            tab[(L::kRab + e) * 32] = mmul(mmul(pre, mid), tail[b]);
+            mid = mmul(mid, cen[b]);
+          }
           ++e;
         }
         pre = mmul(pre, cen[a]);
       }
     }
+    cta_sync();   // tables complete; the centre factors' bytes become the stash
 
     // ---- rule points.  Virtual threads are taken W at a time (vt = W blk + v).  For a fixed step s the W points
     //      vt + 64 s of a block almost always belong to one orbit class, so the block is straight-line code over W
@@ -205,12 +224,16 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
     //      the three blocks that straddle a class boundary take the point-by-point path.  The first log2(W)
     //      levels of the pair tree are fixed-register adds, the remaining ones a binary counter over the blocks.
     constexpr int W = MF::cplx ? 4 : 8;
-    constexpr int kCounterLevels = MF::cplx ? 4 : 3;   // log2(64 / W)
+    constexpr int kCounterLevels = 3;   // log2(kVt / W): 64 / 8 = 32 / 4
     double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
     int axis = 0;
     // split axis bookkeeping (pagani.py:215-223) for direct point i: running first maximum over the axes
     auto split_note = [&](int i, double fx) {
       if constexpr (D > 1) {
+        if (kHalves > 1 && half) {   // virtual threads 32..63: hand the evaluation to half 0, which keeps the running maximum
+          if constexpr (L::kLate > 0) xfer[(5 + i - 32) * 32] = fx;
+          return;
+        }
         const int q = i - 1;
         if (i == 0) two_f0 = 2.0 * fx;
         else if (!(q & 1)) first_of_pair = fx;
@@ -228,8 +251,8 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
     double hold[kCounterLevels][5];
     double cur[5];
 #pragma unroll 1
-    for (int blk = 0; blk < 64 / W; ++blk) {
-      const int vt0 = W * blk;
+    for (int blk = 0; blk < kVt / W; ++blk) {
+      const int vt0 = kVt * half + W * blk;
       double acc[W][5];
       V head[W];
 #pragma unroll
@@ -311,11 +334,27 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
       // remaining levels: binary counter over the blocks
       counter_merge<0, kCounterLevels>(blk, cur, hold);
     }
+    // top level of the pair tree: virtual threads 0..31 (half 0) + 32..63 (half 1)
+    if constexpr (kHalves > 1) {
+      if (half) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) xfer[k * 32] = cur[k];
+      }
+      __syncthreads();
+      if (!half) {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) cur[k] = cur[k] + xfer[k * 32];
+        if constexpr (L::kLate > 0 && D > 1) {
+#pragma unroll 1
+          for (int i = 32; i <= 4 * D; ++i) split_note(i, xfer[(5 + i - 32) * 32]);
+        }
+      }
+    }
 
     double v[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) v[k] = vol * cur[k];
-    if (live) {
+    if (live && !half) {
       if (!(isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]) && isfinite(v[3]) && isfinite(v[4]))) {
         // rare: find the first non-finite evaluation of this region (pagani.py:206-209)
         for (int i = 0; i < L::kFe; ++i) {
@@ -333,6 +372,7 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_kernel(const __grid_cons
       args.errors[r] = region_error(v, rule, args.err_mode, args.rel_floor);
       args.split_axes[r] = axis;
     }
+    cta_sync();   // the next batch's tables overwrite what half 0 has just read
   }
 }
 

@@ -59,10 +59,16 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   // (FP64-bound); short lists keep one warp per region (more parallelism per region).  The two agree bit for
   // bit (tests/test_gpu_pagani.py), so the choice never shows in the results.
   size_t lanes_smem = 0;
-  const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem) : nullptr;
+  int lanes_threads = 32;
+  const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem, &lanes_threads) : nullptr;
   long long lanes_min = 8192;
-  if (const char* env = std::getenv("PCB_PAGANI_LANES_MIN")) lanes_min = std::atoll(env);
-  if (lanes_fn && lanes_smem <= ctx->smem_optin && n >= lanes_min) {
+  size_t lanes_cap = 56u << 10;
+  if (const char* env = std::getenv("PCB_PAGANI_LANES_MIN")) {  // test hook: force either kernel
+    lanes_min = std::atoll(env);
+    lanes_cap = ctx->smem_optin;
+  }
+  // below ~4 resident warps per SM (52 KB of tables per warp) the lane kernel no longer hides its latency
+  if (lanes_fn && lanes_smem <= lanes_cap && n >= lanes_min) {
     size_t& have = ctx->smem_attr[lanes_fn];
     if (have < lanes_smem) {
       PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(lanes_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lanes_smem));
@@ -72,7 +78,7 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
     if (per_sm < 1) per_sm = 1;
     const long long want = (n + 31) / 32;
     ProfileSpan span(ctx, 0, (double)n);
-    PCB_CUDA_TRY(ctx, launch(ctx, lanes_fn, dim3((unsigned)std::min<long long>(want, (long long)per_sm * ctx->sm_count)), dim3(32), lanes_smem, a));
+    PCB_CUDA_TRY(ctx, launch(ctx, lanes_fn, dim3((unsigned)std::min<long long>(want, (long long)per_sm * ctx->sm_count)), dim3(lanes_threads), lanes_smem, a));
     return PCB_OK;
   }
   const void* fn = eval_kernel(f->family, f->d);

@@ -32,9 +32,10 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
 
 // one-region-per-lane kernel (multiplicative or generic form) and its dynamic shared memory
 template <int D>
-static const void* lanes_kernel_for(size_t* smem) {
+static const void* lanes_kernel_for(size_t* smem, int* threads) {
   if constexpr (MultFamily<PCB_FAM>::enabled) {
     *smem = LaneLayout<D>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
+    *threads = MultFamily<PCB_FAM>::cplx ? 64 : 32;   // complex factors: two warps share the tables of 32 regions
     return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
   } else if constexpr (PCB_FAM == PCB_F3_CORNER_PEAK) {
     // the double-double power dominates f3 and the warp-per-region kernel hides its latency better (measured:
@@ -43,13 +44,14 @@ static const void* lanes_kernel_for(size_t* smem) {
     return nullptr;
   } else {
     *smem = GenericLaneLayout<D>::smem_bytes();
+    *threads = 32;
     return (const void*)&pagani_eval_lanes_generic_kernel<PCB_FAM, D>;
   }
 }
 
-const void* PCB_CAT(lanes_kernel_fam, PCB_FAM)(int d, size_t* smem) {
+const void* PCB_CAT(lanes_kernel_fam, PCB_FAM)(int d, size_t* smem, int* threads) {
   switch (d) {
-#define X(D) case D: return lanes_kernel_for<D>(smem);
+#define X(D) case D: return lanes_kernel_for<D>(smem, threads);
     PCB_DIMS(X)
 #undef X
   }
