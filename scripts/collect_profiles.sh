@@ -19,14 +19,17 @@ cap() {  # name kernel-regex skip units unit-name -- target args
     python scripts/ncu_summary.py gpurun_out/${R}_$name.ncu-rep $units $uname; } > profiles/${R}_ncu_$name.txt 2>/dev/null
 }
 cap vsample_config2 vsample 2 32768 warp-sample vsample f2 6 1e6
-cap bin_config2 bin_kernel 2 32768 record-group vsample f2 6 1e6
 cap reduce_config2 reduce_kernel 2 1 launch vsample f2 6 1e6
 cap finish_config2 finish_kernel 2 1 launch vsample f2 6 1e6
 cap vsample_config4 vsample 1 26873856 warp-sample vsample f3 8 1e9
-cap bin_config4 bin_kernel 1 26873856 record-group vsample f3 8 1e9
 cap pagani_lanes_f1_d8 pagani_eval 2 390625 region eval f1 8 5
 cap pagani_lanes_f4_d8 pagani_eval 2 390625 region eval f4 8 5
 cap pagani_lanes_f2_d8 pagani_eval 2 390625 region eval f2 8 5
 cap pagani_warp_f3_d8 pagani_eval 2 390625 region eval f3 8 5
 cap pagani_warp_f4_d5_small pagani_eval 2 1024 region eval f4 5 4
+cap pagani_warp_f1_d8_small pagani_eval 2 6561 region eval f1 8 3
+# the final bench lines (own arm with the secondary workloads, reference arm) and the config-5 sweep
+python bench.py > profiles/${R}_bench_config2.json 2> gpurun_out/bench_final.err
+python bench.py --impl reference > profiles/${R}_bench_config2_reference.json 2>> gpurun_out/bench_final.err
+python scripts/sweep.py --out profiles/${R}_sweep_config5 > gpurun_out/sweep.log 2>&1
 ls -la profiles/
