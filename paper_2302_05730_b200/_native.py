@@ -375,7 +375,7 @@ def pagani_refine(spec: DeviceSpec, orbit, cfg, progress=None, device=None):
         except BaseException as exc:  # noqa: BLE001 - re-raised after the native call returns
             failure.append(exc)
 
-    cb = PAGANI_PROGRESS_FN(_cb)
+    cb = PAGANI_PROGRESS_FN(_cb) if progress is not None else C.cast(None, PAGANI_PROGRESS_FN)
     with ctx.call_lock:
         st = ctx.lib.pcb_pagani_refine(ctx.handle, C.byref(fc), C.byref(rc), C.byref(cc), C.byref(res), records, cb, None,
                                        C.byref(bad))
@@ -454,7 +454,8 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
         except BaseException as exc:  # noqa: BLE001
             failure.append(exc)
 
-    cb = MCUBES_PROGRESS_FN(_cb)
+    # no Python trampoline per iteration unless somebody listens (each call back into Python costs ~10 us)
+    cb = MCUBES_PROGRESS_FN(_cb) if progress is not None else C.cast(None, MCUBES_PROGRESS_FN)
     with ctx.call_lock:
         st = ctx.lib.pcb_mcubes_run(ctx.handle, C.byref(fc), C.byref(pc), int(iterations), C.c_uint64(seed & (2**64 - 1)),
                                     rng_kind, int(bool(adapt)), float(alpha), int(bool(smoothing)), float(rel_tol), its,

@@ -101,6 +101,7 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
+  if (ctx->pg_record) cudaFreeHost(ctx->pg_record);
   for (auto ev : ctx->mc_events) cudaEventDestroy(ev);
   for (int k = 0; k < 3; ++k)
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);

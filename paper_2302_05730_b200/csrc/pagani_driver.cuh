@@ -230,4 +230,164 @@ __global__ void widen_axes_kernel(long long n, const int32_t* __restrict__ in, l
     out[r] = in[r];
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// One refinement iteration of a SHORT list (n <= 1024 regions) in one CTA: global sums, stop tests, threshold
+// classification (with the forced-progress fallback), stable compaction + bisection and the retired sums
+// (pagani.py:336-378) -- the work of ten launches and two host round trips of the general path.  The arithmetic
+// is the general path's: 1024-leaf adjacent-pair trees (= engine.tree_sum with zero padding), serial volume
+// products, the same comparisons.  The host passes the running totals in and reads one record back from pinned
+// memory; `bad` is the evaluate kernel's non-finite flag, re-armed here for the next evaluation.
+// ------------------------------------------------------------------------------------------------------------
+struct ShortIterRecord {       // pinned host memory
+  double estimate, errorest;   // of this iteration (pagani.py:336-337)
+  double fin_i, fin_e;         // finished totals after this iteration's retirements
+  long long n_split;           // regions bisected (children = 2 * n_split)
+  unsigned long long bad;      // first non-finite evaluation (region * f_eval + point) or ~0
+  int action;                  // 0: continue with the children   1: tolerance met   2: max iterations   3: region cap
+  int pad;
+  volatile unsigned long long seq;
+};
+
+struct ShortIterArgs {
+  int n, d;
+  long long ld_in, ld_out_unused;
+  const double* lefts;         // [d][ld_in]
+  const double* lengths;
+  const double* integrals;
+  const double* errors;
+  const int32_t* axes;
+  double* out_lefts;           // [d][ld_out], ld_out = round_up(2 * n_split, 32), capacity for n_split = n
+  double* out_lengths;
+  double fin_i, fin_e;
+  long long processed, region_cap;
+  double rel_tol;
+  int iteration, max_iterations;
+  unsigned long long* bad;     // device flag of the evaluate kernel
+  ShortIterRecord* record;
+  unsigned long long seq;
+};
+
+// adjacent-pair tree over 1024 values, one per thread (zeros beyond the data); every thread gets the sum
+__device__ __forceinline__ double tree1024(double v, double* s_warp /* [32] */) {
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) v = v + __shfl_xor_sync(PCB_FULL_MASK, v, m);
+  __syncthreads();   // s_warp may still be read from a previous call
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = s_warp[threadIdx.x & 31];
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) t = t + __shfl_xor_sync(PCB_FULL_MASK, t, m);
+  return t;
+}
+
+__global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_constant__ ShortIterArgs a) {
+  __shared__ double s_warp[32];
+  __shared__ unsigned int s_cnt[32];
+  __shared__ double s_ret_i[1024], s_ret_e[1024];
+  __shared__ double s_emax;
+  const int r = threadIdx.x, lane = r & 31, w = r >> 5;
+  const bool have = r < a.n;
+  const double my_i = have ? a.integrals[r] : 0.0, my_e = have ? a.errors[r] : 0.0;
+  const double sum_i = tree1024(my_i, s_warp);
+  const double sum_e = tree1024(my_e, s_warp);
+  const double estimate = a.fin_i + sum_i, errorest = a.fin_e + sum_e;
+  const unsigned long long bad = *a.bad;
+  int action = 0;
+  if (bad != ~0ULL) action = 4;   // the host raises; nothing else matters
+  else if (errorest <= a.rel_tol * fabs(estimate)) action = 1;
+  else if (a.iteration == a.max_iterations) action = 2;
+  long long n_split = 0;
+  double fin_i = a.fin_i, fin_e = a.fin_e;
+  if (action == 0) {
+    // classification (pagani.py:361-365)
+    const double budget = 0.8 * a.rel_tol * fabs(estimate);
+    bool split = false;
+    if (have) {
+      double vol = a.lengths[r];
+      for (int j = 1; j < a.d; ++j) vol = vol * a.lengths[j * a.ld_in + r];  // np.prod, left to right
+      split = my_e > budget * vol;
+    }
+    unsigned total = __syncthreads_count(split);
+    if (total == 0) {  // nothing exceeds its budget: force progress on the worst regions, ties included
+      double m = have ? my_e : -1.0;
+#pragma unroll
+      for (int k = 16; k >= 1; k >>= 1) m = fmax(m, __shfl_xor_sync(PCB_FULL_MASK, m, k));
+      if (lane == 0) s_warp[w] = m;
+      __syncthreads();
+      if (w == 0) {
+        double t = s_warp[lane];
+#pragma unroll
+        for (int k = 16; k >= 1; k >>= 1) t = fmax(t, __shfl_xor_sync(PCB_FULL_MASK, t, k));
+        if (lane == 0) s_emax = fmax(t, 0.0);
+      }
+      __syncthreads();
+      split = have && my_e >= s_emax;
+      total = __syncthreads_count(split);
+    }
+    n_split = total;
+    if (a.processed + 2 * n_split > a.region_cap) {
+      action = 3;
+    } else {
+      // stable ranks: exclusive scan of the split flags
+      const unsigned ballot = __ballot_sync(PCB_FULL_MASK, split);
+      if (lane == 0) s_cnt[w] = __popc(ballot);
+      __syncthreads();
+      if (w == 0) {
+        unsigned c = s_cnt[lane], z = c;
+#pragma unroll
+        for (int m = 1; m < 32; m <<= 1) {
+          unsigned y = __shfl_up_sync(PCB_FULL_MASK, z, m);
+          if (lane >= m) z += y;
+        }
+        s_cnt[lane] = z - c;
+      }
+      s_ret_i[r] = 0.0;
+      s_ret_e[r] = 0.0;
+      __syncthreads();
+      const unsigned rank = s_cnt[w] + __popc(ballot & ((1u << lane) - 1u));
+      const long long ld_out = (2 * n_split + 31) / 32 * 32;
+      if (have) {
+        if (split) {
+          const int axis = a.axes[r];
+          const unsigned c = 2u * rank;
+          for (int j = 0; j < a.d; ++j) {
+            const double left = a.lefts[j * a.ld_in + r];
+            double len = a.lengths[j * a.ld_in + r];
+            double upper = left;
+            if (j == axis) {
+              len = len * 0.5;        // half = length * 0.5
+              upper = left + len;     // hi_left = left + half
+            }
+            *reinterpret_cast<double2*>(a.out_lefts + j * ld_out + c) = make_double2(left, upper);
+            *reinterpret_cast<double2*>(a.out_lengths + j * ld_out + c) = make_double2(len, len);
+          }
+        } else {
+          const unsigned k = (unsigned)r - rank;   // parent order among the retired
+          s_ret_i[k] = my_i;
+          s_ret_e[k] = my_e;
+        }
+      }
+      __syncthreads();
+      // fin += tree_sum(act[~mask]) (pagani.py:371-372)
+      const double ret_i = tree1024(s_ret_i[r], s_warp);
+      const double ret_e = tree1024(s_ret_e[r], s_warp);
+      fin_i = a.fin_i + ret_i;
+      fin_e = a.fin_e + ret_e;
+    }
+  }
+  if (r == 0) {
+    *a.bad = ~0ULL;   // re-arm for the next evaluation
+    ShortIterRecord* rec = a.record;
+    rec->estimate = estimate;
+    rec->errorest = errorest;
+    rec->fin_i = fin_i;
+    rec->fin_e = fin_e;
+    rec->n_split = n_split;
+    rec->bad = bad;
+    rec->action = action;
+    __threadfence_system();
+    rec->seq = a.seq;
+  }
+}
+
 }  // namespace pcb

@@ -307,7 +307,83 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   int n_rec = 0, reason = PCB_STOP_MAX_ITER;
   bool converged = false, have_retired = false;
 
+  // short lists (<= 1024 regions) run the whole iteration in one CTA and hand one record back through pinned memory
+  bool use_short = true;
+  if (const char* env = std::getenv("PCB_PAGANI_SHORT")) use_short = std::atoi(env) != 0;
+  if (use_short && !ctx->pg_record) {
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 128));
+    std::memset(ctx->pg_record, 0, 128);
+  }
+  ShortIterRecord* srec = static_cast<ShortIterRecord*>(ctx->pg_record);
+
   for (int it = 0; it <= cfg->max_iterations; ++it) {
+    if (use_short && n >= 1 && n <= 1024) {
+      if (have_retired) {  // fold the general path's pending retirements first
+        PCB_TRY(read_scalars(ctx, 0, 8));
+        fin_i += host[S_RET_I];
+        fin_e += host[S_RET_E];
+        have_retired = false;
+      }
+      const int nxt = cur ^ 1;
+      const long long ld_cap = round_up(2 * n, 32);
+      PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_cap * d * sizeof(double)));
+      PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_cap * d * sizeof(double)));
+      ShortIterArgs sa;
+      sa.n = (int)n; sa.d = d; sa.ld_in = ld; sa.ld_out_unused = 0;
+      sa.lefts = ctx->lefts[cur].as<double>();
+      sa.lengths = ctx->lengths[cur].as<double>();
+      sa.integrals = ctx->est_i.as<double>();
+      sa.errors = ctx->est_e.as<double>();
+      sa.axes = ctx->est_k.as<int32_t>();
+      sa.out_lefts = ctx->lefts[nxt].as<double>();
+      sa.out_lengths = ctx->lengths[nxt].as<double>();
+      sa.fin_i = fin_i; sa.fin_e = fin_e;
+      sa.processed = processed; sa.region_cap = cfg->region_cap;
+      sa.rel_tol = cfg->rel_tol;
+      sa.iteration = it; sa.max_iterations = cfg->max_iterations;
+      sa.bad = sc_u + S_BAD;
+      sa.record = srec;
+      sa.seq = ++ctx->pg_seq;
+      short_iteration_kernel<<<1, 1024, 0, ctx->stream>>>(sa);
+      ctx->launches++;
+      PCB_CUDA_TRY(ctx, cudaGetLastError());
+      for (unsigned spin = 0; srec->seq != sa.seq; ++spin) {
+        if ((spin & 0xfff) == 0xfff) {
+          cudaError_t e = cudaStreamQuery(ctx->stream);
+          if (e != cudaErrorNotReady && srec->seq != sa.seq) {
+            (void)cudaGetLastError();
+            return fail(ctx, PCB_CUDA, "pagani_refine: short iteration did not publish its record (%s)", cudaGetErrorString(e));
+          }
+        }
+      }
+      if (srec->action == 4)
+        return fetch_nonfinite_pagani(ctx, f, rule, ld, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(), srec->bad, bad);
+      estimate = srec->estimate;
+      errorest = srec->errorest;
+      pcb_pagani_progress rec;
+      rec.iteration = it;
+      rec.reserved = 0;
+      rec.n_regions = fin_count + n;
+      rec.active = n;
+      rec.estimate = estimate;
+      rec.errorest = errorest;
+      if (records) records[n_rec] = rec;
+      ++n_rec;
+      if (progress) progress(user, &rec);
+      if (srec->action == 1) { converged = true; reason = PCB_STOP_TOLERANCE; break; }
+      if (srec->action == 2) { reason = PCB_STOP_MAX_ITER; break; }
+      if (srec->action == 3) { reason = PCB_STOP_REGION_CAP; break; }
+      const long long n_split = srec->n_split;
+      fin_i = srec->fin_i;
+      fin_e = srec->fin_e;
+      fin_count += n - n_split;
+      processed += 2 * n_split;
+      n = 2 * n_split;
+      ld = round_up(n, 32);
+      cur = nxt;
+      PCB_TRY(evaluate(n, ld));
+      continue;
+    }
     PCB_TRY(tree_sum_dev(ctx, ctx->est_i.as<double>(), n, sc + S_SUM_I));
     PCB_TRY(tree_sum_dev(ctx, ctx->est_e.as<double>(), n, sc + S_SUM_E));
     PCB_TRY(read_scalars(ctx, 0, 8));

@@ -58,6 +58,8 @@ struct pcb_ctx {
   long long launches = 0;
   char name[256] = {0};
   void* pinned = nullptr;  // 64 KiB staging for small device->host reads
+  void* pg_record = nullptr;          // pinned record of the short-list PAGANI iteration kernel
+  unsigned long long pg_seq = 0;
   // scratch device buffers, grown on demand and reused across calls
   pcb::DevBuf lefts[2], lengths[2], est_i, est_e, est_k, flags, counts, offsets, ret_i, ret_e, tree[2], scalars;
   pcb::DevBuf rows_a, rows_b, k64;

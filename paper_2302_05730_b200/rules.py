@@ -197,9 +197,23 @@ def _null_rows(d: int, orb: np.ndarray, table: dict, w7: np.ndarray, w5: np.ndar
     return [n1, n2, n3, n4], (5, 3, 1, 0), (1.0, SAFEGUARD_SCALE, SAFEGUARD_SCALE, SAFEGUARD_SCALE)
 
 
+_RULE_CACHE: dict = {}
+
+
 def build_rule(d: int) -> RuleTable:
-    """Rule table for dimension d (reference: quadrature.py:260-289)."""
+    """Rule table for dimension d (reference: quadrature.py:260-289).
+
+    The table is immutable (read-only arrays), so one instance per dimension is shared: the
+    moment solve and the SVD cost ~0.4 ms, more than a whole refine() of a short list on the device.
+    """
     d = check_dimension(d)
+    hit = _RULE_CACHE.get(d)
+    if hit is None:
+        hit = _RULE_CACHE[d] = _build_rule(d)
+    return hit
+
+
+def _build_rule(d: int) -> RuleTable:
     gen, orb = _point_set(d)
     table = _moment_table(d)
     w7, w5 = _degree7_and_5(d, table)
@@ -225,12 +239,27 @@ class OrbitRule(_Frozen):
                  "high_mask", "null_scales")
 
 
+_ORBIT_CACHE: dict = {}
+
+
 def orbit_form(rule: RuleTable) -> OrbitRule:
     """Compress a RuleTable, verifying it has the canonical fully symmetric layout.
 
     Raises ValueError for tables whose points or weights are not orbit-structured
     (the device kernels derive abscissae and weights from the point index).
+    Verified forms are remembered per table object (tables are immutable).
     """
+    hit = _ORBIT_CACHE.get(id(rule))
+    if hit is not None and hit[0] is rule:
+        return hit[1]
+    out = _orbit_form(rule)
+    if len(_ORBIT_CACHE) > 64:
+        _ORBIT_CACHE.clear()
+    _ORBIT_CACHE[id(rule)] = (rule, out)   # the strong reference keeps id(rule) from being reused
+    return out
+
+
+def _orbit_form(rule: RuleTable) -> OrbitRule:
     d = rule.d
     gen_ref, orb = _point_set(d)
     if rule.f_eval != gen_ref.shape[0] or rule.generators.shape != gen_ref.shape:

@@ -332,3 +332,22 @@ def test_lane_kernel_reports_first_nonfinite(monkeypatch):
         cause = exc.value.cause
         errs.append((cause.region_index, tuple(np.asarray(cause.point).tolist())))
     assert errs[0] == errs[1]
+
+
+@pytest.mark.parametrize("fam,d,tol,kw", [
+    ("f4", 5, 1e-3, {}), ("f2", 5, 1e-3, {}), ("sum", 3, 1e-9, {}), ("f5", 2, 1e-6, {}), ("f1", 3, 1e-8, {}),
+    ("f3", 4, 1e-5, {}), ("f6", 3, 1e-4, {"max_iterations": 7}), ("f2", 4, 1e-6, {"region_cap": 3000}),
+    ("f4", 6, 1e-3, {"max_iterations": 12}),
+])
+def test_short_list_iteration_kernel_equals_general_path(fam, d, tol, kw, monkeypatch):
+    """Lists of <= 1024 regions run a whole refinement iteration in one CTA (short_iteration_kernel); the
+    history must be the general path's, bit for bit, through every transition between the two."""
+    f = pb.get_integrand(fam, d)
+    cfg = pb.PaganiConfig(rel_tol=tol, **kw)
+    monkeypatch.setenv("PCB_PAGANI_SHORT", "1")
+    a = pb.refine(f, cfg)
+    monkeypatch.setenv("PCB_PAGANI_SHORT", "0")
+    b = pb.refine(f, cfg)
+    assert a.history == b.history
+    assert (a.estimate, a.errorest, a.iterations, a.regions_processed, a.converged, a.reason) == \
+           (b.estimate, b.errorest, b.iterations, b.regions_processed, b.converged, b.reason)
