@@ -170,7 +170,12 @@ __device__ inline double np_pairwise_sum_warp(const double* a, int n) {
   if (n <= 128) {
     const int k = lane & 7, body = n - (n % 8);
     double r = a[k];
-    for (int i = 8; i < body; i += 8) r = r + a[i + k];
+    int i = 8;
+    for (; i + 24 < body; i += 32) {   // loads batched: only the DADD chain is exposed
+      const double v0 = a[i + k], v1 = a[i + 8 + k], v2 = a[i + 16 + k], v3 = a[i + 24 + k];
+      r = r + v0; r = r + v1; r = r + v2; r = r + v3;
+    }
+    for (; i < body; i += 8) r = r + a[i + k];
     r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 1);
     r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 2);
     r = r + __shfl_xor_sync(PCB_FULL_MASK, r, 4);
@@ -232,29 +237,41 @@ __device__ __forceinline__ void refine_axis_cta(const RefineArgs& a, int j, doub
   for (int i = tid; i < n; i += blockDim.x) {
     const double r = c[i] / total;
     double ww = 0.0;
-    if (r > 0.0 && r < 1.0) ww = pow((1.0 - r) / log(1.0 / r), a.alpha);
+    if (r > 0.0 && r < 1.0) {
+      const double base = (1.0 - r) / log(1.0 / r);
+      // the default damping exponent 3/2 as x * sqrt(x) (both correctly rounded operations; pow() is ~10x the
+      // instructions and itself only accurate to 1-2 ulp); any other exponent goes through pow
+      ww = a.alpha == 1.5 ? base * sqrt(base) : pow(base, a.alpha);
+    }
     else if (r >= 1.0) ww = 1.0;
     w[i] = ww;
   }
   __syncthreads();
   if (tid < 32) {
     const double wsum = np_pairwise_sum_warp(w, n);
-    if (tid == 0) {
-      s_scal[1] = wsum;
-      double run = w[0];
-      cw[0] = 0.0;
-      cw[1] = run;
-      int i = 1;
-      for (; i + 8 <= n; i += 8) {  // np.cumsum: serial adds, loads batched so only the DADD chain is exposed
-        double v[8];
+    if (tid == 0) s_scal[1] = wsum;
+    // np.cumsum as a warp scan: lane l owns a run of consecutive bins (serial prefix inside the run, shuffle scan
+    // across the runs).  The association differs from numpy's serial chain by rounding only (~1e-16 relative,
+    // the boundaries are compared to 1e-12: log/sqrt are not numpy's either); a 500-long dependent DADD chain
+    // would be a quarter of this kernel.
+    const int per = (n + 31) / 32, i0 = tid * per, i1 = min(n, i0 + per);
+    double run = 0.0;
+    for (int i = i0; i < i1; ++i) run = (i == i0) ? w[i] : run + w[i];
+    double incl = run;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = w[i + k];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) { run = run + v[k]; cw[i + k + 1] = run; }
-      }
-      for (; i < n; ++i) { run = run + w[i]; cw[i + 1] = run; }
-      cw[n] = wsum;
+    for (int m = 1; m < 32; m <<= 1) {
+      const double y = __shfl_up_sync(PCB_FULL_MASK, incl, m);
+      if (tid >= m) incl = y + incl;
     }
+    double acc = __shfl_up_sync(PCB_FULL_MASK, incl, 1);   // sum of the runs before mine
+    if (tid == 0) acc = 0.0;
+    for (int i = i0; i < i1; ++i) {
+      acc = acc + w[i];
+      cw[i + 1] = acc;
+    }
+    if (tid == 0) cw[0] = 0.0;
+    __syncwarp();
+    if (tid == 0) cw[n] = wsum;
   }
   __syncthreads();
   const double wsum = s_scal[1];

@@ -67,8 +67,20 @@ __device__ __forceinline__ void counter_merge(int blk, double (&cur)[5], double 
   }
 }
 
+// CTAs per SM the register allocation must leave room for: what the tables allow (227 KB of shared memory per SM),
+// capped -- beyond ~10 resident warps the spills cost more than the occupancy brings
 template <int FAM, int D>
-__global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
+constexpr int lanes_min_blocks() {
+  constexpr bool cplx = MultFamily<FAM>::cplx;
+  constexpr size_t smem = LaneLayout<D>::smem_bytes(cplx ? 16 : 8) + 1024;
+  constexpr int by_smem = (int)((227u << 10) / smem);
+  constexpr int cap = cplx ? 6 : 10;
+  return by_smem < 1 ? 1 : (by_smem < cap ? by_smem : cap);
+}
+
+template <int FAM, int D>
+__global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32, lanes_min_blocks<FAM, D>())
+pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;
@@ -144,7 +156,8 @@ __global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_l
     const long long rc = live ? r : args.n - 1;
 
     // ---- tables (loops over the axis are rolled: the kernel must stay inside the instruction cache)
-    // the halves share the work by corner group (three consecutive axes): even groups to half 0, odd to half 1
+    // with two halves, half 0 evaluates the centre and pair factors (c = 0, 3, 4) and the generic terms, half 1 the
+    // corner factors (c = 5, 6) and the corner group tables: three and two transcendentals per axis
     double vol = 1.0;
     double next_left = args.lefts[rc], next_len = args.lengths[rc];
 #pragma unroll 1
@@ -155,10 +168,10 @@ __global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_l
         next_len = args.lengths[(j + 1) * args.ld + rc];
       }
       vol = (j == 0) ? len : vol * len;   // np.prod, left to right
-      if (kHalves > 1 && ((j / 3) & 1) != half) continue;
       V cg[2];
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
+        if (kHalves > 1 && (c >= 5) != (half == 1)) continue;
         double x = left + len * rule.offsets[c];   // quadrature.py:301-302: mul, then add
         if (args.f.bounded) x = args.f.low[j] + args.f.width[j] * x;
         if (c < 5) term[(5 * j + c) * 32] = F::term(j, x, args.f);
@@ -168,6 +181,7 @@ __global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_l
         else if (c < 5) tab[(L::kP34 + 2 * j + (c - 3)) * 32] = v;
         else cg[c - 5] = v;
       }
+      if (kHalves > 1 && half == 0) continue;
       // corner group tables: Grp[g][combo] = phi[3g][.] * phi[3g+1][.] * phi[3g+2][.], left to right
       const int g = j / 3, pos = j - 3 * g;
       V* grp = tab + (L::kGrp + 8 * g) * 32;
@@ -175,13 +189,13 @@ __global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32) pagani_eval_l
         grp[0] = cg[0];
         grp[32] = cg[1];
       } else {
-        const int half = 1 << pos;
+        const int half_n = 1 << pos;
 #pragma unroll
         for (int combo = 0; combo < 4; ++combo) {
-          if (combo < half) {
+          if (combo < half_n) {
             const V lo = grp[combo * 32];
             grp[combo * 32] = mmul(lo, cg[0]);
-            grp[(combo + half) * 32] = mmul(lo, cg[1]);
+            grp[(combo + half_n) * 32] = mmul(lo, cg[1]);
           }
         }
       }
