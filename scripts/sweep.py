@@ -24,6 +24,12 @@ for fam in fams:
     for d in dims:
         f = pb.get_integrand(fam, d)
         truth = pb.reference_value(fam, d).value
+        # warm-up: the first launch of a kernel pays CUDA's lazy module loading (tens of ms for the large evaluate
+        # kernels); it is not part of a time-to-epsrel
+        spec, orbit = f.device_spec(), pb.rules.orbit_form(pb.build_rule(d))
+        _native.pagani_refine(spec, orbit, pb.PaganiConfig(rel_tol=1e-2 if fam != "f1" else 1e-5, max_iterations=12))
+        _native.mcubes_run(spec, pb.make_plan(10**8, d), 500, 1, 0, _native.RNG_REFERENCE_HASH, True, 1.5, True, 0.0,
+                           keep_contributions=False)
         for tol in tols:
             spec, orbit = f.device_spec(), pb.rules.orbit_form(pb.build_rule(d))
             res, hist = _native.pagani_refine(spec, orbit, pb.PaganiConfig(rel_tol=tol))
