@@ -27,7 +27,7 @@
 
 namespace pcb {
 
-template <int D>
+template <int D, bool UNIT = false>
 struct LaneLayout {
   static constexpr int kFe = (1 << D) + 2 * D * D + 2 * D + 1;
   static constexpr int kCorner0 = 2 * D * D + 2 * D + 1;
@@ -35,8 +35,8 @@ struct LaneLayout {
   static constexpr int kGroups = (D + 2) / 3;
   static constexpr int kSteps = (kFe + 63) / 64;
   static constexpr int kP34 = 0;                                  // phi[j][3], phi[j][4] at 2j, 2j+1
-  static constexpr int kRab = 2 * D;
-  static constexpr int kGrp = kRab + (kPairs > 0 ? kPairs : 1);  // Grp[g][combo] at kGrp + 8g + combo
+  static constexpr int kRab = 2 * D;                              // unit-modulus families keep no Rab table (rho form)
+  static constexpr int kGrp = kRab + (UNIT ? 0 : (kPairs > 0 ? kPairs : 1));  // Grp[g][combo] at kGrp + 8g + combo
   static constexpr int kTab = kGrp + 8 * kGroups;                 // V entries per lane
   static constexpr int kTerm = 5 * D;                             // doubles per lane: term[j][c], c = 0..4
   // stash: D doubles per lane (second differences at l2) during the point phase; while the tables are built the
@@ -46,8 +46,14 @@ struct LaneLayout {
   // warp hands over its five sums and the centre/axial evaluations with index >= 32 (split-axis inputs)
   static constexpr int kLate = 4 * D + 1 > 32 ? 4 * D + 1 - 32 : 0;
   static constexpr int kXfer = 5 + kLate;                         // doubles per lane
+  // scratch per lane: the D centre factors while the tables are built, afterwards the split-axis stash (D doubles)
+  // and, with two halves, the hand-over slots
+  __host__ __device__ static constexpr size_t scratch_doubles(size_t vsize) {
+    const size_t a = D * vsize / 8, b = D + (vsize > 8 ? kXfer : 0);
+    return a > b ? a : b;
+  }
   static constexpr size_t smem_bytes(size_t vsize) {
-    return 32 * (kTab * vsize + (size_t)(kTerm + (vsize > 8 ? kXfer : 0)) * 8 + D * vsize) + 6 * 8 * 8 + (size_t)kDesc * 4;
+    return 32 * (kTab * vsize + (size_t)kTerm * 8 + scratch_doubles(vsize) * 8) + 6 * 8 * 8 + (size_t)kDesc * 4;
   }
 };
 
@@ -72,7 +78,7 @@ __device__ __forceinline__ void counter_merge(int blk, double (&cur)[5], double 
 template <int FAM, int D>
 constexpr int lanes_min_blocks() {
   constexpr bool cplx = MultFamily<FAM>::cplx;
-  constexpr size_t smem = LaneLayout<D>::smem_bytes(cplx ? 16 : 8) + 1024;
+  constexpr size_t smem = LaneLayout<D, MultFamily<FAM>::unit>::smem_bytes(cplx ? 16 : 8) + 1024;
   constexpr int by_smem = (int)((227u << 10) / smem);
   constexpr int cap = cplx ? 6 : 10;
   return by_smem < 1 ? 1 : (by_smem < cap ? by_smem : cap);
@@ -84,7 +90,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;
-  using L = LaneLayout<D>;
+  using L = LaneLayout<D, MF::unit>;
   // Complex factors (f1) double the tables, and one warp per 48 KB of tables cannot hide the FP64 latency: there two
   // warps ("halves") share the tables of 32 regions and take virtual threads 0..31 and 32..63.  Real families run
   // one warp per CTA with twice the chains per lane (measured faster: no duplicated prologue, no CTA barriers).
@@ -95,11 +101,12 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   auto cta_sync = [&]() { if constexpr (kHalves > 1) __syncthreads(); else __syncwarp(); };
   V* tab = reinterpret_cast<V*>(smem_raw) + lane;                                                   // entry e: tab[e * 32]
   double* term = reinterpret_cast<double*>(smem_raw + sizeof(V) * 32 * L::kTab) + lane;             // term[(5j + c) * 32]
-  constexpr int kXferD = kHalves > 1 ? L::kXfer : 0;
-  double* xfer = term + 32 * L::kTerm;                                                              // xfer[k * 32]: sums, late evaluations
-  double* stash = xfer + 32 * kXferD;                                                               // stash[j * 32]
-  V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * (L::kTerm + kXferD)) + lane;  // aliases stash
-  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * (L::kTerm + kXferD) + sizeof(V) * D));   // [6][8]
+  constexpr size_t kScratchD = L::scratch_doubles(sizeof(V));
+  double* scratch = term + 32 * L::kTerm;
+  V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * L::kTerm) + lane;   // cen_s[j * 32] (table phase)
+  double* stash = scratch;                                                                          // stash[j * 32] (point phase)
+  double* xfer = scratch + 32 * D;                                                                  // xfer[k * 32]: sums, late evaluations
+  double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * L::kTerm + 8 * kScratchD));   // [6][8]
   unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                                          // [4 * kPairs]
 
   const pcb_rule& rule = args.rule;
@@ -111,6 +118,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
       for (int k = j + 1; k < D; ++k, ++idx)
         if (idx == e) { a = j; b = k; }
     desc[q] = (unsigned)(L::kRab + e) | ((unsigned)(L::kP34 + 2 * a + (q & 1)) << 10) | ((unsigned)(L::kP34 + 2 * b + ((q >> 1) & 1)) << 20);
+    (void)e;
   }
   if (threadIdx.x < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
     const int o = threadIdx.x / 5, k = threadIdx.x % 5;
@@ -124,9 +132,11 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   const V one = mone(V{});
 
   // value of pair / corner points from the lane's tables
+  V full = one;   // unit-modulus families: product of the centre factors of the current region
   auto pair_value = [&](int i) -> double {
     const unsigned dsc = desc[i - 1 - 4 * D];
-    const V v = mmul(mmul(tab[(dsc & 1023u) * 32], tab[((dsc >> 10) & 1023u) * 32]), tab[(dsc >> 20) * 32]);
+    const V lead = MF::unit ? full : tab[(dsc & 1023u) * 32];
+    const V v = mmul(mmul(lead, tab[((dsc >> 10) & 1023u) * 32]), tab[(dsc >> 20) * 32]);
     return v.re * jac;
   };
   auto corner_head = [&](unsigned bits) -> V {   // groups 0 and 1 (all groups when D < 6)
@@ -178,7 +188,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
         if (c == 1 || c == 2) continue;            // axial points never use a factor
         const V v = MF::factor(j, x, args.f);
         if (c == 0) cen_s[j * 32] = v;
-        else if (c < 5) tab[(L::kP34 + 2 * j + (c - 3)) * 32] = v;
+        else if (c < 5) tab[(L::kP34 + 2 * j + (c - 3)) * 32] = MF::unit ? mmul(mconj(cen_s[j * 32]), v) : v;
         else cg[c - 5] = v;
       }
       if (kHalves > 1 && half == 0) continue;
@@ -203,7 +213,11 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     cta_sync();
     // Rab[a][b] = (E[0][a] * E[a+1][b]) * E[b+1][D] with E[x][y] = ((1 * c_x) * c_{x+1}) ... * c_{y-1}; half h
     // stores the pairs with a = h (mod 2)
-    if constexpr (L::kPairs > 0) {
+    if constexpr (MF::unit) {
+      full = one;   // E[0][D] = ((1 * c_0) * c_1) ... * c_{D-1}
+#pragma unroll
+      for (int j = 0; j < D; ++j) full = mmul(full, cen_s[j * 32]);
+    } else if constexpr (L::kPairs > 0) {
       V cen[D], tail[D];   // tail[b] = E[b+1][D]
 #pragma unroll
       for (int j = 0; j < D; ++j) cen[j] = cen_s[j * 32];

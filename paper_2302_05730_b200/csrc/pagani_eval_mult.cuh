@@ -41,6 +41,9 @@ __device__ __forceinline__ MVal<false> mmul(MVal<false> a, MVal<false> b) { retu
 __device__ __forceinline__ MVal<true> mmul(MVal<true> a, MVal<true> b) {
   return MVal<true>{__fma_rn(a.re, b.re, -(a.im * b.im)), __fma_rn(a.re, b.im, a.im * b.re)};
 }
+// conjugate: the inverse of a unit-modulus factor
+__device__ __forceinline__ MVal<false> mconj(MVal<false> a) { return a; }
+__device__ __forceinline__ MVal<true> mconj(MVal<true> a) { return MVal<true>{a.re, -a.im}; }
 __device__ __forceinline__ MVal<false> mone(MVal<false>) { return MVal<false>{1.0}; }
 __device__ __forceinline__ MVal<true> mone(MVal<true>) { return MVal<true>{1.0, 0.0}; }
 
@@ -48,12 +51,17 @@ template <int FAM>
 struct MultFamily {
   static constexpr bool enabled = false;
   static constexpr bool cplx = false;
+  // unit-modulus factors (f1: exp(i theta)) have their conjugate as inverse, so a pair point is
+  // Full * rho_a * rho_b with Full = prod_j phi[j][0] and rho_x = conj(phi[x][0]) * phi[x][c]: no table of
+  // "everything but axes a and b" (D(D-1)/2 entries per region) is needed
+  static constexpr bool unit = false;
   __device__ static MVal<false> factor(int, double, const pcb_integrand&) { return MVal<false>{1.0}; }
 };
 template <>
 struct MultFamily<PCB_F1_OSCILLATORY> {
   static constexpr bool enabled = true;
   static constexpr bool cplx = true;
+  static constexpr bool unit = true;
   __device__ static MVal<true> factor(int j, double x, const pcb_integrand&) {
     double s, c;
     sincos((double)(j + 1) * x, &s, &c);
@@ -64,6 +72,7 @@ template <>
 struct MultFamily<PCB_F4_GAUSSIAN> {
   static constexpr bool enabled = true;
   static constexpr bool cplx = false;
+  static constexpr bool unit = false;
   __device__ static MVal<false> factor(int, double x, const pcb_integrand& f) {
     const double u = x - 0.5;
     return MVal<false>{exp(-f.param[0] * (u * u))};
@@ -73,12 +82,14 @@ template <>
 struct MultFamily<PCB_F5_KINKED> {
   static constexpr bool enabled = true;
   static constexpr bool cplx = false;
+  static constexpr bool unit = false;
   __device__ static MVal<false> factor(int, double x, const pcb_integrand& f) { return MVal<false>{exp(-f.param[0] * fabs(x - 0.5))}; }
 };
 template <>
 struct MultFamily<PCB_F6_DISCONTINUOUS> {
   static constexpr bool enabled = true;
   static constexpr bool cplx = false;
+  static constexpr bool unit = false;
   __device__ static MVal<false> factor(int j, double x, const pcb_integrand& f) {
     return MVal<false>{(x < f.param[j]) ? exp((double)(j + 5) * x) : 0.0};
   }
@@ -195,6 +206,14 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const
       }
     }
     __syncwarp();
+    // ---- 2b. unit-modulus factors: rho[j][c] = conj(phi[j][0]) * phi[j][c] for the pair candidates c = 3, 4 (in place)
+    if constexpr (MF::unit) {
+      if (lane < 2 * D) {
+        const int j = lane >> 1, c = 3 + (lane & 1);
+        tab[j * 8 + c] = mmul(mconj(tab[j * 8]), tab[j * 8 + c]);
+      }
+      __syncwarp();
+    } else
     // ---- 2b. Rab[pair] = E[0][a] * E[a+1][b] * E[b+1][D]: everything of a pair point but its two moved axes
     if constexpr (L::kPairs > 0) {
 #pragma unroll
@@ -244,7 +263,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const
           const int q = i - 1 - 4 * D, e = q >> 2;
           const unsigned ab = s_pair[e];
           const int a = ab & 255u, b = ab >> 8;
-          const V v = mmul(mmul(tab[L::kRab + e], tab[a * 8 + 3 + (q & 1)]), tab[b * 8 + 3 + ((q >> 1) & 1)]);
+          const V v = mmul(mmul(tab[MF::unit ? L::kE + D : L::kRab + e], tab[a * 8 + 3 + (q & 1)]), tab[b * 8 + 3 + ((q >> 1) & 1)]);
           const double fx = v.re * jac;
           if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
 #pragma unroll

@@ -34,7 +34,7 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
 template <int D>
 static const void* lanes_kernel_for(size_t* smem, int* threads) {
   if constexpr (MultFamily<PCB_FAM>::enabled) {
-    *smem = LaneLayout<D>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
+    *smem = LaneLayout<D, MultFamily<PCB_FAM>::unit>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
     *threads = MultFamily<PCB_FAM>::cplx ? 64 : 32;   // complex factors: two warps share the tables of 32 regions
     return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
   } else if constexpr (PCB_FAM == PCB_F3_CORNER_PEAK) {
