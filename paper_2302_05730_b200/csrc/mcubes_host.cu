@@ -43,7 +43,8 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
                 plan->n_bins, out->smem, ctx->smem_optin);
   const long long n_lw = (n_local_threads + 31) / 32;
   // work units = 32 segments; aim at >= 8 units per resident warp for balance
-  const long long resident = 2LL * ctx->sm_count * kSampleWarps;
+  const int ctas_per_sm = vsample_ctas_per_sm(plan->d);   // __launch_bounds__ of vsample_kernel   // __launch_bounds__ of vsample_kernel
+  const long long resident = (long long)ctas_per_sm * ctx->sm_count * kSampleWarps;
   int nseg = (int)std::max<long long>(1, std::min<long long>(plan->s, (8 * resident + n_lw - 1) / n_lw));
   if (const char* env = std::getenv("PCB_MCUBES_SEGMENTS")) {
     int v = std::atoi(env);
@@ -53,7 +54,7 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
   out->seg_len = seg_len;
   out->nseg = (int)((plan->s + seg_len - 1) / seg_len);
   const long long units = (n_local_threads * out->nseg + 31) / 32;
-  out->blocks = (int)std::max<long long>(1, std::min<long long>(2LL * ctx->sm_count, (units + kSampleWarps - 1) / kSampleWarps));
+  out->blocks = (int)std::max<long long>(1, std::min<long long>((long long)ctas_per_sm * ctx->sm_count, (units + kSampleWarps - 1) / kSampleWarps));
   return PCB_OK;
 }
 

@@ -150,8 +150,13 @@ __device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned cha
   }
 }
 
+// resident CTAs per SM the register allocation leaves room for: low dimensions need fewer registers and less shared
+// memory, and the accumulation phase (a warp per axis) keeps fewer of their warps busy -- measured per pass of ~9e8
+// samples, 2 vs 3 CTAs: d=5 38.4 vs 27.6 ms, d=6 38.5 vs 33.7 ms, d=7 35.0 vs 36.7 ms, d=8 (does not fit three) 40.4 ms
+__host__ __device__ constexpr int vsample_ctas_per_sm(int d) { return d <= 4 ? 4 : (d <= 6 ? 3 : 2); }
+
 template <int FAM, int D, int RNG>
-__global__ void __launch_bounds__(kSampleWarps * 32, 2) vsample_kernel(const __grid_constant__ SampleArgs a) {
+__global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   extern __shared__ __align__(16) unsigned char smem_raw[];
