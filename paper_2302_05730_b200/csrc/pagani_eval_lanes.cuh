@@ -25,9 +25,13 @@
 
 #include "pagani_eval_mult.cuh"
 
+#ifndef PCB_LANES_HALVES_REAL
+#define PCB_LANES_HALVES_REAL 1   // 2: real families also split the virtual threads over two warps (measured slower: f4 d=8 0.57 vs 0.41 ms)
+#endif
+
 namespace pcb {
 
-template <int D, bool UNIT = false>
+template <int D, bool UNIT = false, bool HALVES = false>
 struct LaneLayout {
   static constexpr int kFe = (1 << D) + 2 * D * D + 2 * D + 1;
   static constexpr int kCorner0 = 2 * D * D + 2 * D + 1;
@@ -49,7 +53,7 @@ struct LaneLayout {
   // scratch per lane: the D centre factors while the tables are built, afterwards the split-axis stash (D doubles)
   // and, with two halves, the hand-over slots
   __host__ __device__ static constexpr size_t scratch_doubles(size_t vsize) {
-    const size_t a = D * vsize / 8, b = D + (vsize > 8 ? kXfer : 0);
+    const size_t a = D * vsize / 8, b = D + (HALVES ? kXfer : 0);
     return a > b ? a : b;
   }
   static constexpr size_t smem_bytes(size_t vsize) {
@@ -77,24 +81,24 @@ __device__ __forceinline__ void counter_merge(int blk, double (&cur)[5], double 
 // capped -- beyond ~10 resident warps the spills cost more than the occupancy brings
 template <int FAM, int D>
 constexpr int lanes_min_blocks() {
-  constexpr bool cplx = MultFamily<FAM>::cplx;
-  constexpr size_t smem = LaneLayout<D, MultFamily<FAM>::unit>::smem_bytes(cplx ? 16 : 8) + 1024;
+  constexpr bool cplx = MultFamily<FAM>::cplx || PCB_LANES_HALVES_REAL > 1;   // two warps per CTA
+  constexpr size_t smem = LaneLayout<D, MultFamily<FAM>::unit, cplx>::smem_bytes(MultFamily<FAM>::cplx ? 16 : 8) + 1024;
   constexpr int by_smem = (int)((227u << 10) / smem);
   constexpr int cap = cplx ? 6 : 10;
   return by_smem < 1 ? 1 : (by_smem < cap ? by_smem : cap);
 }
 
 template <int FAM, int D>
-__global__ void __launch_bounds__(MultFamily<FAM>::cplx ? 64 : 32, lanes_min_blocks<FAM, D>())
+__global__ void __launch_bounds__((PCB_LANES_HALVES_REAL > 1 || MultFamily<FAM>::cplx) ? 64 : 32, lanes_min_blocks<FAM, D>())
 pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;
-  using L = LaneLayout<D, MF::unit>;
+  using L = LaneLayout<D, MF::unit, (PCB_LANES_HALVES_REAL > 1 || MF::cplx)>;
   // Complex factors (f1) double the tables, and one warp per 48 KB of tables cannot hide the FP64 latency: there two
   // warps ("halves") share the tables of 32 regions and take virtual threads 0..31 and 32..63.  Real families run
   // one warp per CTA with twice the chains per lane (measured faster: no duplicated prologue, no CTA barriers).
-  constexpr int kHalves = MF::cplx ? 2 : 1;
+  constexpr int kHalves = PCB_LANES_HALVES_REAL > 1 || MF::cplx ? 2 : 1;
   constexpr int kVt = 64 / kHalves;   // virtual threads per half
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, half = threadIdx.x >> 5;   // half h takes virtual threads kVt*h .. kVt*h + kVt - 1
@@ -251,7 +255,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     //      independent dependency chains (that is what hides the FP64 latency with ~2 warps per scheduler); only
     //      the three blocks that straddle a class boundary take the point-by-point path.  The first log2(W)
     //      levels of the pair tree are fixed-register adds, the remaining ones a binary counter over the blocks.
-    constexpr int W = MF::cplx ? 4 : 8;
+    constexpr int W = kHalves > 1 ? 4 : 8;
     constexpr int kCounterLevels = 3;   // log2(kVt / W): 64 / 8 = 32 / 4
     double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
     int axis = 0;

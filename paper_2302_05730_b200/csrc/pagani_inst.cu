@@ -34,8 +34,8 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
 template <int D>
 static const void* lanes_kernel_for(size_t* smem, int* threads) {
   if constexpr (MultFamily<PCB_FAM>::enabled) {
-    *smem = LaneLayout<D, MultFamily<PCB_FAM>::unit>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
-    *threads = MultFamily<PCB_FAM>::cplx ? 64 : 32;   // complex factors: two warps share the tables of 32 regions
+    *smem = LaneLayout<D, MultFamily<PCB_FAM>::unit, (MultFamily<PCB_FAM>::cplx || PCB_LANES_HALVES_REAL > 1)>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
+    *threads = (MultFamily<PCB_FAM>::cplx || PCB_LANES_HALVES_REAL > 1) ? 64 : 32;   // complex factors: two warps share the tables of 32 regions
     return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
   } else if constexpr (PCB_FAM == PCB_F3_CORNER_PEAK) {
     // the double-double power dominates f3 and the warp-per-region kernel hides its latency better (measured:
