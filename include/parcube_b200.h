@@ -87,6 +87,8 @@ typedef struct {
   int32_t initial_regions;
   int32_t err_mode;        /* pcb_err_mode */
   double rel_floor;
+  double abs_tol;          /* extension (epsabs, default 0 = the reference): converged when
+                              errorest <= max(abs_tol, rel_tol*|estimate|)                  */
 } pcb_pagani_config;
 
 /* First non-finite evaluation in row-major (region, point) order (pagani.py:206-209,
@@ -281,12 +283,14 @@ pcb_status pcb_grid_transform(pcb_ctx* ctx, int32_t d, int32_t n_bins, const dou
                               const double* y, double* x, double* jac, int64_t* bins);
 
 /* ---- m-Cubes driver: replaces run (mcubes.py:332-382), loop device-resident ---------------
- * rel_tol <= 0 reproduces the reference (fixed iteration count); rel_tol > 0 adds the
+ * rel_tol <= 0 and abs_tol <= 0 reproduce the reference (fixed iteration count); otherwise the run stops after
+ * the first iteration with errorest <= max(abs_tol, rel_tol*|estimate|).  rel_tol > 0 adds the
  * time-to-epsrel stop of BASELINE.md section 3.  iterations_out: capacity `iterations`.
  * final_boundaries (optional): (d, n_bins+1).                                                 */
 pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan,
                           int32_t iterations, uint64_t seed, int32_t rng_kind, int32_t adapt, double alpha,
-                          int32_t smoothing, double rel_tol, pcb_mcubes_iteration* iterations_out,
+                          int32_t smoothing, double rel_tol, double abs_tol,
+                          pcb_mcubes_iteration* iterations_out,
                           int32_t* n_done, pcb_mcubes_progress_fn progress, void* user,
                           double* contributions_out /* optional (iterations, d, n_bins) */,
                           double* final_boundaries, double* seconds_device, pcb_nonfinite* bad);

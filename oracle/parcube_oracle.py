@@ -206,7 +206,7 @@ def bisect(lefts, lengths, axes):
 
 
 def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1 << 26,
-                  initial_regions=1024, workers=1, bounds=None, time_budget_s=None, **kw):
+                  initial_regions=1024, workers=1, bounds=None, time_budget_s=None, abs_tol=0.0, **kw):
     """The refinement driver (pagani.py:300-391). Returns a dict mirroring IntegralResult.
     `time_budget_s` is an oracle-only escape hatch for the bounded CPU baseline."""
     import time
@@ -225,7 +225,8 @@ def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1
         errorest = fin_e + tree_sum(act_e)
         history.append((estimate, errorest, fin_n + act_i.size))
         active_counts.append(int(act_i.size))
-        if errorest <= rel_tol * abs(estimate):
+        # abs_tol = 0 is the reference (pagani.py:350, 362); abs_tol > 0 is the epsabs extension of the B200 build
+        if errorest <= max(abs_tol, rel_tol * abs(estimate)):
             converged, reason = True, "tolerance met"
             break
         if it == max_iterations:
@@ -238,7 +239,7 @@ def pagani_refine(family, d, rule, rel_tol=1e-3, max_iterations=50, region_cap=1
             reason = "oracle time budget"
             break
         vol = np.prod(lengths, axis=1)
-        budget = 0.8 * rel_tol * abs(estimate)
+        budget = 0.8 * abs_tol if abs_tol > rel_tol * abs(estimate) else 0.8 * rel_tol * abs(estimate)
         mask = act_e > budget * vol
         if not mask.any():
             mask = act_e >= act_e.max()
@@ -454,7 +455,7 @@ def combine(integrals, variances):
 
 
 def mcubes_run(family, n, d, iterations, seed=0, workers=1, n_bins=500, adapt=True,
-               alpha=1.5, smoothing=True, bounds=None, rel_tol=None):
+               alpha=1.5, smoothing=True, bounds=None, rel_tol=None, abs_tol=None):
     """mcubes.run (mcubes.py:332-382); `rel_tol` adds the time-to-epsrel stop rule of
     BASELINE.md section 3 (stop after the first iteration whose cumulative
     errorest/|estimate| <= rel_tol) -- the reference itself has no tolerance stop."""
@@ -469,7 +470,7 @@ def mcubes_run(family, n, d, iterations, seed=0, workers=1, n_bins=500, adapt=Tr
         est, err, chi2 = combine([r["integral"] for r in its], [r["variance"] for r in its])
         progress.append(dict(iteration=it, estimate=est, errorest=err, chi2_per_dof=chi2,
                              iter_integral=res["integral"], iter_sd=math.sqrt(res["variance"])))
-        if rel_tol is not None and err <= rel_tol * abs(est):
+        if (rel_tol is not None or abs_tol is not None) and err <= max(abs_tol or 0.0, (rel_tol or 0.0) * abs(est)):
             break
     est, err, chi2 = combine([r["integral"] for r in its], [r["variance"] for r in its])
     return dict(estimate=est, errorest=err, chi2_per_dof=chi2, iterations=its, plan=plan,

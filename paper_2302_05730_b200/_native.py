@@ -55,7 +55,7 @@ class RuleC(C.Structure):
 class PaganiConfigC(C.Structure):
     _fields_ = [("rel_tol", C.c_double), ("max_iterations", C.c_int32), ("group_size", C.c_int32),
                 ("region_cap", C.c_int64), ("initial_regions", C.c_int32), ("err_mode", C.c_int32),
-                ("rel_floor", C.c_double)]
+                ("rel_floor", C.c_double), ("abs_tol", C.c_double)]
 
 
 class NonFiniteC(C.Structure):
@@ -136,7 +136,7 @@ SIGNATURES = {
     "pcb_grid_refine": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                                   C.c_void_p]),
     "pcb_mcubes_run": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_int32, C.c_uint64,
-                                 C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.POINTER(McubesIterationC),
+                                 C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(McubesIterationC),
                                  C.POINTER(C.c_int32), MCUBES_PROGRESS_FN, C.c_void_p, C.c_void_p, C.c_void_p, _DP,
                                  C.POINTER(NonFiniteC)]),
     "pcb_grid_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
@@ -315,6 +315,7 @@ def pagani_config_to_c(cfg) -> PaganiConfigC:
     c.rel_tol, c.max_iterations, c.group_size = float(cfg.rel_tol), int(cfg.max_iterations), int(cfg.group_size)
     c.region_cap, c.initial_regions = int(cfg.region_cap), int(cfg.initial_regions)
     c.err_mode, c.rel_floor = ERR_MODES[cfg.err_mode], float(cfg.rel_floor)
+    c.abs_tol = float(getattr(cfg, "abs_tol", 0.0))
     return c
 
 
@@ -433,7 +434,7 @@ def grid_refine(boundaries: np.ndarray, contributions: np.ndarray, alpha: float,
 
 
 def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, rng_kind: int, adapt: bool, alpha: float,
-               smoothing: bool, rel_tol: float = 0.0, progress=None, keep_contributions=True, device=None):
+               smoothing: bool, rel_tol: float = 0.0, progress=None, keep_contributions=True, device=None, abs_tol: float = 0.0):
     ctx = context(device)
     d = plan.d
     fc, pc, bad = spec.to_c(), plan_to_c(plan, n_bins), NonFiniteC()
@@ -458,7 +459,7 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
     cb = MCUBES_PROGRESS_FN(_cb) if progress is not None else C.cast(None, MCUBES_PROGRESS_FN)
     with ctx.call_lock:
         st = ctx.lib.pcb_mcubes_run(ctx.handle, C.byref(fc), C.byref(pc), int(iterations), C.c_uint64(seed & (2**64 - 1)),
-                                    rng_kind, int(bool(adapt)), float(alpha), int(bool(smoothing)), float(rel_tol), its,
+                                    rng_kind, int(bool(adapt)), float(alpha), int(bool(smoothing)), float(rel_tol), float(abs_tol), its,
                                     C.byref(n_done), cb, None, None if contribs is None else _ptr(contribs),
                                     _ptr(final_b), C.byref(seconds), C.byref(bad))
         if failure:

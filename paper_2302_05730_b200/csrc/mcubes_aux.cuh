@@ -340,7 +340,7 @@ struct FinishArgs {
   double* hist_i;               // run history of (integral, variance), capacity = iterations
   double* hist_v;
   int iteration;
-  double rel_tol;
+  double rel_tol, abs_tol;
   McRecord* record;             // pinned host memory (nullptr: leave the results in scalars only)
   unsigned long long seq;
 };
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ Fin
     const double var = fmax(variance, 0.0);
     a.hist_i[a.iteration] = integral;
     a.hist_v[a.iteration] = var;
-    if (a.rel_tol > 0.0) {
+    if (a.rel_tol > 0.0 || a.abs_tol > 0.0) {
       double wsum = 0.0, dot = 0.0;
       for (int i = 0; i <= a.iteration; ++i) {
         const double w = 1.0 / fmax(a.hist_v[i], 1e-30);
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ Fin
         dot = dot + w * a.hist_i[i];
       }
       const double est = dot / wsum, err = 1.0 / sqrt(wsum);
-      if (err <= a.rel_tol * fabs(est)) stop = 1;
+      if (err <= fmax(a.abs_tol, a.rel_tol * fabs(est))) stop = 1;
     }
     // re-arm the scalars for the next pass of the run
     a.scalars[0] = ~0ULL;

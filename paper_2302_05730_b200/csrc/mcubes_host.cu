@@ -139,7 +139,7 @@ struct PassTail {
   double* contrib_copy = nullptr;      // device slot of the run's per-iteration tables (optional)
   double* hist_i = nullptr;            // device run history
   double* hist_v = nullptr;
-  double rel_tol = 0.0;
+  double rel_tol = 0.0, abs_tol = 0.0;
   McRecord* record = nullptr;          // pinned
   unsigned long long seq = 0;
 };
@@ -263,6 +263,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   fa.hist_v = tail.hist_v;
   fa.iteration = tail.iteration;
   fa.rel_tol = tail.rel_tol;
+  fa.abs_tol = tail.abs_tol;
   fa.record = tail.record;
   fa.seq = tail.seq;
   const size_t finish_smem = std::max<size_t>((size_t)(4 * nb + 4), 2048) * sizeof(double);
@@ -424,7 +425,7 @@ pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g,
 }
 
 pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, int32_t iterations, uint64_t seed,
-                          int32_t rng_kind, int32_t adapt, double alpha, int32_t smoothing, double rel_tol,
+                          int32_t rng_kind, int32_t adapt, double alpha, int32_t smoothing, double rel_tol, double abs_tol,
                           pcb_mcubes_iteration* iterations_out, int32_t* n_done, pcb_mcubes_progress_fn progress, void* user,
                           double* contributions_out, double* final_boundaries, double* seconds_device, pcb_nonfinite* bad) {
   if (!ctx) return PCB_INVALID;
@@ -494,6 +495,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     tail.hist_i = hist_i;
     tail.hist_v = hist_v;
     tail.rel_tol = rel_tol;
+    tail.abs_tol = abs_tol > 0 ? abs_tol : 0.0;
     tail.record = records + it;
     tail.seq = (token << 20) | (unsigned long long)(it + 1);
     const unsigned long long it_seed = derive_seed(seed, (unsigned long long)it);  // mcubes.py:58-60, 359

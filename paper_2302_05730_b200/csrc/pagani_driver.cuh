@@ -7,6 +7,17 @@
 
 namespace pcb {
 
+// errorest target and per-unit-volume split budget (pagani.py:350, 362).  With abs_tol = 0 (the reference) these are
+// the reference's own expressions, rel_tol*|estimate| and 0.8*rel_tol*|estimate| in that association; a positive
+// abs_tol (epsabs extension) takes over where it is the larger target.
+__host__ __device__ inline double tolerance_target(double rel_tol, double abs_tol, double estimate) {
+  const double rel = rel_tol * fabs(estimate);
+  return abs_tol > rel ? abs_tol : rel;
+}
+__host__ __device__ inline double split_budget(double rel_tol, double abs_tol, double estimate) {
+  return abs_tol > rel_tol * fabs(estimate) ? 0.8 * abs_tol : 0.8 * rel_tol * fabs(estimate);
+}
+
 constexpr int kTreeBlock = 256;                 // threads
 constexpr int kTreeSpan = kTreeBlock * 4;       // elements per CTA: one aligned 2^10 subtree
 
@@ -260,7 +271,7 @@ struct ShortIterArgs {
   double* out_lengths;
   double fin_i, fin_e;
   long long processed, region_cap;
-  double rel_tol;
+  double rel_tol, abs_tol;
   int iteration, max_iterations;
   unsigned long long* bad;     // device flag of the evaluate kernel
   ShortIterRecord* record;
@@ -294,13 +305,13 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
   const unsigned long long bad = *a.bad;
   int action = 0;
   if (bad != ~0ULL) action = 4;   // the host raises; nothing else matters
-  else if (errorest <= a.rel_tol * fabs(estimate)) action = 1;
+  else if (errorest <= tolerance_target(a.rel_tol, a.abs_tol, estimate)) action = 1;
   else if (a.iteration == a.max_iterations) action = 2;
   long long n_split = 0;
   double fin_i = a.fin_i, fin_e = a.fin_e;
   if (action == 0) {
     // classification (pagani.py:361-365)
-    const double budget = 0.8 * a.rel_tol * fabs(estimate);
+    const double budget = split_budget(a.rel_tol, a.abs_tol, estimate);
     bool split = false;
     if (have) {
       double vol = a.lengths[r];

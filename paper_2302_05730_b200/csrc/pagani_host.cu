@@ -252,6 +252,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   PCB_TRY(validate_rule(ctx, f, rule, cfg));
   if (!result) return fail(ctx, PCB_INVALID, "result is NULL");
   if (!(cfg->rel_tol > 0)) return fail(ctx, PCB_INVALID, "rel_tol must be > 0");
+  if (!(cfg->abs_tol >= 0)) return fail(ctx, PCB_INVALID, "abs_tol must be >= 0");
   if (cfg->max_iterations < 0 || cfg->initial_regions < 1) return fail(ctx, PCB_INVALID, "bad iteration/initial-region budget");
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int d = f->d;
@@ -340,6 +341,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       sa.fin_i = fin_i; sa.fin_e = fin_e;
       sa.processed = processed; sa.region_cap = cfg->region_cap;
       sa.rel_tol = cfg->rel_tol;
+      sa.abs_tol = cfg->abs_tol;
       sa.iteration = it; sa.max_iterations = cfg->max_iterations;
       sa.bad = sc_u + S_BAD;
       sa.record = srec;
@@ -406,7 +408,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     if (records) records[n_rec] = rec;
     ++n_rec;
     if (progress) progress(user, &rec);
-    if (errorest <= cfg->rel_tol * std::fabs(estimate)) {
+    if (errorest <= tolerance_target(cfg->rel_tol, cfg->abs_tol, estimate)) {
       converged = true;
       reason = PCB_STOP_TOLERANCE;
       break;
@@ -415,7 +417,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     if (n == 0) { reason = PCB_STOP_NO_ACTIVE; break; }
 
     // classification (pagani.py:361-365)
-    const double budget = 0.8 * cfg->rel_tol * std::fabs(estimate);
+    const double budget = split_budget(cfg->rel_tol, cfg->abs_tol, estimate);
     const long long nblk = (n + kScanBlock - 1) / kScanBlock;
     PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)n));
     PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));

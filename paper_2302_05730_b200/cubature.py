@@ -27,19 +27,23 @@ TWO_LEVEL_SAFETY = 10.0  # pagani.py:40
 class PaganiConfig(_Frozen):
     """Tolerance, budgets and schedule shape (pagani.py:44-69).
 
+    `abs_tol` (epsabs, an extension; 0 = the reference) widens the target to
+    max(abs_tol, rel_tol*|estimate|), for the stop test and for the split threshold alike.
     `group_size` (the strided schedule width, 1..64 on the device) changes floating-point
     association only; `chunk` is accepted for compatibility and only affects which group id a
     non-finite report carries.
     """
 
     __slots__ = ("rel_tol", "max_iterations", "group_size", "region_cap", "initial_regions", "err_mode",
-                 "rel_floor", "chunk")
+                 "rel_floor", "chunk", "abs_tol")
 
     def __init__(self, rel_tol: float = 1e-3, max_iterations: int = 50, group_size: int = 64,
                  region_cap: int = DEFAULT_REGION_CAP, initial_regions: int = 1024, err_mode: str = ERR_TWO_LEVEL,
-                 rel_floor: float = 1e-15, chunk: int = 512):
+                 rel_floor: float = 1e-15, chunk: int = 512, abs_tol: float = 0.0):
         if rel_tol <= 0:
             raise ValueError("rel_tol must be > 0")
+        if not abs_tol >= 0:
+            raise ValueError("abs_tol must be >= 0")
         if group_size < 1 or chunk < 1:
             raise ValueError("group_size and chunk must be >= 1")
         if err_mode not in (ERR_TWO_LEVEL, ERR_MAX_NULL, ERR_MAX_PAIRWISE):
@@ -47,7 +51,7 @@ class PaganiConfig(_Frozen):
         for k, v in (("rel_tol", float(rel_tol)), ("max_iterations", int(max_iterations)),
                      ("group_size", int(group_size)), ("region_cap", int(region_cap)),
                      ("initial_regions", int(initial_regions)), ("err_mode", err_mode),
-                     ("rel_floor", float(rel_floor)), ("chunk", int(chunk))):
+                     ("rel_floor", float(rel_floor)), ("chunk", int(chunk)), ("abs_tol", float(abs_tol))):
             self._put(k, v)
 
 

@@ -127,7 +127,7 @@ def mcubes_iteration_sharded(spec, plan, boundaries, seed, comm, backend, rng_ki
 
 
 def mcubes_run_sharded(f, n, d, iterations, comm, backend=None, params=None, seed=0, n_bins=500, group_size=128,
-                       target_groups=256, adapt=True, progress=None, rel_tol=None, rng="reference-hash"):
+                       target_groups=256, adapt=True, progress=None, rel_tol=None, rng="reference-hash", abs_tol=None):
     """mcubes.run (mcubes.py:332-382) with the sub-cubes sharded over comm.world GPUs.
 
     Every rank returns the same MonteCarloResult; (integral, variance) per iteration are
@@ -153,7 +153,7 @@ def mcubes_run_sharded(f, n, d, iterations, comm, backend=None, params=None, see
         if progress is not None:
             progress({"iteration": it, "estimate": est, "errorest": err, "chi2_per_dof": chi2,
                       "iter_integral": integral, "iter_sd": math.sqrt(variance)})
-        if rel_tol is not None and err <= rel_tol * abs(est):
+        if (rel_tol is not None or abs_tol is not None) and err <= max(abs_tol or 0.0, (rel_tol or 0.0) * abs(est)):
             break
     est, err, chi2 = combine_iterations(history)
     return MonteCarloResult(est, err, chi2, history, plan)
@@ -282,7 +282,9 @@ def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None):
         if progress is not None:
             progress({"iteration": iteration, "n_regions": fin_count + n_active, "active": n_active,
                       "estimate": estimate, "errorest": errorest})
-        if errorest <= cfg.rel_tol * abs(estimate):
+        abs_tol = getattr(cfg, "abs_tol", 0.0)
+        rel_target = cfg.rel_tol * abs(estimate)
+        if errorest <= (abs_tol if abs_tol > rel_target else rel_target):
             converged, reason = True, "tolerance met"
             break
         if iteration == cfg.max_iterations:
@@ -291,7 +293,7 @@ def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None):
         if n_active == 0:
             reason = "no active regions left"
             break
-        budget = 0.8 * cfg.rel_tol * abs(estimate)
+        budget = 0.8 * abs_tol if abs_tol > rel_target else 0.8 * cfg.rel_tol * abs(estimate)
         local_split = shard.classify(budget, 0, 0.0)
         split_counts = [int(round(v[0])) for v in comm.allgather(np.array([float(local_split)]))]
         if sum(split_counts) == 0:                      # force progress on the globally worst regions

@@ -203,13 +203,15 @@ def combine_iterations(iteration_results: list) -> tuple[float, float, float]:
 
 def run(f: Integrand, n, d: int, iterations: int, params: GridRefineParams | None = None, seed: int = 0,
         exec_cfg: ExecConfig | None = None, n_bins: int = 500, group_size: int = 128, target_groups: int = 256,
-        adapt: bool = True, progress=None, rel_tol: float | None = None, rng: str = "reference-hash") -> MonteCarloResult:
+        adapt: bool = True, progress=None, rel_tol: float | None = None, rng: str = "reference-hash",
+        abs_tol: float | None = None) -> MonteCarloResult:
     """Iterate {sample; refine grid} and combine the iteration estimates (mcubes.py:332-382).
 
     The loop is device-resident (grid, contribution table and partial sums never leave HBM);
     the host receives one (integral, variance) pair per iteration.  `rel_tol` (extension,
     default None = reference behaviour) stops after the first iteration whose cumulative
-    errorest/|estimate| is <= rel_tol; `iterations` is then the maximum.
+    errorest/|estimate| is <= rel_tol; `iterations` is then the maximum.  `abs_tol` (epsabs) widens the
+    target to max(abs_tol, rel_tol*|estimate|); either one alone may be given.
     """
     if iterations < 1:
         raise ValueError("iterations must be >= 1")
@@ -221,7 +223,8 @@ def run(f: Integrand, n, d: int, iterations: int, params: GridRefineParams | Non
     try:
         its, contribs, _final_b, _secs = _native.mcubes_run(
             f.device_spec(), plan, n_bins, iterations, seed, RNG_KINDS[rng], adapt, params.alpha, params.smoothing,
-            0.0 if rel_tol is None else float(rel_tol), progress, device=_device_of(exec_cfg))
+            0.0 if rel_tol is None else float(rel_tol), progress, device=_device_of(exec_cfg),
+            abs_tol=0.0 if abs_tol is None else float(abs_tol))
     except _native.NonFiniteStatus as exc:
         _raise_nonfinite(exc, plan)
     history = [McubesIterationResult(r.integral, r.variance, _table(d, n_bins, contribs[i]), r.n_samples, r.clamp_events)

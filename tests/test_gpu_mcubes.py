@@ -296,3 +296,23 @@ def test_constant_integrand_is_exact():
     assert abs(res.integral - 1.0) <= 1e-12 and res.variance <= 1e-20
     assert res.integral == want["integral"] and abs(res.variance - want["variance"]) <= 1e-6 * want["variance"]
     assert res.clamp_events == want["clamp_events"]
+
+
+def test_run_abs_tol_extension():
+    """epsabs for m-Cubes: stop after the first iteration with errorest <= max(abs_tol, rel_tol*|estimate|)."""
+    import paper_2302_05730_b200 as pb
+    from oracle import parcube_oracle as po
+    f = pb.get_integrand("f4", 5)
+    free = pb.mcubes_run(f, 10**5, 5, 8, seed=3)
+    errs = []
+    for k in range(1, len(free.iterations) + 1):
+        errs.append(pb.combine_iterations(free.iterations[:k])[1])
+    target = errs[3] * 1.0000001          # reached at iteration 3 (0-based), not before
+    assert all(e > target for e in errs[:3])
+    got = pb.mcubes_run(f, 10**5, 5, 8, seed=3, abs_tol=target)
+    assert len(got.iterations) == 4
+    assert got.estimate == pb.combine_iterations(free.iterations[:4])[0]
+    want = po.mcubes_run("f4", 10**5, 5, 8, seed=3, abs_tol=target)
+    assert len(want["iterations"]) == 4
+    both = pb.mcubes_run(f, 10**5, 5, 8, seed=3, abs_tol=target, rel_tol=1e-30)
+    assert len(both.iterations) == 4

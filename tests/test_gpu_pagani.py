@@ -351,3 +351,20 @@ def test_short_list_iteration_kernel_equals_general_path(fam, d, tol, kw, monkey
     assert a.history == b.history
     assert (a.estimate, a.errorest, a.iterations, a.regions_processed, a.converged, a.reason) == \
            (b.estimate, b.errorest, b.iterations, b.regions_processed, b.converged, b.reason)
+
+
+@pytest.mark.parametrize("fam,d,rel,absv", [("f2", 4, 1e-12, 1e4), ("sum", 3, 1e-16, 1e-13), ("f4", 5, 1e-9, 1e-11),
+                                            ("f5", 3, 1e-12, 1e-6), ("f2", 5, 1e-3, 0.0)])
+def test_abs_tol_extension_matches_oracle(fam, d, rel, absv):
+    """epsabs (BASELINE.json north_star; the reference has rel_tol only): the target becomes
+    max(abs_tol, rel_tol*|estimate|) for the stop test and the split threshold.  abs_tol = 0 is the reference."""
+    res = pb.refine(pb.get_integrand(fam, d), pb.PaganiConfig(rel_tol=rel, abs_tol=absv, max_iterations=30))
+    want = po.pagani_refine(fam, d, rule_dict(pb.build_rule(d)), rel_tol=rel, abs_tol=absv, max_iterations=30)
+    assert (res.iterations, res.regions_processed, res.reason, res.converged) == \
+           (want["iterations"], want["regions_processed"], want["reason"], want["converged"])
+    if fam in EXACT:
+        assert res.history == want["history"]
+    else:
+        assert abs(res.estimate - want["estimate"]) <= REL_EST * abs(want["estimate"])
+    if res.converged:
+        assert res.errorest <= max(absv, rel * abs(res.estimate))
