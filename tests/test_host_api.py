@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_sizes_match_header_layout():
     assert ctypes.sizeof(_native.IntegrandC) == 16 + 8 * (3 * 12 + 1)
     assert ctypes.sizeof(_native.RuleC) == 8 + 8 * 7 + 8 * 25 + 4 * 6 + 16 + 16 + 32
-    assert ctypes.sizeof(_native.PaganiConfigC) == 40
+    assert ctypes.sizeof(_native.PaganiConfigC) == 48   # ... rel_floor, abs_tol
     assert ctypes.sizeof(_native.NonFiniteC) == 24 + 96
     assert ctypes.sizeof(_native.McubesPlanC) == 40
 
@@ -156,3 +156,14 @@ def test_cli_argument_handling_matches_reference(capsys):
     with pytest.raises(harness.CliError):
         harness.parse_config("threads=8")
     capsys.readouterr()
+
+
+def test_abs_tol_is_an_extension_with_reference_default():
+    """epsabs (BASELINE.json north_star): accepted everywhere, 0 by default = the reference's rel_tol-only rule."""
+    import paper_2302_05730_b200 as pb
+    assert pb.PaganiConfig().abs_tol == 0.0
+    assert pb.PaganiConfig(abs_tol=1e-7).abs_tol == 1e-7
+    with pytest.raises(ValueError):
+        pb.PaganiConfig(abs_tol=-1.0)
+    c = _native.pagani_config_to_c(pb.PaganiConfig(rel_tol=1e-4, abs_tol=2e-9))
+    assert (c.rel_tol, c.abs_tol) == (1e-4, 2e-9)
