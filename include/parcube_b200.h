@@ -185,9 +185,10 @@ int64_t pcb_launch_count(const pcb_ctx* ctx);
 pcb_status pcb_measure_fp64_peak(pcb_ctx* ctx, double* tflops);
 
 /* ---- per-kernel timing for the roofline report -------------------------------------------
- * Between begin and end every launch of the two dominant kernels (PAGANI evaluate, m-Cubes
- * V-Sample and its bin accumulation) is bracketed by CUDA events on the launching stream.  `kind` 0 =
- * evaluate (units = regions), 1 = V-Sample (units = samples), 2 = bin accumulation (units = records).  end() synchronises and returns the sums.          */
+ * Between begin and end every launch of the two dominant kernels (PAGANI evaluate, the m-Cubes
+ * V-Sample pass) is bracketed by CUDA events on the launching stream.  `kind` 0 = evaluate (units =
+ * regions), 1 = V-Sample pass, sampling and accumulation phases (units = samples); 2 is unused since the
+ * accumulation moved into the pass kernel.  end() synchronises and returns the sums.          */
 pcb_status pcb_profile_begin(pcb_ctx* ctx);
 pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_t* launches, double* units);
 

@@ -78,7 +78,7 @@ struct pcb_ctx {
   struct Span { cudaEvent_t a, b; double units; int tag; };
   std::vector<Span> spans[3];
   std::vector<Span> span_pool;
-  pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject, mc_rec;
+  pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject;
   // pcb_mcubes_run: device run state (stop iteration, history), per-iteration tables, pinned iteration records
   pcb::DevBuf mc_state, mc_tables;
   void* mc_records = nullptr;
