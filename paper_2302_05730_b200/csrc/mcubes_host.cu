@@ -41,7 +41,9 @@ static pcb_status plan_launch(pcb_ctx* ctx, const pcb_mcubes_plan* plan, long lo
   if (out->smem > ctx->smem_optin)
     return fail(ctx, PCB_INVALID, "d=%d, n_bins=%d needs %zu B of shared memory per CTA, device offers %zu", plan->d,
                 plan->n_bins, out->smem, ctx->smem_optin);
-  const long long n_lw = (n_local_threads + 31) / 32;
+  // Segments per logical thread are a function of the PLAN, not of the shard: a thread's (I, Var) is the serial sum of
+  // its segment sums, so a shard must cut its threads exactly like the single-device run to reproduce its bits.
+  const long long n_lw = ((plan->m + plan->s - 1) / plan->s + 31) / 32;
   // work units = 32 segments; aim at >= 8 units per resident warp for balance
   const int ctas_per_sm = vsample_ctas_per_sm(plan->d);   // __launch_bounds__ of vsample_kernel   // __launch_bounds__ of vsample_kernel
   const long long resident = (long long)ctas_per_sm * ctx->sm_count * kSampleWarps;

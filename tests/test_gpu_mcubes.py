@@ -316,3 +316,46 @@ def test_run_abs_tol_extension():
     assert len(want["iterations"]) == 4
     both = pb.mcubes_run(f, 10**5, 5, 8, seed=3, abs_tol=target, rel_tol=1e-30)
     assert len(both.iterations) == 4
+
+
+def test_full_size_pass_properties_config4():
+    """BASELINE config 4 at its full size (f3, d = 8, n = 1e9 -> 8.6e8 samples per pass), through properties that
+    do not need the CPU oracle: every sample lands in exactly one bin per axis (equal row sums), the pass is
+    deterministic bit for bit, work-group shards reassemble to the single-device sums, and the estimate sits
+    within 3 sigma of the closed-form value (mcubes.py:268-308)."""
+    d, n = 8, 10**9
+    plan, grid = pb.make_plan(n, d), pb.init_grid(d)
+    assert (plan.g, plan.m, plan.p, plan.s) == (12, 429981696, 2, 13122)   # SURVEY 8(a) M2
+    spec = pb.get_integrand("f3", d).device_spec()
+    a, ca, gpa = _native.mcubes_sample(spec, plan, grid.boundaries, 0, want_group_partials=True)
+    b, cb, _ = _native.mcubes_sample(spec, plan, grid.boundaries, 0, want_group_partials=True)
+    assert (a.integral, a.variance, a.clamp_events) == (b.integral, b.variance, b.clamp_events)
+    assert np.array_equal(ca, cb)
+    assert a.n_samples == plan.m * plan.p == 859963392
+    rows = ca.sum(axis=1)
+    assert np.all(np.abs(rows - rows[0]) <= 1e-11 * rows[0])
+    truth = pb.reference_value("f3", d).value
+    assert abs(a.integral - truth) <= 3.0 * np.sqrt(a.variance)
+    # two shards on work-group boundaries: same group partials, tables add up
+    cut = (plan.n_groups // 3) * plan.group_size
+    lo, clo, gplo = _native.mcubes_sample(spec, plan, grid.boundaries, 0, thread_range=(0, cut), want_group_partials=True)
+    hi, chi, gphi = _native.mcubes_sample(spec, plan, grid.boundaries, 0, thread_range=(cut, plan.n_threads), want_group_partials=True)
+    assert np.array_equal(np.concatenate([gplo, gphi]), gpa)
+    assert np.allclose(clo + chi, ca, rtol=1e-12, atol=0)
+    assert lo.n_samples + hi.n_samples == a.n_samples
+
+
+def test_segmented_thread_shards_reassemble_bit_for_bit():
+    """Same contract as test_vsample_thread_shards_reassemble, with the launch free to cut each logical thread into
+    segments: the cut is a function of the plan, never of the shard, so shards of any size reproduce the bits."""
+    d, n = 7, 3 * 10**7
+    plan, grid = pb.make_plan(n, d), pb.init_grid(d)
+    assert plan.s > 8
+    spec = pb.get_integrand("f5", d).device_spec()
+    whole, c_whole, gp_whole = _native.mcubes_sample(spec, plan, grid.boundaries, 11, want_group_partials=True)
+    cuts = [0, plan.group_size, 7 * plan.group_size, 200 * plan.group_size, plan.n_threads]
+    parts = []
+    for t0, t1 in zip(cuts[:-1], cuts[1:]):
+        _it, _c, gp = _native.mcubes_sample(spec, plan, grid.boundaries, 11, thread_range=(t0, t1), want_group_partials=True)
+        parts.append(gp)
+    assert np.array_equal(np.concatenate(parts), gp_whole)
