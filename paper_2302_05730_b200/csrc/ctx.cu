@@ -102,6 +102,7 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
   if (ctx->pg_record) cudaFreeHost(ctx->pg_record);
+  if (ctx->mc_out_pinned) cudaFreeHost(ctx->mc_out_pinned);
   for (auto ev : ctx->mc_events) cudaEventDestroy(ev);
   for (int k = 0; k < 3; ++k)
     for (auto& sp : ctx->spans[k]) ctx->span_pool.push_back(sp);

@@ -120,6 +120,17 @@ __device__ __forceinline__ void group_pairs_tree_cta(const double* __restrict__ 
   variance = s[1024];
 }
 
+// start of pcb_mcubes_run: uniform grid (init_grid, vegas_grid.py:77-84: k / n_bins), run not stopped, pass scalars armed
+__global__ void run_init_kernel(int nb, double* __restrict__ bounds, int* __restrict__ stop, unsigned long long* __restrict__ scalars) {
+  double* row = bounds + (size_t)blockIdx.x * (nb + 1);
+  for (int k = threadIdx.x; k <= nb; k += blockDim.x) row[k] = (double)k / (double)nb;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *stop = 0x7fffffff;
+    scalars[0] = ~0ULL;   // M_BAD
+    scalars[1] = 0ULL;    // M_CLAMPS
+  }
+}
+
 // transform_many (vegas_grid.py:99-114) for caller-supplied points; flags[0] set on y outside [0,1)
 __global__ void grid_transform_kernel(int d, int nb, const double* __restrict__ bnd, long long n, const double* __restrict__ y,
                                       double* __restrict__ x, double* __restrict__ jac, long long* __restrict__ bins, int* flags) {

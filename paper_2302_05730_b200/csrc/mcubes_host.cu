@@ -447,7 +447,18 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   int* stop_dev = ctx->mc_state.as<int>();
   double* hist_i = reinterpret_cast<double*>(ctx->mc_state.as<char>() + 16);
   double* hist_v = hist_i + iterations;
-  if (contributions_out) PCB_CUDA_TRY(ctx, ctx->mc_tables.ensure((size_t)iterations * tbytes));
+  // per-iteration tables and the final boundaries are staged in pinned host memory: reduce_kernel writes each table
+  // there while the run goes on, so nothing but one small copy is left when it ends
+  const size_t out_bytes = (contributions_out ? (size_t)iterations * tbytes : 0) + bbytes;
+  if (ctx->mc_out_cap < out_bytes) {
+    if (ctx->mc_out_pinned) cudaFreeHost(ctx->mc_out_pinned);
+    ctx->mc_out_pinned = nullptr;
+    ctx->mc_out_cap = 0;
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->mc_out_pinned, out_bytes + out_bytes / 4));
+    ctx->mc_out_cap = out_bytes + out_bytes / 4;
+  }
+  double* out_bounds_host = static_cast<double*>(ctx->mc_out_pinned);
+  double* out_tables_host = out_bounds_host + (size_t)d * (nb + 1);
   if (ctx->mc_records_cap < (size_t)iterations) {
     if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
     ctx->mc_records = nullptr;
@@ -464,18 +475,11 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     ctx->mc_events.push_back(ev);
   }
   const unsigned long long token = ++ctx->mc_run_token;
-  {  // init_grid: k / n_bins on every axis (vegas_grid.py:77-84); stop iteration = "never"
-    double* b = static_cast<double*>(ctx->pinned) + 64;  // 64-KiB staging block, first 512 B hold the scalar slots
-    std::vector<double> big;
-    if ((64 + (size_t)d * (nb + 1)) * sizeof(double) > (1u << 16)) { big.resize((size_t)d * (nb + 1)); b = big.data(); }
-    for (int j = 0; j < d; ++j)
-      for (int k = 0; k <= nb; ++k) b[(size_t)j * (nb + 1) + k] = (double)k / (double)nb;
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, b, bbytes, cudaMemcpyHostToDevice, ctx->stream));
-    static const int never = 0x7fffffff;
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(stop_dev, &never, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    PCB_TRY(arm_pass_scalars(ctx));
-    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  }
+  // init_grid (k / n_bins on every axis, vegas_grid.py:77-84), stop iteration = "never", pass scalars armed: one launch
+  run_init_kernel<<<d, 256, 0, ctx->stream>>>(nb, ctx->mc_bounds[0].as<double>(), stop_dev,
+                                               ctx->scalars.as<unsigned long long>() + kMcSlot);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
   const size_t span_mark[3] = {ctx->spans[0].size(), ctx->spans[1].size(), ctx->spans[2].size()};
   PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[0], ctx->stream));
 
@@ -493,7 +497,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     const int cur = adapt ? (it & 1) : 0;
     tail.bounds_in = ctx->mc_bounds[cur].as<double>();
     tail.bounds_out = ctx->mc_bounds[cur ^ 1].as<double>();
-    tail.contrib_copy = contributions_out ? ctx->mc_tables.as<double>() + (size_t)it * d * nb : nullptr;
+    tail.contrib_copy = contributions_out ? out_tables_host + (size_t)it * d * nb : nullptr;
     tail.hist_i = hist_i;
     tail.hist_v = hist_v;
     tail.rel_tol = rel_tol;
@@ -591,13 +595,13 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[done]));
   if (seconds_device) *seconds_device = ms * 1e-3;
   *n_done = done;
-  if (contributions_out)
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(contributions_out, ctx->mc_tables.p, (size_t)done * tbytes, cudaMemcpyDeviceToHost, ctx->stream));
   if (final_boundaries) {
     const int cur = adapt ? (done & 1) : 0;
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(final_boundaries, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_bounds_host, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    std::memcpy(final_boundaries, out_bounds_host, bbytes);
   }
-  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (contributions_out) std::memcpy(contributions_out, out_tables_host, (size_t)done * tbytes);   // the stream is drained
   return PCB_OK;
 }
 
