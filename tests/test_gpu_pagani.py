@@ -294,12 +294,12 @@ def test_apply_rules_single_region(golden):
 
 # ------------------------------------------------------------------ one-region-per-lane kernel
 @pytest.mark.parametrize("fam", FAMILIES)
-@pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 7, 8, 10])
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12])
 def test_lane_kernel_equals_warp_kernel_bit_for_bit(fam, d, monkeypatch):
     """Long lists run one region per lane, short ones one warp per region (pagani_eval_lanes.cuh vs
     pagani_eval.cuh / pagani_eval_mult.cuh).  The results must not depend on which kernel evaluated
     a region -- otherwise a sharded list would not reproduce the single-GPU tree."""
-    n = {1: 1000, 2: 999, 3: 777, 5: 555, 6: 333, 7: 200, 8: 130, 10: 70}[d]
+    n = {1: 1000, 2: 999, 3: 777, 4: 600, 5: 555, 6: 333, 7: 200, 8: 130, 9: 100, 10: 70, 12: 40}[d]
     lefts, lengths = random_boxes(d, n, 1234 + d)
     regions, rule = pb.RegionList(lefts, lengths), pb.build_rule(d)
     for wrap in (False, True):
