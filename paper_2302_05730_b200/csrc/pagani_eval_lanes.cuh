@@ -25,6 +25,9 @@
 
 #include "pagani_eval_mult.cuh"
 
+#ifndef PCB_LANES_GENERIC_W
+#define PCB_LANES_GENERIC_W 4
+#endif
 #ifndef PCB_LANES_HALVES_REAL
 #define PCB_LANES_HALVES_REAL 1   // 2: real families also split the virtual threads over two warps (measured slower: f4 d=8 0.57 vs 0.41 ms)
 #endif
@@ -463,7 +466,7 @@ struct LaneCorner {
 };
 
 template <int FAM, int D>
-__global__ void __launch_bounds__(32) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
+__global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using L = GenericLaneLayout<D>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -531,7 +534,8 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_generic_kernel(const __g
       }
     }
 
-    constexpr int W = 8;
+    constexpr int W = PCB_LANES_GENERIC_W;
+    constexpr int kLevels = W == 8 ? 3 : 4;   // log2(64 / W)
     double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
     int axis = 0;
     auto split_note = [&](int i, double fx) {   // pagani.py:215-223: running first maximum over the axes
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_generic_kernel(const __g
         }
       }
     };
-    double hold[3][5];
+    double hold[kLevels][5];
     double cur[5];
 #pragma unroll 1
     for (int blk = 0; blk < 64 / W; ++blk) {
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(32) pagani_eval_lanes_generic_kernel(const __g
           for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + acc[v + span][k];
 #pragma unroll
       for (int k = 0; k < 5; ++k) cur[k] = acc[0][k];
-      counter_merge<0, 3>(blk, cur, hold);
+      counter_merge<0, kLevels>(blk, cur, hold);
     }
 
     double v[5];
