@@ -258,8 +258,10 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     //      independent dependency chains (that is what hides the FP64 latency with ~2 warps per scheduler); only
     //      the three blocks that straddle a class boundary take the point-by-point path.  The first log2(W)
     //      levels of the pair tree are fixed-register adds, the remaining ones a binary counter over the blocks.
-    constexpr int W = kHalves > 1 ? 4 : 8;
-    constexpr int kCounterLevels = 3;   // log2(kVt / W): 64 / 8 = 32 / 4
+    // chains per lane: where the tables leave room for >= 10 warps per SM (d <= 6) four chains and more warps win, above
+    // that the eight-chain version hides the latency better (measured: f4 d=5 0.50 -> 0.42 ms, d=6 0.185 -> 0.161, d=8 0.41 vs 0.45)
+    constexpr int W = kHalves > 1 ? 4 : (D <= 6 ? 4 : 8);
+    constexpr int kCounterLevels = (kVt / W) == 8 ? 3 : 4;   // log2(kVt / W)
     double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
     int axis = 0;
     // split axis bookkeeping (pagani.py:215-223) for direct point i: running first maximum over the axes
