@@ -61,7 +61,7 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   size_t lanes_smem = 0;
   int lanes_threads = 32;
   const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem, &lanes_threads) : nullptr;
-  long long lanes_min = 8192;
+  long long lanes_min = 12288;   // measured crossover: one batch of 32 regions per warp takes ~21 us whatever the list length
   size_t lanes_cap = 56u << 10;
   if (const char* env = std::getenv("PCB_PAGANI_LANES_MIN")) {  // test hook: force either kernel
     lanes_min = std::atoll(env);
