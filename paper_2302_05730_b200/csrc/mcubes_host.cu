@@ -447,8 +447,8 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   int* stop_dev = ctx->mc_state.as<int>();
   double* hist_i = reinterpret_cast<double*>(ctx->mc_state.as<char>() + 16);
   double* hist_v = hist_i + iterations;
-  // per-iteration tables and the final boundaries are staged in pinned host memory: reduce_kernel writes each table
-  // there while the run goes on, so nothing but one small copy is left when it ends
+  // per-iteration tables are kept on the device (reduce_kernel writes each one) and leave, with the final boundaries,
+  // through one pinned staging block when the run ends: two DMA copies and one synchronisation
   const size_t out_bytes = (contributions_out ? (size_t)iterations * tbytes : 0) + bbytes;
   if (ctx->mc_out_cap < out_bytes) {
     if (ctx->mc_out_pinned) cudaFreeHost(ctx->mc_out_pinned);
@@ -459,6 +459,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   }
   double* out_bounds_host = static_cast<double*>(ctx->mc_out_pinned);
   double* out_tables_host = out_bounds_host + (size_t)d * (nb + 1);
+  if (contributions_out) PCB_CUDA_TRY(ctx, ctx->mc_tables.ensure((size_t)iterations * tbytes));
   if (ctx->mc_records_cap < (size_t)iterations) {
     if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
     ctx->mc_records = nullptr;
@@ -497,7 +498,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     const int cur = adapt ? (it & 1) : 0;
     tail.bounds_in = ctx->mc_bounds[cur].as<double>();
     tail.bounds_out = ctx->mc_bounds[cur ^ 1].as<double>();
-    tail.contrib_copy = contributions_out ? out_tables_host + (size_t)it * d * nb : nullptr;
+    tail.contrib_copy = contributions_out ? ctx->mc_tables.as<double>() + (size_t)it * d * nb : nullptr;
     tail.hist_i = hist_i;
     tail.hist_v = hist_v;
     tail.rel_tol = rel_tol;
@@ -598,10 +599,12 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   if (final_boundaries) {
     const int cur = adapt ? (done & 1) : 0;
     PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_bounds_host, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
-    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    std::memcpy(final_boundaries, out_bounds_host, bbytes);
   }
-  if (contributions_out) std::memcpy(contributions_out, out_tables_host, (size_t)done * tbytes);   // the stream is drained
+  if (contributions_out)
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_tables_host, ctx->mc_tables.p, (size_t)done * tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (final_boundaries || contributions_out) PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (final_boundaries) std::memcpy(final_boundaries, out_bounds_host, bbytes);
+  if (contributions_out) std::memcpy(contributions_out, out_tables_host, (size_t)done * tbytes);
   return PCB_OK;
 }
 
