@@ -15,8 +15,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJDIR = os.path.join(CSRC, "build")
-LIB = os.path.join(HERE, "libparcube_b200.so")
+OBJDIR = os.path.join(CSRC, os.environ.get("PCB_OBJDIR", "build"))
+LIB = os.path.join(HERE, os.environ.get("PCB_LIB_NAME", "libparcube_b200.so"))
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 N_FAMILIES = 8
 
@@ -26,6 +26,7 @@ NVCC_FLAGS = [
     "-fmad=false",  # numpy's a*b+c is two roundings; fused ops are explicit __fma_rn in the sources
     "-Xcompiler", "-fPIC",
     "-I", INCLUDE,
+    *os.environ.get("PCB_NVCC_EXTRA", "").split(),   # experiments: -DPCB_...=...
 ]
 
 
@@ -55,6 +56,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     """Compile (if stale) and return the path of the shared library."""
     os.makedirs(OBJDIR, exist_ok=True)
     newest = _newest_source()
+    # an up-to-date library needs no objects (csrc/build/ is not shipped to the GPU box)
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
+        return LIB
     nvcc = _nvcc()
     todo, objs = [], []
     for obj, src, extra in _units():

@@ -13,7 +13,7 @@ import threading
 import numpy as np
 
 MAX_DIM = 12
-LIB_NAME = "libparcube_b200.so"
+LIB_NAME = os.environ.get("PCB_LIB_NAME", "libparcube_b200.so")   # PCB_LIB_NAME: A/B builds in experiments
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 PCB_OK, PCB_NONFINITE, PCB_BUDGET, PCB_INVALID, PCB_CUDA = range(5)

@@ -20,6 +20,8 @@
 // fixed order (reduce_kernel), so the table is deterministic.
 #pragma once
 
+#include <type_traits>
+
 #include "pcb_device.cuh"
 
 namespace pcb {
@@ -74,52 +76,47 @@ struct SampleArgs {
   int iteration;
 };
 
-// One sample: draw u per axis, stratify, push through the grid, evaluate (mcubes.py:224-243).
-template <class F, int D, int RNG>
-__device__ __forceinline__ void draw_sample(const SampleArgs& a, const double* s_b, const double (&coord)[D],
-                                            unsigned long long kc, unsigned long long T, unsigned long long ctr,
-                                            unsigned long long inj_base, bool active, int (&bin)[D], double& fx,
-                                            double& v) {
+// One axis of one sample: draw u, stratify, push through the grid (mcubes.py:224-236, vegas_grid.py:99-114).
+template <int RNG>
+__device__ __forceinline__ void draw_axis(const SampleArgs& a, const double* s_b, int j, double coord_j,
+                                          unsigned long long kc, unsigned long long T, unsigned long long ctr,
+                                          unsigned long long inj_base, bool active, double& xj, double& jac, int& bin_j) {
   const int nb = a.nb, nb1 = a.nb + 1;
   const double nbd = (double)nb;
-  double x[D];
-  double jac = 1.0;
-#pragma unroll
-  for (int j = 0; j < D; ++j) {
-    double uu;
-    if constexpr (RNG == PCB_RNG_REFERENCE_HASH) {
-      uu = u53_to_unit(mix64(kc + (unsigned long long)j * kGolden));
-    } else {
-      if (a.rng_kind == PCB_RNG_PHILOX) uu = philox_uniform(a.seed, T, ctr + j);
-      else uu = active ? a.injected[inj_base + j] : 0.5;
-    }
-    const double y = div_by_const(coord[j] + uu, a.gd, a.rg);   // (coord + u) / g
-    const double z = y * nbd;
-    const double zi = __dadd_rz(z, 4503599627370496.0);         // 2^52 + floor(z)
-    int b = __double2loint(zi);
-    b = b < nb ? b : nb - 1;
-    const double frac = z - (zi - 4503599627370496.0);
-    const double lo = s_b[j * nb1 + b];
-    const double wd = s_b[j * nb1 + b + 1] - lo;
-    x[j] = lo + frac * wd;
-    const double jw = nbd * wd;
-    jac = (j == 0) ? jw : jac * jw;
-    bin[j] = b;
+  double uu;
+  if constexpr (RNG == PCB_RNG_REFERENCE_HASH) {
+    uu = u53_to_unit(mix64(kc + (unsigned long long)j * kGolden));
+  } else {
+    if (a.rng_kind == PCB_RNG_PHILOX) uu = philox_uniform(a.seed, T, ctr + j);
+    else uu = active ? a.injected[inj_base + j] : 0.5;
   }
-  fx = eval_at<F, D>(x, a.f);
-  v = fx * jac;
+  const double y = div_by_const(coord_j + uu, a.gd, a.rg);   // (coord + u) / g
+  const double z = y * nbd;
+  const double zi = __dadd_rz(z, 4503599627370496.0);         // 2^52 + floor(z)
+  int b = __double2loint(zi);
+  b = b < nb ? b : nb - 1;
+  const double frac = z - (zi - 4503599627370496.0);
+  const double lo = s_b[j * nb1 + b];
+  const double wd = s_b[j * nb1 + b + 1] - lo;
+  xj = lo + frac * wd;
+  const double jw = nbd * wd;
+  jac = (j == 0) ? jw : jac * jw;
+  bin_j = b;
 }
 
 constexpr int kSampleWarps = 8;  // warps per CTA; two CTAs per SM at 128 registers
+constexpr int kSlot = kSampleWarps * 32;   // records per staged sample slot
 
-// shared memory of one CTA: boundaries, one table row + tag bytes per axis, the staged records of one round
+// shared memory of one CTA: boundaries, one table row + tag bytes per axis, the staged records of TWO rounds
+// (the round being drawn and the round being added to the rows)
+__host__ __device__ inline size_t vsample_stage_bytes(int d) { return (size_t)2 * kSlot * 8 + (size_t)d * 2 * kSlot * 2; }
 __host__ __device__ inline size_t vsample_smem_bytes(int d, int nb) {
   const size_t tags = (size_t)((nb + 15) & ~15);
-  return (size_t)d * (nb + 1) * 8 + 8 /* pad */ + (size_t)d * ((size_t)nb * 8 + tags) + 2 * kSampleWarps * 32 * 8 +
-         (size_t)d * 2 * kSampleWarps * 32 * 2;
+  return (size_t)d * (nb + 1) * 8 + 8 /* pad */ + (size_t)d * ((size_t)nb * 8 + tags) + 2 * vsample_stage_bytes(d);
 }
 
-// Add two staged records per lane into the warp's private row (see the header comment).
+// Add two staged records per lane into the warp's private row (see the header comment).  Straight-line code: the
+// caller interleaves it with the arithmetic of the round being drawn, which hides the shared-memory round trips.
 __device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
                                          double w1, int b1) {
   // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
@@ -129,9 +126,9 @@ __device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned cha
   unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
   // Only lanes that still have an update pending touch shared memory: the table is bound by shared-memory
   // wavefronts, so the second round -- a handful of collision losers -- must not replay the whole warp's loads.
-#pragma unroll 1
+  // 64 records in ~500 bins collide somewhere in 98 % of the calls: the second round is unconditional.
+#pragma unroll
   for (int round = 0; round < 2; ++round) {
-    if (!__any_sync(PCB_FULL_MASK, want)) return;
     if (want & 1u) tags[b0] = (unsigned char)lane;
     if (want & 2u) tags[b1] = (unsigned char)lane;
     __syncwarp();
@@ -151,9 +148,14 @@ __device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned cha
 }
 
 // resident CTAs per SM the register allocation leaves room for: low dimensions need fewer registers and less shared
-// memory, and the accumulation phase (a warp per axis) keeps fewer of their warps busy -- measured per pass of ~9e8
-// samples, 2 vs 3 CTAs: d=5 38.4 vs 27.6 ms, d=6 38.5 vs 33.7 ms, d=7 35.0 vs 36.7 ms, d=8 (does not fit three) 40.4 ms
-__host__ __device__ constexpr int vsample_ctas_per_sm(int d) { return d <= 4 ? 4 : (d <= 6 ? 3 : 2); }
+// memory, and the accumulation (a warp per axis) keeps fewer of their warps busy
+#ifndef PCB_VS_CTAS_LOW
+#define PCB_VS_CTAS_LOW 4
+#endif
+#ifndef PCB_VS_CTAS_MID
+#define PCB_VS_CTAS_MID 3
+#endif
+__host__ __device__ constexpr int vsample_ctas_per_sm(int d) { return d <= 4 ? PCB_VS_CTAS_LOW : (d <= 6 ? PCB_VS_CTAS_MID : 2); }
 
 template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsample_kernel(const __grid_constant__ SampleArgs a) {
@@ -165,35 +167,58 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   double* s_b = reinterpret_cast<double*>(smem_raw);                                   // [D][nb+1]
   double* s_hist = s_b + (((size_t)D * nb1 + 1) & ~(size_t)1);                         // [D][nb]
   unsigned char* s_tag = reinterpret_cast<unsigned char*>(s_hist + (size_t)D * nb);    // [D][tag_bytes]
-  double* s_rw = reinterpret_cast<double*>(s_tag + (size_t)D * tag_bytes);             // [2][kSampleWarps][32]
-  unsigned short* s_rb = reinterpret_cast<unsigned short*>(s_rw + 2 * kSampleWarps * 32);  // [D][2][kSampleWarps][32]
+  // staging buffer q at s_stage + q * stage_bytes: weights [2][kSampleWarps][32], bin ids [D][2][kSampleWarps][32]
+  unsigned char* s_stage = s_tag + (size_t)D * tag_bytes;
+  constexpr size_t kStageBytes = (size_t)2 * kSlot * 8 + (size_t)D * 2 * kSlot * 2;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
   for (int i = threadIdx.x; i < D * nb; i += blockDim.x) s_hist[i] = 0.0;
+  // both staging buffers start as empty records (weight 0, bin 0)
+  for (int i = threadIdx.x; i < (int)(2 * kStageBytes / 8); i += blockDim.x) reinterpret_cast<double*>(s_stage)[i] = 0.0;
   __syncthreads();
 
   const int p = a.p;
   const double pd = (double)p;
   unsigned long long clamp_count = 0;
-  constexpr int kSlot = kSampleWarps * 32;   // records per staged sample slot
-  // stage one sample of this lane: slot 0 or 1 of the round
+  // the round being drawn is staged in `cur`; `prev` holds the records of the round before, which this warp adds to
+  // its row(s) while it draws
+  unsigned char* cur = s_stage;
+  unsigned char* prev = s_stage + kStageBytes;
+  const int my = wib * 32 + lane;
   auto stage = [&](int slot, double w, const int (&bin)[D]) {
-    s_rw[slot * kSlot + wib * 32 + lane] = w;
+    reinterpret_cast<double*>(cur)[slot * kSlot + my] = w;
+    unsigned short* rb = reinterpret_cast<unsigned short*>(cur + 2 * kSlot * 8);
 #pragma unroll
-    for (int j = 0; j < D; ++j) s_rb[(j * 2 + slot) * kSlot + wib * 32 + lane] = (unsigned short)bin[j];
+    for (int j = 0; j < D; ++j) rb[(j * 2 + slot) * kSlot + my] = (unsigned short)bin[j];
   };
-  // all warps: the staged round is complete -> add it to the rows -> staging may be overwritten
-  auto bin_round = [&]() {
-    __syncthreads();
+  // add the records that source warps [w_lo, w_hi) staged in the previous round to the row(s) of this warp
+  auto bin_rows = [&](int w_lo, int w_hi, auto unrolled) {
+    const double* rw = reinterpret_cast<const double*>(prev);
+    const unsigned short* rb = reinterpret_cast<const unsigned short*>(prev + 2 * kSlot * 8);
     for (int j = wib; j < D; j += kSampleWarps) {
       double* hist = s_hist + (size_t)j * nb;
       unsigned char* tags = s_tag + (size_t)j * tag_bytes;
-#pragma unroll 2
-      for (int w = 0; w < kSampleWarps; ++w)
-        bin_pair(hist, tags, lane, s_rw[w * 32 + lane], s_rb[(j * 2) * kSlot + w * 32 + lane], s_rw[kSlot + w * 32 + lane],
-                 s_rb[(j * 2 + 1) * kSlot + w * 32 + lane]);
+      auto one = [&](int w) {
+        bin_pair(hist, tags, lane, rw[w * 32 + lane], rb[(j * 2) * kSlot + w * 32 + lane], rw[kSlot + w * 32 + lane],
+                 rb[(j * 2 + 1) * kSlot + w * 32 + lane]);
+      };
+      if constexpr (decltype(unrolled)::value) {
+#pragma unroll
+        for (int w = w_lo; w < w_hi; ++w) one(w);
+      } else {
+#pragma unroll 1
+        for (int w = w_lo; w < w_hi; ++w) one(w);
+      }
     }
+  };
+  // inside the draw of a sample pair: straight-line, so that the compiler interleaves it with the draw's arithmetic
+  auto bin_from = [&](int w_lo, int w_hi) { bin_rows(w_lo, w_hi, std::true_type{}); };
+  // everything at once, compact code (single-sample rounds: odd p and the generic generators; the last round)
+  auto bin_all = [&]() { bin_rows(0, kSampleWarps, std::false_type{}); };
+  // the round is staged: publish it, and take the other buffer (whose records every warp has consumed) for the next
+  auto end_round = [&]() {
     __syncthreads();
+    unsigned char* t = cur; cur = prev; prev = t;
   };
 
   // the CTA takes kSampleWarps units at a time (one per warp); all units have the same number of rounds
@@ -239,14 +264,21 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
       const unsigned long long inj_cube = (unsigned long long)(c_begin + i) * (unsigned long long)p;
       double s1 = 0.0, s2 = 0.0;
       int k = 0;
-      // two samples at a time: independent dependency chains keep the FP64 and integer pipes busy
+      // two samples at a time: independent dependency chains keep the FP64 and integer pipes busy.  Axis step j of
+      // the draw carries its share of the accumulation of the previous round (source warps j*W/D .. (j+1)*W/D).
       if constexpr (RNG == PCB_RNG_REFERENCE_HASH)
       for (; k + 1 < p; k += 2) {
         int bin[2][D];
-        double fx[2], v[2];
-        draw_sample<F, D, RNG>(a, s_b, coord, kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, bin[0], fx[0], v[0]);
-        draw_sample<F, D, RNG>(a, s_b, coord, kc + (unsigned long long)D * kGolden, (unsigned long long)T, ctr + D,
-                               (inj_cube + k + 1) * D, active, bin[1], fx[1], v[1]);
+        double x[2][D], jac[2] = {1.0, 1.0};
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          draw_axis<RNG>(a, s_b, j, coord[j], kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, x[0][j], jac[0], bin[0][j]);
+          draw_axis<RNG>(a, s_b, j, coord[j], kc + (unsigned long long)D * kGolden, (unsigned long long)T, ctr + D,
+                         (inj_cube + k + 1) * D, active, x[1][j], jac[1], bin[1][j]);
+          bin_from(j * kSampleWarps / D, (j + 1) * kSampleWarps / D);
+        }
+        const double fx[2] = {eval_at<F, D>(x[0], a.f), eval_at<F, D>(x[1], a.f)};
+        const double v[2] = {fx[0] * jac[0], fx[1] * jac[1]};
         kc += 2ULL * D * kGolden;
         ctr += 2 * D;
         if (active && !(isfinite(fx[0]) && isfinite(fx[1])))
@@ -258,12 +290,17 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
         s2 = (k == 0) ? v2[0] + v2[1] : (s2 + v2[0]) + v2[1];
         stage(0, active ? (a.squared_weighted ? v2[0] : fx[0] * fx[0]) : 0.0, bin[0]);
         stage(1, active ? (a.squared_weighted ? v2[1] : fx[1] * fx[1]) : 0.0, bin[1]);
-        bin_round();
+        end_round();
       }
       for (; k < p; ++k) {
         int bin[D];
-        double fx, v;
-        draw_sample<F, D, RNG>(a, s_b, coord, kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, bin, fx, v);
+        double x[D], jac = 1.0;
+        bin_all();
+#pragma unroll
+        for (int j = 0; j < D; ++j)
+          draw_axis<RNG>(a, s_b, j, coord[j], kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, x[j], jac, bin[j]);
+        const double fx = eval_at<F, D>(x, a.f);
+        const double v = fx * jac;
         kc += (unsigned long long)D * kGolden;
         ctr += D;
         if (active && !isfinite(fx)) atomicMin(a.bad, inj_cube + (unsigned long long)k);
@@ -272,7 +309,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
         s2 = (k == 0) ? v2 : s2 + v2;
         stage(0, active ? (a.squared_weighted ? v2 : fx * fx) : 0.0, bin);
         stage(1, 0.0, bin);
-        bin_round();
+        end_round();
       }
       if (active) {
         const double est = s1 / a.den_est;
@@ -296,6 +333,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
       out[1] = sum_var;
     }
   }
+  bin_all();   // the last round's records
   if (clamp_count) atomicAdd(a.clamps, clamp_count);
   __syncthreads();
   double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
