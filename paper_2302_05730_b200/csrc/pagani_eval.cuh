@@ -22,6 +22,11 @@
 
 namespace pcb {
 
+// The lane kernels take the rule whose corner weights alternate with the bit count in exactly one rule, the parity
+// null rule (quadrature.py:199-203); the host sends every other table to the warp-per-region kernels.
+constexpr int kParityRule = 2;
+
+
 struct EvalArgs {
   pcb_integrand f;
   pcb_rule rule;

@@ -23,6 +23,8 @@
 // A non-finite evaluation poisons the sums; only then the points are walked again to find the first one.
 #pragma once
 
+#include <type_traits>
+
 #include "pagani_eval_mult.cuh"
 
 #ifndef PCB_LANES_GENERIC_W
@@ -104,7 +106,9 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   constexpr int kHalves = PCB_LANES_HALVES_REAL > 1 || MF::cplx ? 2 : 1;
   constexpr int kVt = 64 / kHalves;   // virtual threads per half
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, half = threadIdx.x >> 5;   // half h takes virtual threads kVt*h .. kVt*h + kVt - 1
+  // half h takes virtual threads kVt*h .. kVt*h + kVt - 1; read through a shuffle so that the compiler knows it is
+  // warp-uniform and keeps the point bookkeeping that derives from it on the uniform datapath
+  const int lane = threadIdx.x & 31, half = kHalves > 1 ? __shfl_sync(PCB_FULL_MASK, (int)(threadIdx.x >> 5), 0) : 0;
   auto cta_sync = [&]() { if constexpr (kHalves > 1) __syncthreads(); else __syncwarp(); };
   V* tab = reinterpret_cast<V*>(smem_raw) + lane;                                                   // entry e: tab[e * 32]
   double* term = reinterpret_cast<double*>(smem_raw + sizeof(V) * 32 * L::kTab) + lane;             // term[(5j + c) * 32]
@@ -299,9 +303,69 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
         for (int k = 0; k < 5; ++k) acc[v][k] = init;
         head[v] = corner_head((unsigned)(vt0 + v - L::kCorner0) & 63u);
       }
+      // Corner points of a block: bit pattern = b0 + v + 64 * (step offset).  While the W patterns share their bits
+      // above the sixth (no carry inside the block) the tail groups and the sign of the parity rule's weight are the
+      // same for all W chains: one table load and one weight per step.  The chain's own share of the parity sign
+      // (bit count of its low six bits) is applied by keeping its parity-rule sum negated for the duration of the
+      // corner steps -- negation commutes with every rounding, so the sums carry the same bits.
+      // from D = 7 on a chain has several corner steps and the corners have upper bits to share; below, a chain meets
+      // one corner at most and the plain path is faster (measured, d = 5 / 6: 5-20 %)
+      constexpr bool kSharedCorners = D >= 7;
+      const unsigned b0 = (unsigned)(vt0 - L::kCorner0) & 63u;
+      // b0 = kC0 (mod W): in the one block per 64 / W that carries, chains kSplit .. W-1 have upper bits + 1
+      constexpr int kC0 = (int)((64u * 64u - (unsigned)L::kCorner0) % (unsigned)W);
+      const bool carry_free = b0 + W - 1 <= 63u;
+      bool negated = false;
+      // bit v: bit count of (b0 + v) mod 64 is odd (0x6996... is that parity for 0..63, rotated right by b0)
+      const unsigned odd_chains = (unsigned)((0x6996966996696996ULL >> b0) | ((0x6996966996696996ULL << 1) << (63u - b0)));
+      auto flip_parity_sums = [&]() {
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+          const int hi = __double2hiint(acc[v][kParityRule]) ^ (int)((odd_chains << (31 - v)) & 0x80000000u);
+          acc[v][kParityRule] = __hiloint2double(hi, __double2loint(acc[v][kParityRule]));
+        }
+        negated = !negated;
+      };
+      auto corner_step = [&](int lo, auto carries) {
+        constexpr int kSplit = decltype(carries)::value ? W - kC0 : W;
+        constexpr int kTails = L::kGroups > 2 ? L::kGroups - 2 : 1;
+        const unsigned hb = (unsigned)(lo - L::kCorner0) >> 6;
+        V tail[2][kTails];
+        double w_par[2];
+#pragma unroll
+        for (int c = 0; c < (kSplit < W ? 2 : 1); ++c) {
+#pragma unroll
+          for (int g = 2; g < L::kGroups; ++g) tail[c][g - 2] = tab[(L::kGrp + 8 * g + (((hb + c) >> (3 * g - 6)) & 7u)) * 32];
+          w_par[c] = (__popc(hb + c) & 1) ? -rule.weights[kParityRule][4] : rule.weights[kParityRule][4];
+        }
+        double fx[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+          V val = head[v];
+#pragma unroll
+          for (int g = 2; g < L::kGroups; ++g) val = mmul(val, tail[v < kSplit ? 0 : 1][g - 2]);
+          fx[v] = val.re * jac;
+        }
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            acc[v][k] = acc[v][k] + (k == kParityRule ? w_par[v < kSplit ? 0 : 1] : rule.weights[k][4]) * fx[v];
+      };
 #pragma unroll 1
       for (int s = 0; s < L::kSteps; ++s) {
         const int lo = vt0 + 64 * s, hi = lo + W - 1;
+        if (kSharedCorners && lo >= L::kCorner0 && hi < L::kFe) {  // W corner points
+          if (!negated) flip_parity_sums();
+          if constexpr (kC0 != 0) {
+            if (carry_free) corner_step(lo, std::false_type{});
+            else corner_step(lo, std::true_type{});
+          } else {
+            corner_step(lo, std::false_type{});
+          }
+          continue;
+        }
+        if (kSharedCorners && negated) flip_parity_sums();
         if (hi <= 4 * D) {                                         // W centre / axial points
           double fx[W];
 #pragma unroll
@@ -323,7 +387,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
 #pragma unroll
               for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + rule.weights[k][3] * fx[v];
           }
-        } else if (lo >= L::kCorner0 && hi < L::kFe) {             // W corner points
+        } else if (!kSharedCorners && lo >= L::kCorner0 && hi < L::kFe) {   // W corner points, each with its own weights
           double fx[W];
 #pragma unroll
           for (int v = 0; v < W; ++v) fx[v] = corner_value(head[v], (unsigned)(lo + v - L::kCorner0));
@@ -359,6 +423,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
           }
         }
       }
+      if (kSharedCorners && negated) flip_parity_sums();
       // pair tree inside the block: (v, v+1), then (v, v+2), ... always left + right (engine.py:80-84)
 #pragma unroll
       for (int span = 1; span < W; span *= 2)
@@ -448,22 +513,29 @@ struct LaneCorner {
       p0 = s; p1 = 0.0;
     }
   }
-  __device__ __forceinline__ double tail(const double* term, unsigned bits) const {
-    if constexpr (F::combine == kSumNumpy && D >= 8) {
-      const double a6 = at(term, 6, (bits >> 6) & 1u), a7 = at(term, 7, (bits >> 7) & 1u);
-      double s = p0 + (p1 + (a6 + a7));
+  // the terms of the axes above the sixth depend on the upper bits only: shared by the points of a carry-free block
+  static constexpr int kUp = D > LO ? D - LO : 1;
+  __device__ __forceinline__ static void upper(const double* term, unsigned upper_bits, double (&up)[kUp]) {
 #pragma unroll
-      for (int j = 8; j < D; ++j) s = s + at(term, j, (bits >> j) & 1u);
+    for (int j = LO; j < D; ++j) up[j - LO] = at(term, j, (upper_bits >> (j - LO)) & 1u);
+  }
+  __device__ __forceinline__ double tail_up(const double (&up)[kUp]) const {
+    if constexpr (F::combine == kSumNumpy && D >= 8) {
+      double s = p0 + (p1 + (up[0] + up[1]));
+#pragma unroll
+      for (int j = 8; j < D; ++j) s = s + up[j - LO];
       return s;
     } else {
       double s = p0;
 #pragma unroll
-      for (int j = LO; j < D; ++j) {
-        const double t = at(term, j, (bits >> j) & 1u);
-        s = (F::combine == kProdSeq) ? s * t : s + t;
-      }
+      for (int j = LO; j < D; ++j) s = (F::combine == kProdSeq) ? s * up[j - LO] : s + up[j - LO];
       return s;
     }
+  }
+  __device__ __forceinline__ double tail(const double* term, unsigned bits) const {
+    double up[kUp];
+    upper(term, bits >> LO, up);
+    return tail_up(up);
   }
 };
 
@@ -571,9 +643,58 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
         for (int k = 0; k < 5; ++k) acc[v][k] = init;
         head[v].head(term, (unsigned)(vt0 + v - L::kCorner0) & 63u);
       }
+      // corner steps: shared upper terms, one parity-rule weight per step, the chain's own parity carried by its
+      // negated parity-rule sum (see pagani_eval_lanes_kernel)
+      // from D = 7 on a chain has several corner steps and the corners have upper bits to share; below, a chain meets
+      // one corner at most and the plain path is faster (measured, d = 5 / 6: 5-20 %)
+      constexpr bool kSharedCorners = D >= 7;
+      const unsigned b0 = (unsigned)(vt0 - L::kCorner0) & 63u;
+      constexpr int kC0 = (int)((64u * 64u - (unsigned)L::kCorner0) % (unsigned)W);
+      const bool carry_free = b0 + W - 1 <= 63u;
+      bool negated = false;
+      // bit v: bit count of (b0 + v) mod 64 is odd (0x6996... is that parity for 0..63, rotated right by b0)
+      const unsigned odd_chains = (unsigned)((0x6996966996696996ULL >> b0) | ((0x6996966996696996ULL << 1) << (63u - b0)));
+      auto flip_parity_sums = [&]() {
+#pragma unroll
+        for (int v = 0; v < W; ++v) {
+          const int hi = __double2hiint(acc[v][kParityRule]) ^ (int)((odd_chains << (31 - v)) & 0x80000000u);
+          acc[v][kParityRule] = __hiloint2double(hi, __double2loint(acc[v][kParityRule]));
+        }
+        negated = !negated;
+      };
+      auto corner_step = [&](int lo, auto carries) {
+        constexpr int kSplit = decltype(carries)::value ? W - kC0 : W;
+        const unsigned hb = (unsigned)(lo - L::kCorner0) >> 6;
+        double up[2][LaneCorner<F, D>::kUp];
+        double w_par[2];
+#pragma unroll
+        for (int c = 0; c < (kSplit < W ? 2 : 1); ++c) {
+          LaneCorner<F, D>::upper(term, hb + c, up[c]);
+          w_par[c] = (__popc(hb + c) & 1) ? -rule.weights[kParityRule][4] : rule.weights[kParityRule][4];
+        }
+        double fx[W];
+#pragma unroll
+        for (int v = 0; v < W; ++v) fx[v] = F::template finish<D>(head[v].tail_up(up[v < kSplit ? 0 : 1]), args.f) * jac;
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            acc[v][k] = acc[v][k] + (k == kParityRule ? w_par[v < kSplit ? 0 : 1] : rule.weights[k][4]) * fx[v];
+      };
 #pragma unroll 1
       for (int s = 0; s < L::kSteps; ++s) {
         const int lo = vt0 + 64 * s, hi = lo + W - 1;
+        if (kSharedCorners && lo >= L::kCorner0 && hi < L::kFe) {  // W corner points
+          if (!negated) flip_parity_sums();
+          if constexpr (kC0 != 0) {
+            if (carry_free) corner_step(lo, std::false_type{});
+            else corner_step(lo, std::true_type{});
+          } else {
+            corner_step(lo, std::false_type{});
+          }
+          continue;
+        }
+        if (kSharedCorners && negated) flip_parity_sums();
         if (hi < L::kCorner0) {                                    // W centre / axial / pair points
           double fx[W];
           int row[W];
@@ -586,7 +707,7 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
 #pragma unroll
             for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
           }
-        } else if (lo >= L::kCorner0 && hi < L::kFe) {             // W corner points
+        } else if (!kSharedCorners && lo >= L::kCorner0 && hi < L::kFe) {   // W corner points, each with its own weights
           double fx[W];
 #pragma unroll
           for (int v = 0; v < W; ++v)
@@ -619,6 +740,7 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
           }
         }
       }
+      if (kSharedCorners && negated) flip_parity_sums();
 #pragma unroll
       for (int span = 1; span < W; span *= 2)
 #pragma unroll

@@ -68,7 +68,10 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
     lanes_cap = ctx->smem_optin;
   }
   // below ~4 resident warps per SM (52 KB of tables per warp) the lane kernel no longer hides its latency
-  if (lanes_fn && lanes_smem <= lanes_cap && n >= lanes_min) {
+  // the lane kernels hard-wire which rule alternates its corner weights with the bit count (kParityRule)
+  bool parity_ok = true;
+  for (int k = 0; k < 5; ++k) parity_ok = parity_ok && ((rule->corner_parity[k] != 0) == (k == kParityRule));
+  if (lanes_fn && parity_ok && lanes_smem <= lanes_cap && n >= lanes_min) {
     size_t& have = ctx->smem_attr[lanes_fn];
     if (have < lanes_smem) {
       PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(lanes_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lanes_smem));
