@@ -48,17 +48,14 @@ struct LaneLayout {
   static constexpr int kGrp = kRab + (UNIT ? 0 : (kPairs > 0 ? kPairs : 1));  // Grp[g][combo] at kGrp + 8g + combo
   static constexpr int kTab = kGrp + 8 * kGroups;                 // V entries per lane
   static constexpr int kTerm = 5 * D;                             // doubles per lane: term[j][c], c = 0..4
-  // stash: D doubles per lane (second differences at l2) during the point phase; while the tables are built the
-  // same bytes hold the D centre factors phi[j][0]
+  // term[j][c], c = 1..4, is replaced in place by the VALUE of the axial point (j, c) once the tables are complete
+  // (every slot has exactly one reader, the warp that evaluates that point; the centre terms stay)
   static constexpr int kDesc = 4 * (kPairs > 0 ? kPairs : 1);     // unsigned per CTA
   // the two warps of a CTA share the tables of 32 regions and take virtual threads 0..31 and 32..63; the second
-  // warp hands over its five sums and the centre/axial evaluations with index >= 32 (split-axis inputs)
-  static constexpr int kLate = 4 * D + 1 > 32 ? 4 * D + 1 - 32 : 0;
-  static constexpr int kXfer = 5 + kLate;                         // doubles per lane
-  // scratch per lane: the D centre factors while the tables are built, afterwards the split-axis stash (D doubles)
-  // and, with two halves, the hand-over slots
+  // warp hands over its five sums.  Scratch per lane: the D centre factors while the tables are built, afterwards
+  // the hand-over slots
   __host__ __device__ static constexpr size_t scratch_doubles(size_t vsize) {
-    const size_t a = D * vsize / 8, b = D + (HALVES ? kXfer : 0);
+    const size_t a = D * vsize / 8, b = HALVES ? 5 : 0;
     return a > b ? a : b;
   }
   static constexpr size_t smem_bytes(size_t vsize) {
@@ -115,8 +112,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   constexpr size_t kScratchD = L::scratch_doubles(sizeof(V));
   double* scratch = term + 32 * L::kTerm;
   V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * L::kTerm) + lane;   // cen_s[j * 32] (table phase)
-  double* stash = scratch;                                                                          // stash[j * 32] (point phase)
-  double* xfer = scratch + 32 * D;                                                                  // xfer[k * 32]: sums, late evaluations
+  double* xfer = scratch;                                                                           // xfer[k * 32]: the second half's sums
   double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * L::kTerm + 8 * kScratchD));   // [6][8]
   unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                                          // [4 * kPairs]
 
@@ -161,15 +157,27 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     for (int g = 2; g < L::kGroups; ++g) v = mmul(v, tab[(L::kGrp + 8 * g + ((bits >> (3 * g)) & 7u)) * 32]);
     return v.re * jac;
   };
-  auto direct_value = [&](int i) -> double {   // centre / axial points in the reference's association
-    const int q = i - 1;
-    const int a = i == 0 ? -1 : ((q >= 2 * D ? q - 2 * D : q) >> 1);
-    const int cand = i == 0 ? 0 : 1 + (q & 1) + (q >= 2 * D ? 2 : 0);
+  // Centre / axial points keep the reference's own association (they decide the split axis).  Axial point q
+  // (0-based: l2 pairs of axis 0, 1, ..., then the l3 pairs) moves axis q/2 to candidate 1 + (q & 1) [+ 2 for l3].
+  auto axial_slot = [&](int q) -> int {
+    const int a = (q >= 2 * D ? q - 2 * D : q) >> 1;
+    return 5 * a + 1 + (q & 1) + (q >= 2 * D ? 2 : 0);
+  };
+  auto axial_eval = [&](int q) -> double {   // from the term table (before the slot is overwritten)
+    const int slot = axial_slot(q), a = slot / 5;
     double t[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) t[j] = term[(5 * j + (j == a ? cand : 0)) * 32];
+    for (int j = 0; j < D; ++j) t[j] = term[(j == a ? slot : 5 * j) * 32];
     return F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
   };
+  auto centre_eval = [&]() -> double {
+    double t[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) t[j] = term[(5 * j) * 32];
+    return F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
+  };
+  double f_centre = 0.0;
+  auto direct_value = [&](int i) -> double { return i == 0 ? f_centre : term[axial_slot(i - 1) * 32]; };
 
   for (long long batch = blockIdx.x; batch * 32 < args.n; batch += gridDim.x) {
     const long long r = batch * 32 + lane;
@@ -222,6 +230,14 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
       }
     }
     cta_sync();
+    // the 4D + 1 centre / axial evaluations, dealt to the halves point by point; each value replaces the one term
+    // that only its own evaluation reads
+#pragma unroll 2
+    for (int q = half; q < 4 * D; q += kHalves) {
+      const double fx = axial_eval(q);
+      term[axial_slot(q) * 32] = fx;
+    }
+    if (!half) f_centre = centre_eval();
     // Rab[a][b] = (E[0][a] * E[a+1][b]) * E[b+1][D] with E[x][y] = ((1 * c_x) * c_{x+1}) ... * c_{y-1}; half h
     // stores the pairs with a = h (mod 2)
     if constexpr (MF::unit) {
@@ -255,7 +271,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
         pre = mmul(pre, cen[a]);
       }
     }
-    cta_sync();   // tables complete; the centre factors' bytes become the stash
+    cta_sync();   // tables and axial values complete; the centre factors' bytes become the hand-over slots
 
     // ---- rule points.  Virtual threads are taken W at a time (vt = W blk + v).  For a fixed step s the W points
     //      vt + 64 s of a block almost always belong to one orbit class, so the block is straight-line code over W
@@ -266,29 +282,21 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     // that the eight-chain version hides the latency better (measured: f4 d=5 0.50 -> 0.42 ms, d=6 0.185 -> 0.161, d=8 0.41 vs 0.45)
     constexpr int W = kHalves > 1 ? 4 : (D <= 6 ? 4 : 8);
     constexpr int kCounterLevels = (kVt / W) == 8 ? 3 : 4;   // log2(kVt / W)
-    double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
+    // split axis (pagani.py:215-223): first maximum over the axes of the fourth-difference indicator
     int axis = 0;
-    // split axis bookkeeping (pagani.py:215-223) for direct point i: running first maximum over the axes
-    auto split_note = [&](int i, double fx) {
-      if constexpr (D > 1) {
-        if (kHalves > 1 && half) {   // virtual threads 32..63: hand the evaluation to half 0, which keeps the running maximum
-          if constexpr (L::kLate > 0) xfer[(5 + i - 32) * 32] = fx;
-          return;
-        }
-        const int q = i - 1;
-        if (i == 0) two_f0 = 2.0 * fx;
-        else if (!(q & 1)) first_of_pair = fx;
-        else {
-          const double d2 = (first_of_pair + fx) - two_f0;
-          const int a = (q >= 2 * D ? q - 2 * D : q) >> 1;
-          if (q < 2 * D) stash[a * 32] = d2;
-          else {
-            const double ind = fabs(rule.split_weights[0] * stash[a * 32] - rule.split_weights[1] * d2);
-            if (ind > best) { best = ind; axis = a; }
-          }
+    if constexpr (D > 1) {
+      if (!half) {
+        const double two_f0 = 2.0 * f_centre;
+        double best = -1.0;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          const double d2 = (term[(5 * a + 1) * 32] + term[(5 * a + 2) * 32]) - two_f0;
+          const double d3 = (term[(5 * a + 3) * 32] + term[(5 * a + 4) * 32]) - two_f0;
+          const double ind = fabs(rule.split_weights[0] * d2 - rule.split_weights[1] * d3);
+          if (ind > best) { best = ind; axis = a; }
         }
       }
-    };
+    }
     double hold[kCounterLevels][5];
     double cur[5];
 #pragma unroll 1
@@ -372,7 +380,6 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
           for (int v = 0; v < W; ++v) fx[v] = direct_value(lo + v);
 #pragma unroll
           for (int v = 0; v < W; ++v) {
-            split_note(lo + v, fx[v]);
             const double* w = s_w + 8 * (lo + v == 0 ? 0 : (lo + v <= 2 * D ? 1 : 2));
 #pragma unroll
             for (int k = 0; k < 5; ++k) acc[v][k] = acc[v][k] + w[k] * fx[v];
@@ -406,7 +413,6 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
             if (i <= 4 * D) {
               fx = direct_value(i);
               row = i == 0 ? 0 : (i <= 2 * D ? 1 : 2);
-              split_note(i, fx);
             } else if (i < L::kCorner0) {
               fx = L::kPairs > 0 ? pair_value(i) : 0.0;
               row = 3;
@@ -446,10 +452,6 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
       if (!half) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) cur[k] = cur[k] + xfer[k * 32];
-        if constexpr (L::kLate > 0 && D > 1) {
-#pragma unroll 1
-          for (int i = 32; i <= 4 * D; ++i) split_note(i, xfer[(5 + i - 32) * 32]);
-        }
       }
     }
 
