@@ -186,6 +186,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   a.div_segments = make_fastdiv((unsigned long long)n_segments);
   a.div_nseg = make_fastdiv((unsigned long long)L.nseg);
   a.div_g = make_fastdiv((unsigned long long)plan->g);
+  a.g_m32 = (plan->m < (1LL << 32) && plan->g > 1) ? (unsigned)((1ULL << 32) / (unsigned long long)plan->g) : 0u;
   a.nseg = L.nseg;
   a.rng_kind = rng_kind;
   a.seg_len = L.seg_len;

@@ -8,16 +8,18 @@
 // uniform(seed, T, (L*p + k)*d + j), so the sample set is identical to the reference's for any
 // partition of threads over warps, segments or GPUs.
 //
-// The pass is ONE kernel.  A CTA (8 warps, two CTAs per SM) alternates two phases per round:
-//   sample    every warp draws two samples per lane (hash -> stratified y -> grid transform -> f -> per-cube S1, S2,
-//             estimate, variance) and stages one record per sample -- contribution and D bin ids -- in shared memory;
-//   bin       warp w serves axis w (w + 8 for D > 8): it adds the CTA's 512 staged records into ITS private row of
-//             the contribution table (n_bins doubles in shared memory).  Shared-memory FP64 atomicAdd is a CAS loop
-//             on sm_100 (ATOMS.CAST.SPIN), so same-bin lanes are arbitrated by a tag round (winner does a plain
-//             read-modify-write), losers take a second round, triple collisions use the CAS atomic.
-// The sample phase is bound by the FP64 / integer pipes, the bin phase by shared-memory wavefronts; with two CTAs
-// per SM out of phase the two overlap, and no sample record ever travels to HBM.  Rows are merged CTA -> grid in a
-// fixed order (reduce_kernel), so the table is deterministic.
+// The pass is ONE kernel.  A CTA (8 warps) works in rounds, and in every round each warp does two things at once:
+//   draw      two samples per lane (hash -> stratified y -> grid transform -> f -> per-cube S1, S2, estimate,
+//             variance), staged as one record per sample -- contribution and D bin ids -- in shared memory;
+//   bin       warp w serves axis w (w + 8 for D > 8): it adds the records the CTA staged in the PREVIOUS round to
+//             ITS private row of the contribution table (n_bins doubles in shared memory).  Shared-memory FP64
+//             atomicAdd is a CAS loop on sm_100 (ATOMS.CAST.SPIN), so same-bin lanes are arbitrated by a tag round
+//             (winner does a plain read-modify-write), losers take a second round, triple collisions use the CAS
+//             atomic.
+// The staging is double-buffered and the accumulation is dealt over the axis steps of the draw as straight-line
+// code, so the shared-memory round trips of `bin` hide behind the integer / FP64 arithmetic of `draw` inside every
+// warp; one barrier per round.  No sample record ever travels to HBM.  Rows are merged CTA -> grid in a fixed
+// order (reduce_kernel), so the table is deterministic.
 #pragma once
 
 #include <type_traits>
@@ -46,6 +48,15 @@ __device__ __forceinline__ unsigned long long fast_divmod(unsigned long long x, 
   return q;
 }
 
+// the same for 32-bit operands (m = floor(2^32 / d)): sub-cube indices below 2^32 take their base-g digits this way
+__device__ __forceinline__ unsigned fast_divmod32(unsigned x, unsigned d, unsigned m, unsigned& rem) {
+  unsigned q = __umulhi(x, m);
+  unsigned r = x - q * d;
+  while (r >= d) { r -= d; ++q; }
+  rem = r;
+  return q;
+}
+
 struct SampleArgs {
   pcb_integrand f;
   int g, p, nb, squared_weighted;
@@ -59,6 +70,7 @@ struct SampleArgs {
   long long n_segments;         // (t_end - t_begin) * nseg
   unsigned long long seg_mul;   // coprime to n_segments
   FastDiv div_segments, div_nseg, div_g;
+  unsigned g_m32;               // floor(2^32 / g) when m < 2^32 (digits by 32-bit arithmetic), else 0
   int nseg;                     // segments per logical thread
   int rng_kind;
   long long seg_len;
@@ -242,7 +254,15 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
     }
     // sub-cube coordinates (axis 0 most significant, mcubes.py:132-140), kept as doubles
     double coord[D];
-    {
+    if (a.g_m32) {
+      unsigned rem = (unsigned)c_begin;
+#pragma unroll
+      for (int j = D - 1; j >= 0; --j) {
+        unsigned digit;
+        rem = fast_divmod32(rem, (unsigned)a.g, a.g_m32, digit);
+        coord[j] = (double)(int)digit;
+      }
+    } else {
       unsigned long long rem = (unsigned long long)c_begin;
 #pragma unroll
       for (int j = D - 1; j >= 0; --j) {

@@ -16,10 +16,14 @@
 //              two kernels agree bit for bit and a sharded list does not depend on who evaluates it);
 //              term[j][c] for c in 0..4: the generic per-axis terms of the 4D+1 centre/axial points,
 //              which are evaluated in the reference's own association (split-axis inputs).
+//   axial      pre-pass: the 4D+1 centre/axial evaluations (a full transcendental each), dealt point by point
+//              to the warps that share the tables; each value replaces the one term slot only it reads.
+//              Split axis (first maximum of the fourth-difference indicator) from the stored values.
 //   points     virtual thread vt = 0..63 outer, step s inner (point i = vt + 64 s), five partial sums
 //              per virtual thread started from -0.0 (see pagani_eval.cuh), merged by a binary counter
-//              whose add tree is the adjacent-pair tree of engine.tree_sum.
-//   finish     volume scaling, error estimate, split axis (running first-maximum), coalesced stores.
+//              whose add tree is the adjacent-pair tree of engine.tree_sum.  From D = 7 on the corner
+//              points of a block share the table entries and the parity-rule weight of their upper bits.
+//   finish     volume scaling, error estimate, coalesced stores.
 // A non-finite evaluation poisons the sums; only then the points are walked again to find the first one.
 #pragma once
 

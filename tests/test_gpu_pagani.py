@@ -318,6 +318,28 @@ def test_lane_kernel_equals_warp_kernel_bit_for_bit(fam, d, monkeypatch):
             assert np.array_equal(lanes.integrals, i) and np.array_equal(lanes.errors, e) and np.array_equal(lanes.split_axes, k)
 
 
+def test_rule_with_parity_in_another_row_keeps_warp_kernels(monkeypatch):
+    """The lane kernels hard-wire WHICH null rule alternates its corner weights with the bit count (row 2,
+    quadrature.py:199-203).  A caller-supplied table with that rule in another row must still evaluate
+    exactly: the host routes it to the warp-per-region kernels whatever the list length."""
+    d = 8
+    base = pb.build_rule(d)
+    w = np.array(base.weights)
+    w[[2, 3]] = w[[3, 2]]
+    deg, sc = list(base.null_degrees), list(base.null_scales)
+    deg[1], deg[2] = deg[2], deg[1]
+    sc[1], sc[2] = sc[2], sc[1]
+    rule = pb.RuleTable(d, base.f_eval, base.generators, w, base.split_weights, base.axial_indices, deg, sc)
+    lefts, lengths = random_boxes(d, 200, 99)
+    regions = pb.RegionList(lefts, lengths)
+    f = pb.get_integrand("f2", d)
+    i, e, k = po.pagani_evaluate("f2", lefts, lengths, rule_dict(rule))
+    for lanes_min in ("1", str(10**12)):
+        monkeypatch.setenv("PCB_PAGANI_LANES_MIN", lanes_min)
+        est = pb.pagani_kernel(f, regions, rule)
+        assert np.array_equal(est.integrals, i) and np.array_equal(est.errors, e) and np.array_equal(est.split_axes, k)
+
+
 def test_lane_kernel_reports_first_nonfinite(monkeypatch):
     """A non-finite evaluation surfaces exactly as in the warp kernels (pagani.py:206-209)."""
     d = 3
