@@ -73,6 +73,22 @@ def dram_traffic_bytes(workload):
     return (total, "profiles/" + name) if seen == 2 else (None, None)
 
 
+def ncu_pipe_figures(workload):
+    """FP64-pipe and issue-slot utilisation (%) of the dominant kernel from the same committed capture, or {}."""
+    name = TRAFFIC_PROFILE.get(workload)
+    path = os.path.join(ROOT, "profiles", name) if name else None
+    out = {}
+    if path and os.path.exists(path):
+        keys = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_busy_pct",
+                "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_slots_busy_pct"}
+        for line in open(path):
+            line = line.strip()
+            for k, label in keys.items():
+                if line.startswith(k):
+                    out[label] = round(float(line.split("=")[1]), 1)
+    return out
+
+
 def flops_per_eval(w):
     d = w["d"]
     return FORMULA_FLOPS[w["family"]](d) + (2 * d + 10 if w["kind"] == "pagani" else 10 * d + 4)
@@ -334,7 +350,10 @@ def main():
                      "traffic_source": traffic_src, "launches": int(k_launches), "avg_launch_ms": k_ms / max(k_launches, 1),
                      "flops_per_eval": fpe, "evals_per_launch": k_units * evals_per_unit / max(k_launches, 1),
                      "kernel_share_of_step": k_ms * 1e-3 / dev_s if dev_s else None,
-                     "peak_source": "DFMA micro-benchmark run live (MEASURED_PEAKS.json has no FP64 entry; nominal 37 TFLOP/s)"},
+                     "peak_source": "DFMA micro-benchmark run live (MEASURED_PEAKS.json has no FP64 entry; nominal 37 TFLOP/s)",
+                     # `achieved` counts FORMULA flops (exp/cos/div = 1, the integer hash = 0); what the pipes
+                     # executed for them is in the committed ncu capture of the same kernel
+                     "ncu": ncu_pipe_figures(name)},
         "clocks": clocks.summary(),
         "timed_region_s": region_s,
     }
