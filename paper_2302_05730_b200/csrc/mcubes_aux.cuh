@@ -91,6 +91,8 @@ struct ReduceArgs {
   double* group_out;
 };
 __global__ void __launch_bounds__(kReduceThreads) reduce_kernel(const __grid_constant__ ReduceArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   if (a.stop && a.iteration > *a.stop) return;
   extern __shared__ double s_dyn[];  // max(kMergeChunks*33, 2*pow2) doubles
   if ((int)blockIdx.x < a.merge_ctas)
@@ -122,6 +124,7 @@ __device__ __forceinline__ void group_pairs_tree_cta(const double* __restrict__ 
 
 // start of pcb_mcubes_run: uniform grid (init_grid, vegas_grid.py:77-84: k / n_bins), run not stopped, pass scalars armed
 __global__ void run_init_kernel(int nb, double* __restrict__ bounds, int* __restrict__ stop, unsigned long long* __restrict__ scalars) {
+  pdl_launch_dependents();
   double* row = bounds + (size_t)blockIdx.x * (nb + 1);
   for (int k = threadIdx.x; k <= nb; k += blockDim.x) row[k] = (double)k / (double)nb;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -359,6 +362,8 @@ struct FinishArgs {
 __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ FinishArgs a) {
   // kernels of iteration `it` run iff it <= *stop, so the refinement CTAs of the stopping iteration itself are
   // unaffected by the decision taken by the last CTA of this very launch
+  pdl_launch_dependents();
+  pdl_wait();
   if (a.stop && a.iteration > *a.stop) return;
   extern __shared__ double sh[];
   if ((int)blockIdx.x < a.n_refine) {

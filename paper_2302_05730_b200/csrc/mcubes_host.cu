@@ -120,6 +120,10 @@ static pcb_status read_mc_scalars(pcb_ctx* ctx) {
 }
 
 static pcb_status grant_smem(pcb_ctx* ctx, const void* fn, size_t bytes) {
+  // Every kernel of the pass chain asks for the same (maximal) shared-memory carve-out: a launch whose carve-out
+  // differs from its predecessor's makes the SMs drain and reconfigure, and cannot become resident beside it.
+  if (ctx->smem_attr.find(fn) == ctx->smem_attr.end())
+    PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   size_t& have = ctx->smem_attr[fn];  // cudaFuncSetAttribute is not free: once per kernel and size
   if (have < bytes) {
     PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -215,7 +219,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
     const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
     ProfileSpan span(ctx, 1, (double)(c1 - c0) * plan->p, tail.iteration);
     void* args[] = {&a};
-    PCB_CUDA_TRY(ctx, cudaLaunchKernel(fn, dim3(vs_blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
+    PCB_CUDA_TRY(ctx, launch_pdl(fn, dim3(vs_blocks), dim3(kSampleWarps * 32), args, L.smem, ctx->stream));
     ctx->launches++;
   }
 
@@ -239,9 +243,12 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   r.group_out = ctx->mc_group.as<double>();
   const size_t reduce_smem = std::max<size_t>((size_t)kMergeChunks * 33, (size_t)2 * pow2) * sizeof(double);
   PCB_TRY(grant_smem(ctx, (const void*)&reduce_kernel, reduce_smem));
-  reduce_kernel<<<(unsigned)(r.merge_ctas + n_groups), kReduceThreads, reduce_smem, ctx->stream>>>(r);
-  ctx->launches++;
-  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  {
+    void* args[] = {&r};
+    PCB_CUDA_TRY(ctx, launch_pdl((const void*)&reduce_kernel, dim3((unsigned)(r.merge_ctas + n_groups)), dim3(kReduceThreads), args,
+                                 reduce_smem, ctx->stream));
+    ctx->launches++;
+  }
 
   FinishArgs fa;
   fa.n_groups = (int)n_groups;
@@ -272,9 +279,11 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   const size_t finish_smem = std::max<size_t>((size_t)(4 * nb + 4), 2048) * sizeof(double);
   if (finish_smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
   PCB_TRY(grant_smem(ctx, (const void*)&finish_kernel, finish_smem));
-  finish_kernel<<<fa.n_refine + 1, 512, finish_smem, ctx->stream>>>(fa);
-  ctx->launches++;
-  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  {
+    void* args[] = {&fa};
+    PCB_CUDA_TRY(ctx, launch_pdl((const void*)&finish_kernel, dim3(fa.n_refine + 1), dim3(512), args, finish_smem, ctx->stream));
+    ctx->launches++;
+  }
   if (n_groups_out) *n_groups_out = n_groups;
   return PCB_OK;
 }
@@ -478,6 +487,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   }
   const unsigned long long token = ++ctx->mc_run_token;
   // init_grid (k / n_bins on every axis, vegas_grid.py:77-84), stop iteration = "never", pass scalars armed: one launch
+  PCB_TRY(grant_smem(ctx, (const void*)&run_init_kernel, 0));
   run_init_kernel<<<d, 256, 0, ctx->stream>>>(nb, ctx->mc_bounds[0].as<double>(), stop_dev,
                                                ctx->scalars.as<unsigned long long>() + kMcSlot);
   ctx->launches++;
@@ -485,6 +495,12 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   const size_t span_mark[3] = {ctx->spans[0].size(), ctx->spans[1].size(), ctx->spans[2].size()};
   PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[0], ctx->stream));
 
+  // Device time of the run: one event before the first pass and one after the last enqueued kernel.  No event sits
+  // between the kernels of the chain (an event record between two kernels ends their programmatic overlap and is a
+  // stream operation of its own), so the reported time includes the at most one speculative no-op pass behind the
+  // stopping iteration.  PCB_MC_ITER_EVENTS=1 records one event per iteration instead and reports the time up to the
+  // end of the stopping iteration (A/B measurements).
+  static const bool iteration_events = [] { const char* e = std::getenv("PCB_MC_ITER_EVENTS"); return e && std::atoi(e) != 0; }();
   // The loop is device-resident: every kernel of iteration `it` is a no-op once the device has decided to
   // stop at an earlier iteration, so the host enqueues iteration it+1 BEFORE it waits for the record of
   // iteration it -- the device never idles on the host round trip.
@@ -508,7 +524,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     tail.seq = (token << 20) | (unsigned long long)(it + 1);
     const unsigned long long it_seed = derive_seed(seed, (unsigned long long)it);  // mcubes.py:58-60, 359
     PCB_TRY(enqueue_pass(ctx, f, plan, tail.bounds_in, it_seed, rng_kind, nullptr, 1, 0, n_threads, tail, nullptr));
-    PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[it + 1], ctx->stream));
+    if (iteration_events) PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[it + 1], ctx->stream));
     return PCB_OK;
   };
   auto wait_record = [&](int it) -> pcb_status {
@@ -580,6 +596,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     if (rec.stop) break;
   }
   // drain the (at most one) speculative no-op pass before anything is read back or reused
+  if (!iteration_events && st == PCB_OK) st = cudaEventRecord(ctx->mc_events[1], ctx->stream) == cudaSuccess ? PCB_OK : fail(ctx, PCB_CUDA, "mcubes_run: event record failed");
   cudaError_t drain = cudaStreamSynchronize(ctx->stream);
   if (st != PCB_OK) return st;
   PCB_CUDA_TRY(ctx, drain);
@@ -594,7 +611,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     v.resize(keep);
   }
   float ms = 0;
-  PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[done]));
+  PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[iteration_events ? done : 1]));
   if (seconds_device) *seconds_device = ms * 1e-3;
   *n_done = done;
   if (final_boundaries) {

@@ -172,7 +172,7 @@ __host__ __device__ constexpr int vsample_ctas_per_sm(int d) { return d <= 4 ? P
 template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
-  if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
+  pdl_launch_dependents();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb, nb1 = a.nb + 1;
   const size_t tag_bytes = (size_t)((nb + 15) & ~15);
@@ -183,10 +183,14 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   unsigned char* s_stage = s_tag + (size_t)D * tag_bytes;
   constexpr size_t kStageBytes = (size_t)2 * kSlot * 8 + (size_t)D * 2 * kSlot * 2;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
   for (int i = threadIdx.x; i < D * nb; i += blockDim.x) s_hist[i] = 0.0;
   // both staging buffers start as empty records (weight 0, bin 0)
   for (int i = threadIdx.x; i < (int)(2 * kStageBytes / 8); i += blockDim.x) reinterpret_cast<double*>(s_stage)[i] = 0.0;
+  // the CTA is resident and its tables are clear while the previous kernel of the stream (the grid refinement of the
+  // iteration before) is still finishing; its results -- boundaries, stop decision -- are read from here on
+  pdl_wait();
+  if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
+  for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
   __syncthreads();
 
   const int p = a.p;

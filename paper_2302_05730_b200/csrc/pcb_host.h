@@ -6,6 +6,7 @@
 #include <array>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <utility>
@@ -150,6 +151,27 @@ struct ProfileSpan {
     ctx->spans[kind].push_back(span);
   }
 };
+
+// Launch with programmatic stream serialisation (see pdl_wait() in pcb_device.cuh): back-to-back kernels of one
+// stream overlap the launch latency and the prologue of the next with the tail of the previous one.
+// PCB_NO_PDL=1 launches plainly (A/B measurements).
+inline bool pdl_enabled() {
+  static const bool on = [] { const char* e = std::getenv("PCB_NO_PDL"); return !(e && std::atoi(e) != 0); }();
+  return on;
+}
+inline cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
 
 inline long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
 
