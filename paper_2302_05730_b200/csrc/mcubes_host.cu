@@ -148,6 +148,7 @@ struct PassTail {
   double rel_tol = 0.0, abs_tol = 0.0;
   McRecord* record = nullptr;          // pinned
   unsigned long long seq = 0;
+  unsigned long long* timeline = nullptr;  // device; debug
 };
 
 // Enqueue one V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries; nothing
@@ -214,6 +215,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   a.block_hist = ctx->mc_hist.as<double>();
   a.stop = tail.stop;
   a.iteration = tail.iteration;
+  a.timeline = tail.timeline;
   {
     // units of work for the roofline: the samples actually drawn (active lanes)
     const long long c0 = t_begin * plan->s, c1 = std::min<long long>(t_end * plan->s, plan->m);
@@ -241,7 +243,8 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   r.pow2 = pow2;
   r.n_local_threads = nt;
   r.group_out = ctx->mc_group.as<double>();
-  const size_t reduce_smem = std::max<size_t>((size_t)kMergeChunks * 33, (size_t)2 * pow2) * sizeof(double);
+  r.timeline = tail.timeline;
+  const size_t reduce_smem = reduce_smem_bytes(pow2);
   PCB_TRY(grant_smem(ctx, (const void*)&reduce_kernel, reduce_smem));
   {
     void* args[] = {&r};
@@ -276,7 +279,9 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   fa.abs_tol = tail.abs_tol;
   fa.record = tail.record;
   fa.seq = tail.seq;
-  const size_t finish_smem = std::max<size_t>((size_t)(4 * nb + 4), 2048) * sizeof(double);
+  fa.timeline = tail.timeline;
+  fa.refine.phase_tl = (tail.timeline && tail.iteration == 1) ? tail.timeline + 200 : nullptr;
+  const size_t finish_smem = std::max<size_t>(refine_smem_doubles(nb), 2048) * sizeof(double);
   if (finish_smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
   PCB_TRY(grant_smem(ctx, (const void*)&finish_kernel, finish_smem));
   {
@@ -313,7 +318,7 @@ static pcb_status refine_dev(pcb_ctx* ctx, int d, int nb, const double* bounds_d
   RefineArgs r;
   r.d = d; r.n = nb; r.alpha = alpha; r.smoothing = smoothing;
   r.boundaries = bounds_dev; r.contrib = contrib_dev; r.new_boundaries = out_dev;
-  const size_t smem = (size_t)(4 * nb + 4) * sizeof(double);
+  const size_t smem = refine_smem_doubles(nb) * sizeof(double);
   if (smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
   PCB_TRY(grant_smem(ctx, (const void*)&refine_grid_kernel, smem));
   refine_grid_kernel<<<d, 512, smem, ctx->stream>>>(r);
@@ -485,6 +490,13 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     PCB_CUDA_TRY(ctx, cudaEventCreate(&ev));
     ctx->mc_events.push_back(ev);
   }
+  static const bool timeline_on = [] { const char* e = std::getenv("PCB_TIMELINE"); return e && std::atoi(e) != 0; }();
+  unsigned long long* timeline_dev = nullptr;
+  if (timeline_on) {
+    PCB_CUDA_TRY(ctx, ctx->mc_timeline.ensure(256 * sizeof(unsigned long long)));
+    timeline_dev = ctx->mc_timeline.as<unsigned long long>();
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(timeline_dev, 0xFF, 256 * sizeof(unsigned long long), ctx->stream));
+  }
   const unsigned long long token = ++ctx->mc_run_token;
   // init_grid (k / n_bins on every axis, vegas_grid.py:77-84), stop iteration = "never", pass scalars armed: one launch
   PCB_TRY(grant_smem(ctx, (const void*)&run_init_kernel, 0));
@@ -522,6 +534,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     tail.abs_tol = abs_tol > 0 ? abs_tol : 0.0;
     tail.record = records + it;
     tail.seq = (token << 20) | (unsigned long long)(it + 1);
+    tail.timeline = timeline_dev;
     const unsigned long long it_seed = derive_seed(seed, (unsigned long long)it);  // mcubes.py:58-60, 359
     PCB_TRY(enqueue_pass(ctx, f, plan, tail.bounds_in, it_seed, rng_kind, nullptr, 1, 0, n_threads, tail, nullptr));
     if (iteration_events) PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[it + 1], ctx->stream));
@@ -609,6 +622,23 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
       else ctx->span_pool.push_back(v[i]);
     }
     v.resize(keep);
+  }
+  if (timeline_dev) {  // debug: where the time of the run went, microseconds from the first stamp
+    unsigned long long tl[256];
+    PCB_CUDA_TRY(ctx, cudaMemcpy(tl, timeline_dev, sizeof tl, cudaMemcpyDeviceToHost));
+    const char* names[3] = {"vsample", "reduce", "finish"};
+    const unsigned long long t0 = tl[0];
+    auto us = [&](unsigned long long t) { return t == ~0ULL ? -1.0 : (double)(long long)(t - t0) * 1e-3; };
+    for (int it = 0; it < 16 && it <= done; ++it)
+      for (int k = 0; k < 3; ++k) {
+        const unsigned long long* e = tl + (it * 3 + k) * 4;
+        if (e[0] == ~0ULL) continue;
+        std::fprintf(stderr, "timeline it %d %-8s enter %9.3f go %9.3f end %9.3f end2 %9.3f\n", it, names[k], us(e[0]), us(e[1]),
+                     e[2] == ~0ULL ? -1.0 : us(~e[2]), us(e[3]));
+      }
+    for (int k = 0; k < 8; ++k) std::fprintf(stderr, "timeline it 1 refine axis 0 phase %d at %9.3f\n", k, us(tl[200 + k]));
+    std::fprintf(stderr, "timeline it 1 reduce latest CTA entry %9.3f latest return from wait %9.3f\n", us(~tl[220]), us(~tl[221]));
+    for (int k = 0; k < 8; ++k) std::fprintf(stderr, "timeline it 1 reduce %s CTA %s %9.3f\n", k < 2 ? "first merge" : k < 4 ? "last merge" : k < 6 ? "first group" : "last group", k & 1 ? "end  " : "start", us(tl[210 + k]));
   }
   float ms = 0;
   PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[iteration_events ? done : 1]));

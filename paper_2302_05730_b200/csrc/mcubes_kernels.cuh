@@ -86,6 +86,7 @@ struct SampleArgs {
   double* block_hist;           // [gridDim.x][d*nb]: the CTA's rows of the contribution table
   const int* stop;              // iteration at which the run stopped (INT_MAX while running); may be NULL
   int iteration;
+  unsigned long long* timeline; // debug stamps (tl_stamp) or NULL
 };
 
 // One axis of one sample: draw u, stratify, push through the grid (mcubes.py:224-236, vegas_grid.py:99-114).
@@ -173,6 +174,7 @@ template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   pdl_launch_dependents();
+  tl_stamp(a.timeline, a.iteration, 0, 0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb, nb1 = a.nb + 1;
   const size_t tag_bytes = (size_t)((nb + 15) & ~15);
@@ -189,6 +191,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   // the CTA is resident and its tables are clear while the previous kernel of the stream (the grid refinement of the
   // iteration before) is still finishing; its results -- boundaries, stop decision -- are read from here on
   pdl_wait();
+  tl_stamp(a.timeline, a.iteration, 0, 1);
   if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
   __syncthreads();
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   __syncthreads();
   double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
   for (int i = threadIdx.x; i < D * nb; i += blockDim.x) dst[i] = s_hist[i];
+  tl_stamp(a.timeline, a.iteration, 0, 2);
 }
 
 }  // namespace pcb

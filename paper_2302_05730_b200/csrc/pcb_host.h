@@ -81,7 +81,7 @@ struct pcb_ctx {
   std::vector<Span> span_pool;
   pcb::DevBuf mc_bounds[2], mc_hist, mc_contrib, mc_seg, mc_group, mc_tmp, mc_inject;
   // pcb_mcubes_run: device run state (stop iteration, history), per-iteration tables, pinned iteration records
-  pcb::DevBuf mc_state, mc_tables;
+  pcb::DevBuf mc_state, mc_tables, mc_timeline;
   void* mc_out_pinned = nullptr;      // pinned staging of the per-iteration tables and the final boundaries
   size_t mc_out_cap = 0;
   void* mc_records = nullptr;
