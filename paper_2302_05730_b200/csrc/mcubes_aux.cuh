@@ -47,7 +47,27 @@ __device__ __forceinline__ void merge_hist_cta(int cta, const double* __restrict
   const int per = (nblocks + kMergeChunks - 1) / kMergeChunks;
   const int b0 = c * per, b1 = min(nblocks, b0 + per);
   double t = 0.0;
-  if (i < nbins_total && b0 < b1) {
+  if ((nbins_total & 1) == 0) {
+    // Rows are 16-B aligned: a warp fetches its chunk's rows two at a time with 16-byte copies that bypass L1 (lanes
+    // 0-15 one row, lanes 16-31 the next; half the requests of the 8-byte form), kMergeBatch rows in flight, and
+    // then every lane adds its bin over the rows in the same serial order as ever.
+    double* rows = reinterpret_cast<double*>(s_stage) + (size_t)c * kMergeBatch * 32;   // this warp's [kMergeBatch][32]
+    const int cnt = max(b1 - b0, 0), pair = (lane & 15) * 2, sub = lane >> 4;
+    const bool fetch = cta * 32 + pair < nbins_total;
+    for (int base = 0; base < cnt; base += kMergeBatch) {
+      const int nbatch = min(kMergeBatch, cnt - base);
+      for (int k = sub; k < nbatch; k += 2)
+        if (fetch) cp_async16(rows + k * 32 + pair, block_hist + (size_t)(b0 + base + k) * nbins_total + cta * 32 + pair);
+      cp_async_wait_all();
+      __syncwarp();
+      if (i < nbins_total)
+        for (int k = 0; k < nbatch; ++k) {
+          const double v = rows[k * 32 + lane];
+          t = (base + k == 0) ? v : t + v;
+        }
+      __syncwarp();
+    }
+  } else if (i < nbins_total && b0 < b1) {
     // The kernel is bound by the latency of its loads (tables just written by other SMs), not by bandwidth: a thread
     // puts up to kMergeBatch rows of its chunk in flight, waits once and adds them in the same serial order as ever.
     const double* src = block_hist + (size_t)b0 * nbins_total + i;

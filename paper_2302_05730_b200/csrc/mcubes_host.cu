@@ -637,6 +637,9 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
                      e[2] == ~0ULL ? -1.0 : us(~e[2]), us(e[3]));
       }
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, "timeline it 1 refine axis 0 phase %d at %9.3f\n", k, us(tl[200 + k]));
+    for (int k = 0; k < 4; ++k)
+      std::fprintf(stderr, "timeline it 1 vsample %s: earliest CTA %9.3f latest CTA %9.3f\n",
+                   k == 0 ? "tables ready   " : k == 1 ? "units done     " : k == 2 ? "last round added" : "table flushed  ", us(tl[230 + 2 * k]), us(~tl[231 + 2 * k]));
     std::fprintf(stderr, "timeline it 1 reduce latest CTA entry %9.3f latest return from wait %9.3f\n", us(~tl[220]), us(~tl[221]));
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, "timeline it 1 reduce %s CTA %s %9.3f\n", k < 2 ? "first merge" : k < 4 ? "last merge" : k < 6 ? "first group" : "last group", k & 1 ? "end  " : "start", us(tl[210 + k]));
   }

@@ -193,8 +193,26 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   pdl_wait();
   tl_stamp(a.timeline, a.iteration, 0, 1);
   if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
-  for (int i = threadIdx.x; i < D * nb1; i += blockDim.x) s_b[i] = a.boundaries[i];
+  {  // boundaries: 16-byte asynchronous copies, all in flight at once (one round trip instead of one per 256 doubles)
+    const int total = D * nb1, pairs = total >> 1;
+    for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(s_b + 2 * i);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(a.boundaries + 2 * i) : "memory");
+    }
+    if ((total & 1) && threadIdx.x == 0) s_b[total - 1] = a.boundaries[total - 1];
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
+  unsigned long long* ph = (a.timeline && a.iteration == 1) ? a.timeline + 230 : nullptr;   // debug: phases of the pass
+  auto ph_stamp = [&](int k) {
+    if (ph && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMin(ph + 2 * k, t);        // earliest CTA
+      atomicMin(ph + 2 * k + 1, ~t);   // latest CTA
+    }
+  };
+  ph_stamp(0);
 
   const int p = a.p;
   const double pd = (double)p;
@@ -360,11 +378,14 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
       out[1] = sum_var;
     }
   }
+  ph_stamp(1);
   bin_all();   // the last round's records
   if (clamp_count) atomicAdd(a.clamps, clamp_count);
   __syncthreads();
+  ph_stamp(2);
   double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
   for (int i = threadIdx.x; i < D * nb; i += blockDim.x) dst[i] = s_hist[i];
+  ph_stamp(3);
   tl_stamp(a.timeline, a.iteration, 0, 2);
 }
 
