@@ -627,7 +627,8 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     unsigned long long tl[256];
     PCB_CUDA_TRY(ctx, cudaMemcpy(tl, timeline_dev, sizeof tl, cudaMemcpyDeviceToHost));
     const char* names[3] = {"vsample", "reduce", "finish"};
-    const unsigned long long t0 = tl[0];
+    unsigned long long t0 = ~0ULL;   // earliest kernel entry (the pass kernel's own stamps exist in experiment builds only)
+    for (int k = 0; k < 16 * 3; ++k) t0 = std::min(t0, tl[k * 4]);
     auto us = [&](unsigned long long t) { return t == ~0ULL ? -1.0 : (double)(long long)(t - t0) * 1e-3; };
     for (int it = 0; it < 16 && it <= done; ++it)
       for (int k = 0; k < 3; ++k) {
@@ -640,6 +641,8 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     for (int k = 0; k < 4; ++k)
       std::fprintf(stderr, "timeline it 1 vsample %s: earliest CTA %9.3f latest CTA %9.3f\n",
                    k == 0 ? "tables ready   " : k == 1 ? "units done     " : k == 2 ? "last round added" : "table flushed  ", us(tl[230 + 2 * k]), us(~tl[231 + 2 * k]));
+    for (int k = 240; k < 256; ++k)
+      if (tl[k] != ~0ULL) std::fprintf(stderr, "timeline it 1 vsample CTA 0 batch %d %s %9.3f\n", (k - 240) / 4, (k & 3) == 0 ? "start      " : (k & 3) == 1 ? "round 1 end" : (k & 3) == 2 ? "round 2 end" : "round 3 end", us(tl[k]));
     std::fprintf(stderr, "timeline it 1 reduce latest CTA entry %9.3f latest return from wait %9.3f\n", us(~tl[220]), us(~tl[221]));
     for (int k = 0; k < 8; ++k) std::fprintf(stderr, "timeline it 1 reduce %s CTA %s %9.3f\n", k < 2 ? "first merge" : k < 4 ? "last merge" : k < 6 ? "first group" : "last group", k & 1 ? "end  " : "start", us(tl[210 + k]));
   }

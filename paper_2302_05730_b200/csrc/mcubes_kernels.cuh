@@ -174,7 +174,9 @@ template <int FAM, int D, int RNG>
 __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsample_kernel(const __grid_constant__ SampleArgs a) {
   using F = Family<FAM>;
   pdl_launch_dependents();
+#ifdef PCB_TIMELINE_PASS
   tl_stamp(a.timeline, a.iteration, 0, 0);
+#endif
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nb = a.nb, nb1 = a.nb + 1;
   const size_t tag_bytes = (size_t)((nb + 15) & ~15);
@@ -191,7 +193,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   // the CTA is resident and its tables are clear while the previous kernel of the stream (the grid refinement of the
   // iteration before) is still finishing; its results -- boundaries, stop decision -- are read from here on
   pdl_wait();
+#ifdef PCB_TIMELINE_PASS
   tl_stamp(a.timeline, a.iteration, 0, 1);
+#endif
   if (a.stop && a.iteration > *a.stop) return;  // run already converged: a speculatively enqueued pass is a no-op
   {  // boundaries: 16-byte asynchronous copies, all in flight at once (one round trip instead of one per 256 doubles)
     const int total = D * nb1, pairs = total >> 1;
@@ -203,14 +207,18 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
-  unsigned long long* ph = (a.timeline && a.iteration == 1) ? a.timeline + 230 : nullptr;   // debug: phases of the pass
+  // debug: phases of the pass, earliest and latest CTA.  Experiment builds only (PCB_NVCC_EXTRA="-DPCB_TIMELINE_PASS
+  // -DPCB_DEBUG_ROUNDS"): with the stamps compiled in, the d=8 kernel is 850 instructions longer, allocates its
+  // registers differently and the 8.6e8-sample pass takes 39.4 instead of 37.2 ms.
   auto ph_stamp = [&](int k) {
-    if (ph && threadIdx.x == 0) {
+#ifdef PCB_TIMELINE_PASS
+    if (a.timeline && a.iteration == 1 && threadIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMin(ph + 2 * k, t);        // earliest CTA
-      atomicMin(ph + 2 * k + 1, ~t);   // latest CTA
+      atomicMin(a.timeline + 230 + 2 * k, t);        // earliest CTA
+      atomicMin(a.timeline + 231 + 2 * k, ~t);       // latest CTA
     }
+#endif
   };
   ph_stamp(0);
 
@@ -259,7 +267,21 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   };
 
   // the CTA takes kSampleWarps units at a time (one per warp); all units have the same number of rounds
+  // debug (PCB_TIMELINE): CTA 0 of iteration 1 stamps the start of each unit batch and the end of each of its rounds
+  auto round_stamp = [&](long long ub, int slot) {
+#ifdef PCB_DEBUG_ROUNDS   // costs registers in the hot loop: experiment builds only (PCB_NVCC_EXTRA=-DPCB_DEBUG_ROUNDS)
+    if (a.timeline && a.iteration == 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int idx = 240 + (int)(ub / ((long long)gridDim.x * kSampleWarps)) * 4 + slot;
+      if (idx < 256 && slot < 4) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.timeline[idx] = t;
+      }
+    }
+#endif
+  };
   for (long long ub = (long long)blockIdx.x * kSampleWarps; ub < a.n_units; ub += (long long)gridDim.x * kSampleWarps) {
+    round_stamp(ub, 0);
     const long long u = ub + wib;
     const unsigned long long sin = (unsigned long long)u * 32ULL + (unsigned long long)lane;
     const bool live = u < a.n_units && sin < (unsigned long long)a.n_segments;
@@ -336,6 +358,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
         stage(0, active ? (a.squared_weighted ? v2[0] : fx[0] * fx[0]) : 0.0, bin[0]);
         stage(1, active ? (a.squared_weighted ? v2[1] : fx[1] * fx[1]) : 0.0, bin[1]);
         end_round();
+        round_stamp(ub, (int)i * (p >> 1) + (k >> 1) + 1);
       }
       for (; k < p; ++k) {
         int bin[D];
@@ -386,7 +409,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   double* dst = a.block_hist + (size_t)blockIdx.x * D * nb;
   for (int i = threadIdx.x; i < D * nb; i += blockDim.x) dst[i] = s_hist[i];
   ph_stamp(3);
+#ifdef PCB_TIMELINE_PASS
   tl_stamp(a.timeline, a.iteration, 0, 2);
+#endif
 }
 
 }  // namespace pcb

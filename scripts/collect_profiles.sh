@@ -33,3 +33,6 @@ python bench.py > profiles/${R}_bench_config2.json 2> gpurun_out/bench_final.err
 python bench.py --impl reference > profiles/${R}_bench_config2_reference.json 2>> gpurun_out/bench_final.err
 python scripts/sweep.py --out profiles/${R}_sweep_config5 > gpurun_out/sweep.log 2>&1
 ls -la profiles/
+# device timeline of one config-2 run (%globaltimer stamps per kernel and phase; PCB_TIMELINE=1)
+python scripts/timeline_run.py f2 6 1e6 2>&1 | tail -50 > profiles/${R}_timeline_config2.txt
+python scripts/timeline_run.py f3 8 1e9 2>&1 | tail -50 > profiles/${R}_timeline_config4.txt

@@ -237,7 +237,55 @@ def test_refine_grid_against_oracle(alpha, smoothing, nb):
         grid = new
 
 
+@pytest.mark.parametrize("nb", [2, 7, 100, 128, 129, 257, 1000, 4095, 4096, 5000])
+def test_refine_grid_over_pairwise_tree_shapes(nb):
+    """numpy's pairwise sum is a tree whose shape depends on n_bins: one block (<= 128), shallow and deep trees with
+    blocks of unequal size, the largest table the CTA-parallel tree covers (4096) and the recursive form above it."""
+    rng = np.random.default_rng(1000 + nb)
+    d = 2
+    t = vegas.BinContributions(d, nb)
+    t.c[:] = rng.random((d, nb)) ** 6
+    grid = pb.init_grid(d, nb)
+    for _ in range(2):
+        new = pb.refine_grid(grid, t, pb.GridRefineParams(1.5, True))
+        want = po.refine_grid(grid.boundaries, t.c, 1.5, True)
+        assert np.max(np.abs(new.boundaries - want)) <= 1e-12
+        grid = new
+
+
 # ------------------------------------------------------------------ run
+_RUN_SNIPPET = """
+import json, hashlib, sys
+import numpy as np
+import paper_2302_05730_b200 as pb
+from paper_2302_05730_b200 import _native
+plan = pb.make_plan(200000, 5)
+its, tables, bounds, _ = _native.mcubes_run(pb.get_integrand("f4", 5).device_spec(), plan, 500, 6, 3, _native.RNG_REFERENCE_HASH,
+                                            True, 1.5, True, 0.0)
+print(json.dumps({"its": [(float(r.integral).hex(), float(r.variance).hex(), int(r.clamp_events)) for r in its],
+                  "tables": hashlib.sha256(np.ascontiguousarray(tables).tobytes()).hexdigest(),
+                  "bounds": hashlib.sha256(np.ascontiguousarray(bounds).tobytes()).hexdigest()}))
+"""
+
+
+def test_run_launch_modes_agree_bit_for_bit():
+    """Programmatic dependent launches and the placement of the timing events are scheduling only: plain launches
+    (PCB_NO_PDL=1) and one event per iteration (PCB_MC_ITER_EVENTS=1) give the same bits, tables included."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for extra in ({}, {"PCB_NO_PDL": "1"}, {"PCB_MC_ITER_EVENTS": "1"}, {"PCB_NO_PDL": "1", "PCB_MC_ITER_EVENTS": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        res = subprocess.run([sys.executable, "-c", _RUN_SNIPPET], env=env, capture_output=True, text=True, timeout=300)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(json.loads(res.stdout.strip().splitlines()[-1]))
+    assert all(o == outs[0] for o in outs[1:])
+
+
 def test_run_matches_reference_fixtures(golden):
     for run in golden["mcubes"]["runs"]:
         recs = []
