@@ -19,8 +19,8 @@ cap() {  # name kernel-regex skip units unit-name -- target args
     python scripts/ncu_summary.py gpurun_out/${R}_$name.ncu-rep $units $uname; } > profiles/${R}_ncu_$name.txt 2>/dev/null
 }
 cap vsample_config2 vsample 2 32768 warp-sample vsample f2 6 1e6
-cap reduce_config2 reduce_kernel 2 1 launch vsample f2 6 1e6
-cap finish_config2 finish_kernel 2 1 launch vsample f2 6 1e6
+cap reduce_config2 reduce_kernel 5 1 launch run f2 6 1e6
+cap finish_config2 finish_kernel 5 1 launch run f2 6 1e6
 cap vsample_config4 vsample 1 26873856 warp-sample vsample f3 8 1e9
 cap pagani_lanes_f1_d8 pagani_eval 2 390625 region eval f1 8 5
 cap pagani_lanes_f4_d8 pagani_eval 2 390625 region eval f4 8 5

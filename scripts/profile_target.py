@@ -1,4 +1,4 @@
-"""Small fixed workloads for ncu: `python scripts/profile_target.py eval|vsample [family d size]`."""
+"""Small fixed workloads for ncu: `python scripts/profile_target.py eval|vsample|run [family d size]`."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2302_05730_b200 as pb
@@ -13,6 +13,11 @@ if mode == "eval":
     for _ in range(3):
         est = pb.pagani_kernel(pb.get_integrand(fam, d), rl, rule)
     print("regions", rl.n, "sum", pb.tree_sum(est.integrals))
+elif mode == "run":  # the adaptive run: reduce_kernel and finish_kernel as config 2 launches them (d refinement CTAs)
+    n = int(float(sys.argv[4])) if len(sys.argv) > 4 else 10**6
+    for _ in range(2):
+        r = pb.mcubes_run(pb.get_integrand(fam, d), n, d, 15, seed=0, rel_tol=1e-3)
+    print("iterations", len(r.iterations), r.estimate, r.errorest)
 else:
     n = int(float(sys.argv[4])) if len(sys.argv) > 4 else 10**8
     plan = pb.make_plan(n, d)
