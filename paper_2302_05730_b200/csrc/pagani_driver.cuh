@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
   __shared__ double s_emax;
   const int r = threadIdx.x, lane = r & 31, w = r >> 5;
   const bool have = r < a.n;
+  pdl_wait();   // launched behind the evaluate kernel with programmatic serialisation: its results are visible from here
   const double my_i = have ? a.integrals[r] : 0.0, my_e = have ? a.errors[r] : 0.0;
   const double sum_i = tree1024(my_i, s_warp);
   const double sum_e = tree1024(my_e, s_warp);

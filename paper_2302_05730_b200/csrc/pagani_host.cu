@@ -296,11 +296,12 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   unsigned long long* host_u = (unsigned long long*)ctx->pinned;
   PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc, 0, 16 * sizeof(double), ctx->stream));
 
-  auto evaluate = [&](long long count, long long ldim) -> pcb_status {
+  // arm = false: the short-list iteration kernel has already re-armed the non-finite flag on the device
+  auto evaluate = [&](long long count, long long ldim, bool arm = true) -> pcb_status {
     PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)count * sizeof(double)));
     PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)count * sizeof(double)));
     PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)count * sizeof(int32_t)));
-    PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + S_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+    if (arm) PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + S_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
     return evaluate_launch(ctx, f, rule, cfg, count, ldim, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(),
                            ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), sc_u + S_BAD);
   };
@@ -349,9 +350,11 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       sa.bad = sc_u + S_BAD;
       sa.record = srec;
       sa.seq = ++ctx->pg_seq;
-      short_iteration_kernel<<<1, 1024, 0, ctx->stream>>>(sa);
-      ctx->launches++;
-      PCB_CUDA_TRY(ctx, cudaGetLastError());
+      {  // dependent launch: resident behind the evaluate kernel, waits for its results (pdl_wait)
+        void* args[] = {&sa};
+        PCB_CUDA_TRY(ctx, launch_pdl((const void*)&short_iteration_kernel, dim3(1), dim3(1024), args, 0, ctx->stream));
+        ctx->launches++;
+      }
       for (unsigned spin = 0; srec->seq != sa.seq; ++spin) {
         if ((spin & 0xfff) == 0xfff) {
           cudaError_t e = cudaStreamQuery(ctx->stream);
@@ -386,7 +389,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       n = 2 * n_split;
       ld = round_up(n, 32);
       cur = nxt;
-      PCB_TRY(evaluate(n, ld));
+      PCB_TRY(evaluate(n, ld, false));
       continue;
     }
     PCB_TRY(tree_sum_dev(ctx, ctx->est_i.as<double>(), n, sc + S_SUM_I));
