@@ -379,7 +379,6 @@ def main():
             ww = WORKLOADS[other]
             b200_step(ww, pb)
             reps = 3 if other != "config1" else 50
-            ctx.profile_begin()
             t0 = time.perf_counter()
             tot_e = tot_s = 0
             for _ in range(reps):
@@ -387,6 +386,10 @@ def main():
                 tot_e += e
                 tot_s += s
             wall = time.perf_counter() - t0
+            # the event pairs around the dominant kernel in a leg of their own, as for the main workload
+            ctx.profile_begin()
+            for _ in range(reps):
+                b200_step(ww, pb)
             kk = 0 if ww["kind"] == "pagani" else 1
             ms, nl, units = ctx.profile_end(kk)
             epu = F_EVAL[ww["d"]] if ww["kind"] == "pagani" else 1
