@@ -238,6 +238,9 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   };
   // add the records that source warps [w_lo, w_hi) staged in the previous round to the row(s) of this warp
   auto bin_rows = [&](int w_lo, int w_hi, auto unrolled) {
+#ifdef PCB_EXPERIMENT_NO_BIN   // experiment builds: how long is a round without the accumulation (results are wrong)
+    return;
+#endif
     const double* rw = reinterpret_cast<const double*>(prev);
     const unsigned short* rb = reinterpret_cast<const unsigned short*>(prev + 2 * kSlot * 8);
     for (int j = wib; j < D; j += kSampleWarps) {
