@@ -8,8 +8,11 @@ A *step* is one complete run of the workload through the public API:
   config1  PAGANI  f4 d=5 rel_tol 1e-3            refine() to tolerance          (BASELINE configs[0])
   config2  m-Cubes f2 d=6 n=1e6/iteration 1e-3     run() to tolerance (<=15 its)  (configs[1]; default at N=1)
   config3  PAGANI  f1 d=8 rel_tol 1e-6             refine() to the region cap     (configs[2], one GPU)
-  config4  m-Cubes f3 d=8 n=1e9/iteration          4 iterations, sub-cubes sharded over the ranks with
-           NCCL all-gather/all-reduce (configs[3]; default at N>1; 1e-6 itself needs ~1e11 samples)
+  config4  m-Cubes f3 d=8 n=1e9/iteration 1e-6     run() to epsrel 1e-6 (~170 iterations of 8.6e8 samples), sub-cubes
+           sharded over the ranks, NCCL all-gather/all-reduce per iteration (configs[3]; default at N>1)
+  config4_fixed  the same pass, 4 iterations of fixed work (sampler throughput; round-1 figure)
+With --gpus N > 1 and no torchrun environment the script re-executes itself under torch.distributed.run
+with N ranks (one per GPU); it never prints n_gpus = N from fewer than N ranks.
 Units are integrand evaluations: regions_processed * f_eval(d) for PAGANI, m*p per m-Cubes iteration.
 
 `value` is evaluations/s over the CUDA-event time of the K steps (max over ranks); `e2e` is the same
@@ -46,22 +49,36 @@ WORKLOADS = {
                     label="config2: m-Cubes f2 (product peak) d=6 n=1e6/iteration epsrel=1e-3 seed=0, run() to tolerance"),
     "config3": dict(kind="pagani", family="f1", d=8, rel_tol=1e-6,
                     label="config3: PAGANI f1 (oscillatory) d=8 rel_tol=1e-6, refine() to the 2^26 region cap"),
-    "config4": dict(kind="mcubes", family="f3", d=8, n=10**9, rel_tol=None, max_iterations=4, seed=0,
-                    label="config4: m-Cubes f3 (corner peak) d=8 n=1e9/iteration, 4 iterations, sub-cubes sharded"),
+    "config4": dict(kind="mcubes", family="f3", d=8, n=10**9, rel_tol=1e-6, max_iterations=600, seed=0,
+                    label="config4: m-Cubes f3 (corner peak) d=8 n=1e9/iteration epsrel=1e-6 seed=0, run() to tolerance, sub-cubes sharded"),
+    "config4_fixed": dict(kind="mcubes", family="f3", d=8, n=10**9, rel_tol=None, max_iterations=4, seed=0,
+                          label="config4_fixed: m-Cubes f3 (corner peak) d=8 n=1e9/iteration, 4 iterations of fixed work"),
 }
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, from the committed `ncu --set full` capture of
 # the same kernel at the same size (scripts/collect_profiles.sh writes profiles/<round>_ncu_*.txt)
-TRAFFIC_PROFILE = {"config2": "r1_ncu_vsample_config2.txt", "config4": "r1_ncu_vsample_config4.txt",
-                   "config3": "r1_ncu_pagani_lanes_f1_d8.txt", "config1": "r1_ncu_pagani_warp_f4_d5_small.txt"}
+TRAFFIC_PROFILE = {"config2": "ncu_vsample_config2.txt", "config4": "ncu_vsample_config4.txt",
+                   "config4_fixed": "ncu_vsample_config4.txt",
+                   "config3": "ncu_pagani_lanes_f1_d8.txt", "config1": "ncu_pagani_warp_f4_d5_small.txt"}
+PROFILE_ROUNDS = ("r2", "r1")   # newest committed capture wins
+
+
+def _profile_path(workload):
+    name = TRAFFIC_PROFILE.get(workload)
+    if not name:
+        return None, None
+    for rnd in PROFILE_ROUNDS:
+        path = os.path.join(ROOT, "profiles", f"{rnd}_{name}")
+        if os.path.exists(path):
+            return path, f"profiles/{rnd}_{name}"
+    return None, None
 
 
 def dram_traffic_bytes(workload):
     """(bytes per launch, source file) of the dominant kernel, or (None, None) when no capture is committed."""
-    name = TRAFFIC_PROFILE.get(workload)
-    path = os.path.join(ROOT, "profiles", name) if name else None
-    if not path or not os.path.exists(path):
+    path, shown = _profile_path(workload)
+    if not path:
         return None, None
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     total, seen = 0.0, 0
@@ -71,15 +88,14 @@ def dram_traffic_bytes(workload):
             unit = line[line.index("[") + 1:line.index("]")]
             total += float(line.split("=")[1]) * scale.get(unit, 1.0)
             seen += 1
-    return (total, "profiles/" + name) if seen == 2 else (None, None)
+    return (total, shown) if seen == 2 else (None, None)
 
 
 def ncu_pipe_figures(workload):
     """FP64-pipe and issue-slot utilisation (%) of the dominant kernel from the same committed capture, or {}."""
-    name = TRAFFIC_PROFILE.get(workload)
-    path = os.path.join(ROOT, "profiles", name) if name else None
+    path, _ = _profile_path(workload)
     out = {}
-    if path and os.path.exists(path):
+    if path:
         keys = {"sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_busy_pct",
                 "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_slots_busy_pct"}
         for line in open(path):
@@ -150,18 +166,26 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU reference arm
+def reference_rule(d):
+    """The reference's own rule table for dimension d <= 8, from the fixtures oracle/make_golden.py wrote with the
+    unmodified reference (tests/golden/rules.npz + golden.json).  The reference arm imports nothing of the product."""
+    z = np.load(os.path.join(ROOT, "tests", "golden", "rules.npz"))
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as fh:
+        m = json.load(fh)["rules"][str(d)]
+    return dict(generators=z[f"gen{d}"], weights=z[f"w{d}"], axial_indices=z[f"ax{d}"],
+                split_weights=np.array([float.fromhex(v) for v in m["split"]]),
+                null_degrees=tuple(m["null_degrees"]), null_scales=tuple(m["null_scales"]))
+
+
 def oracle_step(w, workers):
     """One step of the workload on the host cores with the numpy restatement of the reference.
     Returns (evaluations, seconds, description)."""
     from oracle import parcube_oracle as po
-    import paper_2302_05730_b200 as pb  # rule tables only (host numpy); no device call
 
     d = w["d"]
+    rd = reference_rule(d) if w["kind"] == "pagani" else None   # input data, loaded outside the timed region
     t0 = time.perf_counter()
     if w["kind"] == "pagani":
-        rule = pb.build_rule(d)
-        rd = dict(generators=rule.generators, weights=rule.weights, axial_indices=rule.axial_indices,
-                  split_weights=rule.split_weights, null_degrees=rule.null_degrees, null_scales=rule.null_scales)
         budget = None if w["family"] == "f4" else 20.0
         out = po.pagani_refine(w["family"], d, rd, rel_tol=w["rel_tol"], workers=workers, time_budget_s=budget)
         evals = out["regions_processed"] * F_EVAL[d]
@@ -199,6 +223,26 @@ def run_reference_arm(args, w, rank):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- launch
+def spawn_ranks(n):
+    """Re-execute this script under torch.distributed.run with n ranks on this node; returns its exit status."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} requested, {have} CUDA device(s) visible; nothing measured"}), flush=True)
+        return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------------------- B200 arm
 def b200_step(w, pb, comm=None):
     """One step through the public API. Returns (evaluations, device_seconds, info, h2d_bytes, d2h_bytes)."""
@@ -215,29 +259,28 @@ def b200_step(w, pb, comm=None):
         info = dict(estimate=res.estimate, errorest=res.errorest, iterations=res.iterations,
                     regions_processed=int(res.regions_processed), reason=res.reason)
         return evals, secs, info, 312 + 352 + 40, 40 * (res.iterations + 1) + 56
+    ctx = _native.context()
     if w["kind"] == "pagani":
-        cfg = pb.PaganiConfig(rel_tol=w["rel_tol"])
-        res, history = _native.pagani_refine(f.device_spec(), pb.rules.orbit_form(pb.build_rule(d)), cfg)
+        # the call a user makes: refine() of the reference's API (rule table built/cached by the package)
+        res = pb.refine(f, pb.PaganiConfig(rel_tol=w["rel_tol"]))
         evals = int(res.regions_processed) * F_EVAL[d]
         info = dict(estimate=res.estimate, errorest=res.errorest, iterations=res.iterations,
-                    regions_processed=int(res.regions_processed), reason=_native.STOP_REASONS[res.reason])
+                    regions_processed=int(res.regions_processed), reason=res.reason)
         # in: integrand + rule + config structs; out: one progress record per iteration + the result struct
-        return evals, res.seconds_device, info, 312 + 352 + 40, 40 * res.n_records + 56
+        return evals, ctx.last_device_seconds, info, 312 + 352 + 40, 40 * len(res.history) + 56
     if comm is not None and comm.world > 1:
         t0 = time.perf_counter()
         res = sharded.mcubes_run_sharded(f, w["n"], d, w["max_iterations"], comm, seed=w["seed"], rel_tol=w["rel_tol"])
         secs = time.perf_counter() - t0
     else:
-        plan = pb.make_plan(w["n"], d)
-        its, contribs, _b, secs = _native.mcubes_run(f.device_spec(), plan, 500, w["max_iterations"], w["seed"],
-                                                     _native.RNG_REFERENCE_HASH, True, 1.5, True,
-                                                     0.0 if w["rel_tol"] is None else w["rel_tol"])
-        hist = [pb.stratified.McubesIterationResult(r.integral, r.variance, None, r.n_samples, r.clamp_events) for r in its]
-        est, err, chi2 = pb.combine_iterations(hist)
-        res = pb.MonteCarloResult(est, err, chi2, hist, plan)
+        # the call a user makes: mcubes_run() of the reference's API (per-iteration contribution tables included)
+        res = pb.mcubes_run(f, w["n"], d, w["max_iterations"], seed=w["seed"], rel_tol=w["rel_tol"])
+        secs = ctx.last_device_seconds
     n_it = len(res.iterations)
     evals = n_it * res.plan.n_actual
-    info = dict(estimate=res.estimate, errorest=res.errorest, iterations=n_it, samples_per_iteration=res.plan.n_actual)
+    info = dict(estimate=res.estimate, errorest=res.errorest, chi2_per_dof=res.chi2_per_dof, iterations=n_it,
+                samples_per_iteration=res.plan.n_actual,
+                rel_error_reached=res.errorest / abs(res.estimate) if res.estimate else None)
     grid_bytes = d * 501 * 8
     return evals, secs, info, 312 + 40 + grid_bytes, n_it * (32 + d * 500 * 8) + grid_bytes
 
@@ -253,19 +296,26 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary-workload measurements")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        # launched plainly with --gpus N: become N ranks, one per GPU (the launch the driver's torchrun line makes)
+        sys.exit(spawn_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launch has {world} rank(s); refusing to report n_gpus={args.gpus}")
     name = args.workload if args.workload != "auto" else ("config2" if args.gpus == 1 else "config4")
     w = WORKLOADS[name]
-    heavy = name in ("config3", "config4")
+    heavy = name in ("config3", "config4", "config4_fixed")
     if args.steps is None:
-        args.steps = 5 if heavy else 200
+        args.steps = (2 if name == "config4" else 5) if heavy else 200
     if args.warmup is None:
         args.warmup = 3 if heavy else 20
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
+        if rank != 0:
+            return                      # under torchrun the other ranks exit 0 without work
         if args.steps > 20:
             args.steps, args.warmup = 5, 1  # each CPU step takes seconds
         run_reference_arm(args, w, rank)
@@ -295,7 +345,10 @@ def main():
             comm.barrier()
             torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
+    t0 = time.perf_counter()
+    cold = b200_step(w, pb, comm)           # first call of the process: allocations, kernel attributes, module load
+    cold_wall_s, cold_dev_s = time.perf_counter() - t0, cold[1]
+    for _ in range(args.warmup - 1):
         b200_step(w, pb, comm)
     sync_all()
     launches0 = ctx.launch_count()
@@ -348,8 +401,13 @@ def main():
         "config": {"workload": w["label"], "l2": "256 MiB buffer written between steps; the path has no HBM-resident input",
                    "device": dev_name, "sms": sms},
         "time_to_epsrel_s": dev_s / args.steps, "result": info,
+        "cold_first_call": {"wall_ms": 1e3 * cold_wall_s, "device_ms": 1e3 * cold_dev_s,
+                            "note": "first call of the process (buffer reservation, kernel attributes, module load); "
+                                    "every later call reuses the context's reserved buffers"},
         "e2e": {"value": evals / wall_s, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": 1e3 * wall_s / args.steps, "api": "refine()/mcubes_run() C-ABI call, host structs in, host records out"},
+                "ms_per_step": 1e3 * wall_s / args.steps,
+                "api": "the package's public refine() / mcubes_run() (reference names and result types), host objects in, "
+                       "host records + per-iteration tables out"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp64",
                      "bound_note": "FP64 vector pipe (DFMA): the path is ~100 flop per HBM byte and is no dense contraction, "
@@ -373,12 +431,14 @@ def main():
 
     if rank == 0 and not args.no_extras and world == 1:
         extras = {}
-        for other in ("config1", "config3", "config4"):
+        for other in ("config1", "config3", "config4_fixed", "config4"):
             if other == name:
                 continue
             ww = WORKLOADS[other]
-            b200_step(ww, pb)
-            reps = 3 if other != "config1" else 50
+            t0 = time.perf_counter()
+            first = b200_step(ww, pb)
+            cold_ms = 1e3 * (time.perf_counter() - t0)
+            reps = {"config1": 50, "config4": 1}.get(other, 3)
             t0 = time.perf_counter()
             tot_e = tot_s = 0
             for _ in range(reps):
@@ -387,15 +447,20 @@ def main():
                 tot_s += s
             wall = time.perf_counter() - t0
             # the event pairs around the dominant kernel in a leg of their own, as for the main workload
-            ctx.profile_begin()
-            for _ in range(reps):
-                b200_step(ww, pb)
-            kk = 0 if ww["kind"] == "pagani" else 1
-            ms, nl, units = ctx.profile_end(kk)
+            # (config4 to tolerance: the leg above is the first call's; one more 6-second run buys nothing)
+            if other == "config4":
+                ms = nl = units = 0
+            else:
+                ctx.profile_begin()
+                for _ in range(reps):
+                    b200_step(ww, pb)
+                kk = 0 if ww["kind"] == "pagani" else 1
+                ms, nl, units = ctx.profile_end(kk)
             epu = F_EVAL[ww["d"]] if ww["kind"] == "pagani" else 1
-            ach = units * epu * flops_per_eval(ww) / (ms * 1e-3) / 1e12
+            ach = units * epu * flops_per_eval(ww) / (ms * 1e-3) / 1e12 if ms else None
             extras[other] = {"workload": ww["label"], "evals_per_s": tot_e / tot_s, "time_to_epsrel_s": tot_s / reps,
-                             "e2e_evals_per_s": tot_e / wall, "roofline_achieved_tflops": ach, "roofline_frac": ach / peak,
+                             "e2e_evals_per_s": tot_e / wall, "e2e_ms": 1e3 * wall / reps, "first_call_wall_ms": cold_ms,
+                             "roofline_achieved_tflops": ach, "roofline_frac": ach / peak if ach else None,
                              "result": inf}
         line["other_workloads"] = extras
 

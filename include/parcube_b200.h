@@ -82,7 +82,8 @@ typedef enum { PCB_ERR_TWO_LEVEL = 0, PCB_ERR_MAX_NULL = 1, PCB_ERR_MAX_PAIRWISE
 typedef struct {
   double rel_tol;
   int32_t max_iterations;
-  int32_t group_size;      /* strided schedule width G, 1..64 (pagani.py:175-192) */
+  int32_t group_size;      /* strided schedule width G >= 1 (pagani.py:175-192); G <= 64 runs one warp per
+                              region, wider schedules a generic kernel (one CTA per region) */
   int64_t region_cap;
   int32_t initial_regions;
   int32_t err_mode;        /* pcb_err_mode */
@@ -141,7 +142,7 @@ typedef struct {
   int32_t group_size;
   int64_t m;
   int64_t s;
-  int32_t n_bins;
+  int32_t n_bins;          /* 2..65535 (the pass stages bin ids as 16-bit values); the reference default is 500 */
   int32_t reserved;
 } pcb_mcubes_plan;
 
@@ -271,6 +272,16 @@ pcb_status pcb_mcubes_sample(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
                              const double* injected_uniforms, int32_t squared_weighted,
                              int64_t thread_begin, int64_t thread_end, pcb_mcubes_iteration* out,
                              double* contributions, double* group_partials, pcb_nonfinite* bad);
+
+/* ---- single sub-cube sampler: replaces mcubes.sample_cube (mcubes.py:143-164) ----------------
+ * The caller draws the p*d uniforms (the reference takes them from a duck-typed `rng.take(p*d)`, reshaped (p, d):
+ * the injection route of SURVEY 0.1) and gets back S1 = tree_sum(v), S2 = tree_sum(v*v) (engine.py:69-86 over the
+ * p values) and the reference's bin_hits as bins (p, d) int64 + weights (p) = v^2.  A non-finite integrand value
+ * returns PCB_NONFINITE with the sample's point and value in `bad`.                                   */
+pcb_status pcb_mcubes_sample_cube(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan,
+                                  const double* boundaries, int64_t cube_index, const double* uniforms /* (p,d) */,
+                                  double* s1, double* s2, int64_t* bins /* (p,d) */, double* weights /* (p) */,
+                                  pcb_nonfinite* bad);
 
 /* ---- grid refinement: replaces refine_grid (vegas_grid.py:142-193) --------------------- */
 pcb_status pcb_grid_refine(pcb_ctx* ctx, int32_t d, int32_t n_bins, const double* boundaries,

@@ -120,6 +120,66 @@ def gen_pagani_eval(out):
     return meta
 
 
+SWEEP_CASES = [("f1", 6, 1e-3), ("f4", 6, 1e-3), ("f5", 6, 1e-3), ("f3", 7, 1e-3), ("f3", 8, 1e-3)]
+
+
+def run_refine_case(fam, d, tol, kw):
+    t0 = time.perf_counter()
+    recs = []
+    res = parcube.refine(parcube.get_integrand(fam, d), parcube.PaganiConfig(rel_tol=tol, **kw),
+                         parcube.ExecConfig(workers=os.cpu_count() or 8), progress=recs.append)
+    rec = dict(family=fam, d=d, rel_tol=tol, cfg=kw, estimate=hexf(res.estimate),
+               errorest=hexf(res.errorest), iterations=res.iterations,
+               regions_processed=res.regions_processed, converged=res.converged,
+               reason=res.reason,
+               history=[[hexf(a), hexf(b), int(c)] for a, b, c in res.history],
+               active=[r["active"] for r in recs],
+               seconds=round(time.perf_counter() - t0, 2))
+    print("refine", fam, d, tol, kw, res.iterations, res.regions_processed, res.reason, rec["seconds"], flush=True)
+    return rec
+
+
+def gen_sweep(out):
+    """BASELINE config 5: the PAGANI cases of the f1..f6 x d=5..8 sweep at rel_tol 1e-3 that the reference converges
+    on within ~100 s of CPU and that gen_pagani_refine does not already hold.  Written to
+    a file of their own (tests/golden/sweep_refine.json) so the minutes-long cases regenerate independently."""
+    recs = [run_refine_case(fam, d, tol, {}) for fam, d, tol in SWEEP_CASES]
+    with open(os.path.join(out, "sweep_refine.json"), "w") as fh:
+        json.dump(dict(generator="oracle/make_golden.py --sweep", reference="parcube 0.1.0 (/root/reference/pkg)",
+                       numpy=np.__version__, cases=recs), fh, indent=1)
+
+
+def gen_sample_cube(out):
+    """mcubes.sample_cube (mcubes.py:143-164) on a few sub-cubes, with an RngStream and with a table-backed
+    duck-typed rng (the injection route of SURVEY 0.1); written to tests/golden/sample_cube.json."""
+    class TableRng:
+        def __init__(self, table):
+            self.table, self.pos = table, 0
+
+        def take(self, n):
+            out = self.table[self.pos:self.pos + n]
+            self.pos += n
+            return out
+
+    recs = []
+    for fam, d, n, cube, kind in (("f2", 4, 20000, 0, "stream"), ("f3", 5, 100000, 1234, "stream"),
+                                  ("f4", 3, 2000, 999, "table"), ("sum", 2, 200, 17, "table"),
+                                  ("f5", 8, 10**5, 255, "stream")):
+        plan = parcube.make_plan(n, d)
+        grid = parcube.init_grid(d)
+        if kind == "stream":
+            rng = parcube.RngStream(77, cube // plan.s, (cube % plan.s) * plan.p * d)
+            u = parcube.RngStream(77, cube // plan.s, (cube % plan.s) * plan.p * d).take(plan.p * d)
+        else:
+            u = np.random.default_rng(cube).random(plan.p * d)
+            rng = TableRng(u)
+        s1, s2, hits = ref_mc.sample_cube(parcube.get_integrand(fam, d), cube, plan, grid, rng)
+        recs.append(dict(family=fam, d=d, n=n, cube=cube, kind=kind, uniforms=[hexf(v) for v in u], s1=hexf(s1), s2=hexf(s2),
+                         bins=[[int(b) for b in h[0]] for h in hits], weights=[hexf(h[1]) for h in hits]))
+    with open(os.path.join(out, "sample_cube.json"), "w") as fh:
+        json.dump(dict(generator="oracle/make_golden.py --cube", numpy=np.__version__, cases=recs), fh, indent=1)
+
+
 def gen_pagani_refine(slow):
     cases = [("f4", 5, 1e-3, {}), ("f1", 5, 1e-3, {}), ("f2", 5, 1e-3, {}), ("f3", 5, 1e-3, {}),
              ("f5", 5, 1e-3, {}), ("f6", 5, 1e-3, dict(max_iterations=8)),
@@ -225,8 +285,16 @@ def gen_mcubes(out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true", help="also run the minutes-long refine cases")
+    ap.add_argument("--cube", action="store_true", help="only (re)generate tests/golden/sample_cube.json")
+    ap.add_argument("--sweep", action="store_true", help="only (re)generate tests/golden/sweep_refine.json (config 5)")
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
+    if args.sweep:
+        gen_sweep(OUT)
+        return
+    if args.cube:
+        gen_sample_cube(OUT)
+        return
     meta = dict(generator="oracle/make_golden.py", reference="parcube 0.1.0 (/root/reference/pkg)",
                 numpy=np.__version__, blas=str(np.show_config(mode="dicts")["Build Dependencies"]["blas"].get("version")),
                 cpu_features=str(np.show_config(mode="dicts").get("SIMD Extensions", {}).get("found")))

@@ -374,6 +374,23 @@ def vsample_group(family, plan, boundaries, seed, gid, squared_weighted=True, bo
     return gi, ge, c, clamps, cubes.size
 
 
+def sample_cube(family, cube_index, plan, boundaries, uniforms, bounds=None):
+    """mcubes.sample_cube (mcubes.py:143-164) with the p*d uniforms already taken from the stream:
+    returns (S1, S2, bins (p,d), v*v (p))."""
+    d, g, p = plan["d"], plan["g"], plan["p"]
+    coords = cube_coords([cube_index], g, d)[0]
+    u = np.asarray(uniforms, dtype=np.float64).reshape(p, d)
+    y = (coords + u) / g
+    x, jac, bins = grid_transform(y, boundaries)
+    fx = np.asarray(genz_eval(family, d, x, bounds), dtype=np.float64)
+    bad = ~np.isfinite(fx)
+    if bad.any():
+        i = int(np.argmax(bad))
+        raise NonFinite(x[i], float(fx[i]), int(cube_index))
+    v = fx * jac
+    return float(tree_sum(v)), float(tree_sum(v * v)), bins, v * v
+
+
 def vsample(family, plan, boundaries, seed=0, workers=1, squared_weighted=True, bounds=None,
             uniform_fn=None, groups=None):
     """mcubes_kernel (mcubes.py:268-308), deterministic mode. `groups` restricts the pass

@@ -133,6 +133,8 @@ SIGNATURES = {
     "pcb_mcubes_sample": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_void_p, C.c_uint64,
                                     C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(McubesIterationC),
                                     C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_mcubes_sample_cube": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_void_p, C.c_int64,
+                                         C.c_void_p, _DP, _DP, C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
     "pcb_grid_refine": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                                   C.c_void_p]),
     "pcb_mcubes_run": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_int32, C.c_uint64,
@@ -184,6 +186,9 @@ class Context:
             raise NativeError(f"cannot create a B200 context on device {device}: {msg} (no CPU fallback exists)")
         self.device = int(device)
         self.call_lock = threading.Lock()
+        # CUDA-event time of the most recent refine / mcubes_run on this context (reporting only: the public API
+        # returns the reference's result types, which have no field for it)
+        self.last_device_seconds = 0.0
 
     def last_error(self) -> str:
         if not self.handle:
@@ -383,6 +388,7 @@ def pagani_refine(spec: DeviceSpec, orbit, cfg, progress=None, device=None):
         if failure:
             raise failure[0]
         ctx.check(st, bad, spec.d)
+        ctx.last_device_seconds = float(res.seconds_device)
     history = [(records[i].estimate, records[i].errorest, int(records[i].n_regions)) for i in range(res.n_records)]
     return res, history
 
@@ -420,6 +426,21 @@ def mcubes_sample(spec: DeviceSpec, plan, boundaries: np.ndarray, seed: int, rng
                                        C.byref(bad))
         ctx.check(st, bad, d)
     return it, contrib, partials
+
+
+def mcubes_sample_cube(spec: DeviceSpec, plan, boundaries: np.ndarray, cube_index: int, uniforms: np.ndarray, device=None):
+    """(S1, S2, bins (p,d) int64, weights (p)) of one sub-cube from caller-drawn uniforms (mcubes.py:143-164)."""
+    ctx = context(device)
+    d, nb = boundaries.shape[0], boundaries.shape[1] - 1
+    b, u = _f64(boundaries), _f64(uniforms, (plan.p, d))
+    fc, pc, bad = spec.to_c(), plan_to_c(plan, nb), NonFiniteC()
+    s1, s2 = C.c_double(), C.c_double()
+    bins, weights = np.empty((plan.p, d), dtype=np.int64), np.empty(plan.p)
+    with ctx.call_lock:
+        st = ctx.lib.pcb_mcubes_sample_cube(ctx.handle, C.byref(fc), C.byref(pc), _ptr(b), int(cube_index), _ptr(u),
+                                            C.byref(s1), C.byref(s2), _ptr(bins), _ptr(weights), C.byref(bad))
+        ctx.check(st, bad, d)
+    return s1.value, s2.value, bins, weights
 
 
 def grid_refine(boundaries: np.ndarray, contributions: np.ndarray, alpha: float, smoothing: bool, device=None):
@@ -465,6 +486,7 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
         if failure:
             raise failure[0]
         ctx.check(st, bad, d)
+        ctx.last_device_seconds = float(seconds.value)
     done = n_done.value
     return [its[i] for i in range(done)], (None if contribs is None else contribs[:done]), final_b, seconds.value
 

@@ -10,6 +10,7 @@ namespace pcb {
 
 #define PCB_DECL(F, _) \
   const void* eval_kernel_fam##F(int d); \
+  const void* eval_wide_kernel_fam##F(int d); \
   const void* points_kernel_fam##F(int d); \
   const void* invoke_kernel_fam##F(int d); \
   const void* lanes_kernel_fam##F(int d, size_t* smem, int* threads); \
@@ -19,6 +20,8 @@ PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5
 
 static const kernel_getter kEval[PCB_N_FAMILIES] = {eval_kernel_fam0, eval_kernel_fam1, eval_kernel_fam2, eval_kernel_fam3,
                                                     eval_kernel_fam4, eval_kernel_fam5, eval_kernel_fam6, eval_kernel_fam7};
+static const kernel_getter kEvalWide[PCB_N_FAMILIES] = {eval_wide_kernel_fam0, eval_wide_kernel_fam1, eval_wide_kernel_fam2, eval_wide_kernel_fam3,
+                                                        eval_wide_kernel_fam4, eval_wide_kernel_fam5, eval_wide_kernel_fam6, eval_wide_kernel_fam7};
 static const kernel_getter kPoints[PCB_N_FAMILIES] = {points_kernel_fam0, points_kernel_fam1, points_kernel_fam2, points_kernel_fam3,
                                                       points_kernel_fam4, points_kernel_fam5, points_kernel_fam6, points_kernel_fam7};
 typedef const void* (*sample_getter)(int d, int rng);
@@ -32,6 +35,7 @@ static const lanes_getter kLanes[PCB_N_FAMILIES] = {lanes_kernel_fam0, lanes_ker
                                                     lanes_kernel_fam4, lanes_kernel_fam5, lanes_kernel_fam6, lanes_kernel_fam7};
 const void* eval_lanes_kernel(int family, int d, size_t* smem, int* threads) { return kLanes[family](d, smem, threads); }
 const void* eval_kernel(int family, int d) { return kEval[family](d); }
+const void* eval_wide_kernel(int family, int d) { return kEvalWide[family](d); }
 const void* points_kernel(int family, int d) { return kPoints[family](d); }
 const void* vsample_kernel_ptr(int family, int d, int rng) { return kSample[family](d, rng); }
 

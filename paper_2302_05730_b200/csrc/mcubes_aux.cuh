@@ -251,6 +251,46 @@ __global__ void grid_transform_kernel(int d, int nb, const double* __restrict__ 
   }
 }
 
+// sample_cube (mcubes.py:143-164), points: sample k of one sub-cube from caller-drawn uniforms u[k][j] --
+// y = (coord + u) / g (IEEE division, mcubes.py:152), then transform_many.  One thread per sample.
+__global__ void cube_points_kernel(int d, int nb, int p, long long cube, int g, const double* __restrict__ bnd,
+                                   const double* __restrict__ u, double* __restrict__ x, double* __restrict__ jac,
+                                   long long* __restrict__ bins) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  int coord[PCB_MAX_DIM];
+  long long rem = cube;
+  for (int j = d - 1; j >= 0; --j) { coord[j] = (int)(rem % g); rem /= g; }   // axis 0 most significant (mcubes.py:132-140)
+  double jj = 1.0;
+  for (int j = 0; j < d; ++j) {
+    const double yy = __ddiv_rn((double)coord[j] + u[k * d + j], (double)g);
+    const double z = yy * (double)nb;
+    const double zi = __dadd_rz(z, 4503599627370496.0);
+    int b = __double2loint(zi);
+    b = b < nb ? b : nb - 1;
+    const double frac = z - (zi - 4503599627370496.0);
+    const double lo = bnd[j * (nb + 1) + b];
+    const double w = bnd[j * (nb + 1) + b + 1] - lo;
+    x[k * d + j] = lo + frac * w;
+    const double jw = (double)nb * w;
+    jj = (j == 0) ? jw : jj * jw;
+    bins[k * d + j] = b;
+  }
+  jac[k] = jj;
+}
+
+// sample_cube, values: v = f(x) * jac, v^2, and the first non-finite sample (mcubes.py:154-162)
+__global__ void cube_values_kernel(int p, const double* __restrict__ fx, const double* __restrict__ jac, double* __restrict__ v,
+                                   double* __restrict__ v2, int* first_bad) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= p) return;
+  const double f = fx[k];
+  if (!isfinite(f)) atomicMin(first_bad, k);
+  const double vv = f * jac[k];
+  v[k] = vv;
+  v2[k] = vv * vv;
+}
+
 __global__ void debug_divide_kernel(long long n, const double* __restrict__ x, double g, double rg, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] = div_by_const(x[i], g, rg);

@@ -427,6 +427,72 @@ pcb_status pcb_grid_transform(pcb_ctx* ctx, int32_t d, int32_t n_bins, const dou
   return PCB_OK;
 }
 
+pcb_status pcb_mcubes_sample_cube(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, const double* boundaries,
+                                  int64_t cube_index, const double* uniforms, double* s1, double* s2, int64_t* bins,
+                                  double* weights, pcb_nonfinite* bad) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_plan(ctx, f, plan));
+  if (!boundaries || !uniforms || !s1 || !s2 || !bins || !weights) return fail(ctx, PCB_INVALID, "sample_cube: NULL buffer");
+  if (cube_index < 0 || cube_index >= plan->m) return fail(ctx, PCB_INVALID, "cube index %lld out of range [0, %lld)", (long long)cube_index, (long long)plan->m);
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = plan->d, nb = plan->n_bins, p = plan->p;
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  // scratch: u[p*d] x[p*d] bins[p*d] jac[p] fx[p] v[p] v2[p] sums[2] flag
+  PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure(((size_t)3 * p * d + (size_t)4 * p + 4) * sizeof(double)));
+  double* u_dev = ctx->mc_tmp.as<double>();
+  double* x_dev = u_dev + (size_t)p * d;
+  long long* b_dev = reinterpret_cast<long long*>(x_dev + (size_t)p * d);
+  double* jac_dev = reinterpret_cast<double*>(b_dev + (size_t)p * d);
+  double* fx_dev = jac_dev + p;
+  double* v_dev = fx_dev + p;
+  double* v2_dev = v_dev + p;
+  double* sums_dev = v2_dev + p;
+  int* flag_dev = reinterpret_cast<int*>(sums_dev + 2);
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(flag_dev, 0x7F, sizeof(int), ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_bounds[0].p, boundaries, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(u_dev, uniforms, (size_t)p * d * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  const unsigned blocks = (unsigned)((p + 127) / 128);
+  cube_points_kernel<<<blocks, 128, 0, ctx->stream>>>(d, nb, p, (long long)cube_index, plan->g, ctx->mc_bounds[0].as<double>(), u_dev,
+                                                      x_dev, jac_dev, b_dev);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  {
+    long long nn = p;
+    pcb_integrand fv = *f;
+    const double* pts = x_dev;
+    void* args[] = {&fv, &nn, &pts, &fx_dev};
+    PCB_CUDA_TRY(ctx, cudaLaunchKernel(points_kernel(f->family, d), dim3(blocks), dim3(256), args, 0, ctx->stream));
+    ctx->launches++;
+  }
+  cube_values_kernel<<<blocks, 128, 0, ctx->stream>>>(p, fx_dev, jac_dev, v_dev, v2_dev, flag_dev);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  PCB_TRY(tree_sum_dev(ctx, v_dev, p, sums_dev));        // S1, S2: engine.tree_sum over the p values (mcubes.py:160-161)
+  PCB_TRY(tree_sum_dev(ctx, v2_dev, p, sums_dev + 1));
+  double sums[2];
+  int flag = 0;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(sums, sums_dev, sizeof sums, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(&flag, flag_dev, sizeof flag, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(bins, b_dev, (size_t)p * d * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(weights, v2_dev, (size_t)p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (flag >= 0 && flag < p) {   // first non-finite sample: NonFiniteEvaluationError(x[i], fx[i]) (mcubes.py:156-158)
+    if (bad) {
+      bad->region_index = cube_index;
+      bad->point_index = flag;
+      std::memset(bad->point, 0, sizeof bad->point);
+      PCB_CUDA_TRY(ctx, cudaMemcpy(bad->point, x_dev + (size_t)flag * d, (size_t)d * sizeof(double), cudaMemcpyDeviceToHost));
+      PCB_CUDA_TRY(ctx, cudaMemcpy(&bad->value, fx_dev + flag, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return fail(ctx, PCB_NONFINITE, "non-finite integrand value in sub-cube %lld (sample %d)", (long long)cube_index, flag);
+  }
+  *s1 = sums[0];
+  *s2 = sums[1];
+  return PCB_OK;
+}
+
 pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g, double* out) {
   if (!ctx || n < 0 || g < 1 || (n > 0 && (!x || !out))) return fail(ctx, PCB_INVALID, "debug_divide: bad arguments");
   if (n == 0) return PCB_OK;

@@ -209,7 +209,11 @@ struct CornerCombine {
   }
 };
 
-template <int FAM, int D>
+// WIDE = true: schedule widths G > 64 (pagani.py:56,66 accept any G >= 1).  The warp walks the virtual threads in
+// blocks of 64; a block's 64-leaf pair tree is the butterfly above, and the block sums are merged by a binary
+// counter -- complete aligned subtrees of 64 * 2^h leaves -- which is engine.tree_sum's adjacent-pair tree over
+// the G partials (zero leaves beyond the last virtual thread that owns a point: x + 0.0 == x).
+template <int FAM, int D, bool WIDE = false>
 __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   constexpr int kStore = 4 * D + 1;            // f(centre), f(+-l2 e_j), f(+-l3 e_j): split-axis inputs
@@ -222,6 +226,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
   __shared__ __align__(16) double s_w[6][8];   // orbit weights (+pad); rows 4/5 = corners with even/odd bit count
   __shared__ double s_off[8];
   __shared__ unsigned long long s_code[kCorner0][kWords];  // byte j: candidate byte offset on axis j; bits 6-7 of byte 0: orbit
+  __shared__ double s_lvl[WIDE ? kEvalWarps : 1][WIDE ? 8 : 1][5];   // WIDE: the binary counter of block sums
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const pcb_rule& rule = args.rule;
@@ -295,65 +300,98 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __gr
     //         without points keeps the +0.0 of the reference's zero padding.
     double acc[2][5];
     unsigned badpt = 0xffffffffu;
-#pragma unroll
-    for (int set = 0; set < 2; ++set) {
-      const int vt = lane + 32 * set;
-      const double init = (vt < G && vt < fe) ? -0.0 : 0.0;
-#pragma unroll
-      for (int k = 0; k < 5; ++k) acc[set][k] = init;
-      if (vt >= G) continue;
-      int i = vt;
-      // centre, axial and pair points
-      for (; i < kCorner0; i += G) {
-        unsigned long long code[kWords];
-#pragma unroll
-        for (int q = 0; q < kWords; ++q) code[q] = s_code[i][q];
-        const int orbit = (int)((unsigned)code[0] >> 6) & 3;
-        code[0] &= ~0xC0ULL;
-        double t[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const unsigned half = (unsigned)(code[j >> 3] >> (32 * ((j >> 2) & 1)));
-          t[j] = term_at<D>(term_b, j, __byte_perm(half, 0, 0x4440 + (j & 3)));
-        }
-        const double fx = F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
-        if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
-        if (i < kStore) store[i] = fx;
-        const double* w = s_w[orbit];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
-      }
-      // corner points: bit j of (i - kCorner0) set => abscissa candidate 6 (minus), else 5 (plus)
-      if (G == 64) {
-        CornerCombine<F, D, kLo> cc;
-        if (i < fe) cc.head(term_b, (unsigned)(i - kCorner0));
-        for (; i < fe; i += 64) {
-          const unsigned bits = (unsigned)(i - kCorner0);
-          const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
+    // the (up to) 64 virtual threads vt0 .. vt0 + 63: lane l plays vt0 + l and vt0 + l + 32
+    auto play_block = [&](const int vt0) {
+  #pragma unroll
+      for (int set = 0; set < 2; ++set) {
+        const int vt = vt0 + lane + 32 * set;
+        const double init = (vt < G && vt < fe) ? -0.0 : 0.0;
+  #pragma unroll
+        for (int k = 0; k < 5; ++k) acc[set][k] = init;
+        if (vt >= G) continue;
+        int i = vt;
+        // centre, axial and pair points
+        for (; i < kCorner0; i += G) {
+          unsigned long long code[kWords];
+  #pragma unroll
+          for (int q = 0; q < kWords; ++q) code[q] = s_code[i][q];
+          const int orbit = (int)((unsigned)code[0] >> 6) & 3;
+          code[0] &= ~0xC0ULL;
+          double t[D];
+  #pragma unroll
+          for (int j = 0; j < D; ++j) {
+            const unsigned half = (unsigned)(code[j >> 3] >> (32 * ((j >> 2) & 1)));
+            t[j] = term_at<D>(term_b, j, __byte_perm(half, 0, 0x4440 + (j & 3)));
+          }
+          const double fx = F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
           if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
-          const double* w = s_w[4 + (__popc(bits) & 1)];
-#pragma unroll
+          if (i < kStore) store[i] = fx;
+          const double* w = s_w[orbit];
+  #pragma unroll
           for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
         }
-      } else {
-        CornerCombine<F, D, 0> cc;
-        for (; i < fe; i += G) {
-          const unsigned bits = (unsigned)(i - kCorner0);
-          const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
-          if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
-          const double* w = s_w[4 + (__popc(bits) & 1)];
-#pragma unroll
-          for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+        // corner points: bit j of (i - kCorner0) set => abscissa candidate 6 (minus), else 5 (plus)
+        if (G == 64) {
+          CornerCombine<F, D, kLo> cc;
+          if (i < fe) cc.head(term_b, (unsigned)(i - kCorner0));
+          for (; i < fe; i += 64) {
+            const unsigned bits = (unsigned)(i - kCorner0);
+            const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
+            if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
+            const double* w = s_w[4 + (__popc(bits) & 1)];
+  #pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+          }
+        } else {
+          CornerCombine<F, D, 0> cc;
+          for (; i < fe; i += G) {
+            const unsigned bits = (unsigned)(i - kCorner0);
+            const double fx = F::template finish<D>(cc.tail(term_b, bits), args.f) * jac;
+            if (!isfinite(fx)) badpt = min(badpt, (unsigned)i);
+            const double* w = s_w[4 + (__popc(bits) & 1)];
+  #pragma unroll
+            for (int k = 0; k < 5; ++k) acc[set][k] = acc[set][k] + w[k] * fx;
+          }
         }
       }
+    };
+    double sums[5];
+    if constexpr (!WIDE) {
+      play_block(0);
+      schedule_tree(acc[0], acc[1], lane, sums);
+    } else {
+      const int leaves = G < fe ? G : fe;           // virtual threads beyond own no point: zero leaves
+      unsigned have = 0;
+      for (int vt0 = 0; vt0 < leaves; vt0 += 64) {
+        play_block(vt0);
+        schedule_tree(acc[0], acc[1], lane, sums);
+        int h = 0;
+        for (; (have >> h) & 1u; ++h) {             // carry: left subtree (stored) + right subtree (new)
+#pragma unroll
+          for (int k = 0; k < 5; ++k) sums[k] = s_lvl[wib][h][k] + sums[k];
+          have &= ~(1u << h);
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) s_lvl[wib][h][k] = sums[k];
+        }
+        have |= 1u << h;
+        __syncwarp();
+      }
+      bool first = true;
+      for (int h = 0; h < 8; ++h) {
+        if (!((have >> h) & 1u)) continue;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) sums[k] = first ? s_lvl[wib][h][k] : s_lvl[wib][h][k] + sums[k];
+        first = false;
+      }
+      __syncwarp();
     }
     if (__any_sync(PCB_FULL_MASK, badpt != 0xffffffffu)) {
       if (badpt != 0xffffffffu) atomicMin(args.bad, (unsigned long long)r * (unsigned long long)fe + (unsigned long long)badpt);
     }
 
-    // ---- 3. schedule tree, 4. volume scaling / error / split axis
-    double sums[5];
-    schedule_tree(acc[0], acc[1], lane, sums);
+    // ---- 3. schedule tree (above), 4. volume scaling / error / split axis
     double v[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) v[k] = vol * sums[k];

@@ -23,8 +23,7 @@ static pcb_status validate_rule(pcb_ctx* ctx, const pcb_integrand* f, const pcb_
   if (rule->d != f->d) return fail(ctx, PCB_INVALID, "rule, regions, and integrand dimensions must agree");
   if (rule->f_eval != (1 << rule->d) + 2 * rule->d * rule->d + 2 * rule->d + 1)
     return fail(ctx, PCB_INVALID, "rule f_eval %d is not 2^d + 2d^2 + 2d + 1", rule->f_eval);
-  if (cfg->group_size < 1 || cfg->group_size > 64)
-    return fail(ctx, PCB_INVALID, "group_size %d unsupported: the warp schedule covers 1..64 virtual threads", cfg->group_size);
+  if (cfg->group_size < 1) return fail(ctx, PCB_INVALID, "group_size must be >= 1");
   if (cfg->err_mode < 0 || cfg->err_mode > 2) return fail(ctx, PCB_INVALID, "unknown err_mode %d", cfg->err_mode);
   return PCB_OK;
 }
@@ -84,7 +83,8 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
     PCB_CUDA_TRY(ctx, launch(ctx, lanes_fn, dim3((unsigned)std::min<long long>(want, (long long)per_sm * ctx->sm_count)), dim3(lanes_threads), lanes_smem, a));
     return PCB_OK;
   }
-  const void* fn = eval_kernel(f->family, f->d);
+  // widths above 64 take the exact-order kernel in its block-walking form (pagani.py:175-192 for any G)
+  const void* fn = cfg->group_size > 64 ? eval_wide_kernel(f->family, f->d) : eval_kernel(f->family, f->d);
   ProfileSpan span(ctx, 0, (double)n);
   PCB_CUDA_TRY(ctx, launch(ctx, fn, dim3(eval_grid(ctx, fn, n)), dim3(kEvalWarps * 32), 0, a));
   return PCB_OK;

@@ -30,6 +30,16 @@ const void* PCB_CAT(eval_kernel_fam, PCB_FAM)(int d) {
   return nullptr;
 }
 
+// schedule widths above 64: the exact-order kernel walking the virtual threads in blocks of 64
+const void* PCB_CAT(eval_wide_kernel_fam, PCB_FAM)(int d) {
+  switch (d) {
+#define X(D) case D: return (const void*)&pagani_eval_kernel<PCB_FAM, D, true>;
+    PCB_DIMS(X)
+#undef X
+  }
+  return nullptr;
+}
+
 // one-region-per-lane kernel (multiplicative or generic form) and its dynamic shared memory
 template <int D>
 static const void* lanes_kernel_for(size_t* smem, int* threads) {

@@ -121,6 +121,7 @@ inline pcb_status fail(pcb_ctx* ctx, pcb_status code, const char* fmt, ...) {
 // kernel getters, one translation unit per integrand family (pagani_inst.cu / mcubes_inst.cu)
 typedef const void* (*kernel_getter)(int d);
 const void* eval_kernel(int family, int d);
+const void* eval_wide_kernel(int family, int d);   // schedule widths above 64 (exact-order form, every family)
 const void* eval_lanes_kernel(int family, int d, size_t* smem, int* threads);  // nullptr: family has no one-region-per-lane kernel
 const void* points_kernel(int family, int d);
 const void* vsample_kernel_ptr(int family, int d, int rng);

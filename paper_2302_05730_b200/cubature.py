@@ -29,7 +29,7 @@ class PaganiConfig(_Frozen):
 
     `abs_tol` (epsabs, an extension; 0 = the reference) widens the target to
     max(abs_tol, rel_tol*|estimate|), for the stop test and for the split threshold alike.
-    `group_size` (the strided schedule width, 1..64 on the device) changes floating-point
+    `group_size` (the strided schedule width, any G >= 1 as in the reference) changes floating-point
     association only; `chunk` is accepted for compatibility and only affects which group id a
     non-finite report carries.
     """

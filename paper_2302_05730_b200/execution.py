@@ -83,6 +83,65 @@ def reduce(values, mode: str = DETERMINISTIC_TREE) -> float:
     return tree_sum(a) if a.size else 0.0
 
 
+class _Accumulator:
+    """Indexed accumulation handle of the reference's engine (engine.py:181-253): `add(index, value, stream)`,
+    `add_array(values, stream)`, `snapshot()`.  The integrators do not use it -- their accumulation is the
+    V-Sample kernel's shared-memory table -- but host callers of the reference API do.  Deterministic mode keeps
+    one partial buffer per logical stream and merges them in ascending stream order with the device pair tree
+    (`tree_sum`, engine.py:217-220); unordered mode is one shared buffer."""
+
+    def __init__(self, size, per_stream: bool):
+        import threading
+        self._shape = (int(size),) if np.isscalar(size) else tuple(int(v) for v in size)
+        self._per_stream = per_stream
+        self._bufs: dict = {}
+        self._lock = threading.Lock()
+
+    def _buf(self, stream):
+        key = stream if self._per_stream else 0
+        with self._lock:
+            return self._bufs.setdefault(key, np.zeros(self._shape))
+
+    def add(self, index, value, stream=0):
+        buf = self._buf(stream)
+        with self._lock:
+            buf[index] += value
+
+    def add_array(self, values, stream=0):
+        values = np.asarray(values, dtype=float)
+        if values.shape != self._shape:
+            raise IndexError(f"expected shape {self._shape}, got {values.shape}")
+        buf = self._buf(stream)
+        with self._lock:
+            buf += values
+
+    def snapshot(self) -> np.ndarray:
+        with self._lock:
+            parts = [self._bufs[k].copy() for k in sorted(self._bufs)]
+        if not parts:
+            return np.zeros(self._shape)
+        return tree_sum(np.stack(parts, axis=0), axis=0) if len(parts) > 1 else parts[0]
+
+
+class DeterministicAccumulator(_Accumulator):
+    def __init__(self, size):
+        super().__init__(size, per_stream=True)
+
+
+class UnorderedAccumulator(_Accumulator):
+    def __init__(self, size):
+        super().__init__(size, per_stream=False)
+
+
+def accumulator(size, mode: str = DETERMINISTIC_TREE):
+    """Shared accumulation handle for an index space (engine.py:247-253)."""
+    if mode == DETERMINISTIC_TREE:
+        return DeterministicAccumulator(size)
+    if mode == UNORDERED:
+        return UnorderedAccumulator(size)
+    raise ValueError(f"unknown accumulation mode {mode!r}")
+
+
 def parallel_for_groups(n_groups: int, task, cfg: ExecConfig | None = None) -> list:
     """task(group_id) for every id, results in id order (engine.py:106-161).
 

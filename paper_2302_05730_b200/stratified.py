@@ -113,6 +113,26 @@ def cube_coordinates(cube_index, g: int, d: int) -> np.ndarray:
     return out
 
 
+def sample_cube(f: Integrand, cube_index: int, plan: McubesPlan, grid: VegasGrid, rng):
+    """Draw p samples in one sub-cube; returns (S1, S2, bin_hits) (mcubes.py:143-164).
+
+    `rng` is duck-typed like the reference's: anything with `take(n) -> n uniforms in [0, 1)`
+    (an `RngStream`, or a table-backed object -- the reference's second injection route,
+    SURVEY.md section 0.1).  The stratified map, the grid transform, the integrand and the two
+    `tree_sum`s run on the device (pcb_mcubes_sample_cube); `bin_hits` is the reference's list of
+    (bin ids of sample k, v_k^2)."""
+    if not 0 <= cube_index < plan.m:
+        raise IndexError(f"cube index {cube_index} out of range [0, {plan.m})")
+    if plan.d != grid.d or plan.d != f.d:
+        raise ValueError("plan, grid, and integrand dimensions must agree")
+    u = np.asarray(rng.take(plan.p * plan.d), dtype=np.float64).reshape(plan.p, plan.d)
+    try:
+        s1, s2, bins, weights = _native.mcubes_sample_cube(f.device_spec(), plan, grid.boundaries, int(cube_index), u)
+    except _native.NonFiniteStatus as exc:
+        raise NonFiniteEvaluationError(exc.point, exc.value) from None
+    return s1, s2, [(bins[k], float(weights[k])) for k in range(plan.p)]
+
+
 def update_variance(s1: float, s2: float, p: int, m: int):
     """Per-cube estimate and clamped variance from sample sums (mcubes.py:167-179).
     Three scalars; the V-Sample kernel evaluates the same expressions per sub-cube."""

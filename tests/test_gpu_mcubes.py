@@ -185,6 +185,72 @@ def test_vsample_thread_shards_reassemble(monkeypatch):
         _native.mcubes_sample(spec, plan, grid.boundaries, 9, thread_range=(5, 100))
 
 
+def test_sample_cube_matches_reference_fixture():
+    """The single-cube API (mcubes.py:143-164) with a duck-typed rng: an RngStream (device hash) and a table-backed
+    object (the reference's second injection route).  Bins identical; S1, S2 and the hit weights bit-exact on the
+    families without transcendentals, 1e-12 otherwise."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sample_cube.json")) as fh:
+        cases = json.load(fh)["cases"]
+
+    class TableRng:
+        def __init__(self, table):
+            self.table, self.pos = table, 0
+
+        def take(self, n):
+            out = self.table[self.pos:self.pos + n]
+            self.pos += n
+            return out
+
+    for c in cases:
+        d = c["d"]
+        plan, grid = pb.make_plan(c["n"], d), pb.init_grid(d)
+        u = np.array([fromhex(v) for v in c["uniforms"]])
+        rng = (pb.RngStream(77, c["cube"] // plan.s, (c["cube"] % plan.s) * plan.p * d) if c["kind"] == "stream" else TableRng(u))
+        s1, s2, hits = stratified.sample_cube(pb.get_integrand(c["family"], d), c["cube"], plan, grid, rng)
+        assert [h[0].tolist() for h in hits] == c["bins"]
+        want_s1, want_s2 = fromhex(c["s1"]), fromhex(c["s2"])
+        want_w = np.array([fromhex(v) for v in c["weights"]])
+        got_w = np.array([h[1] for h in hits])
+        if c["family"] in ("f2", "sum"):
+            assert (s1, s2) == (want_s1, want_s2) and np.array_equal(got_w, want_w)
+        else:
+            assert abs(s1 - want_s1) <= REL_SUM * abs(want_s1) and abs(s2 - want_s2) <= REL_SUM * abs(want_s2)
+            assert np.allclose(got_w, want_w, rtol=REL_SUM, atol=0)
+    with pytest.raises(IndexError):
+        stratified.sample_cube(pb.get_integrand("f2", 4), 10**9, pb.make_plan(20000, 4), pb.init_grid(4), TableRng(u))
+    # a non-finite value surfaces as the reference's NonFiniteEvaluationError(point, value)
+    f = pb.get_integrand("f2", 2)
+    f.a2 = 0.0
+    p2 = pb.make_plan(8, 2)   # g = 2: the sub-cube corner (0.5, 0.5) is reachable with u = 0 in cube 3
+    with pytest.raises(pb.NonFiniteEvaluationError) as info:
+        stratified.sample_cube(f, 3, p2, pb.init_grid(2), TableRng(np.zeros(p2.p * 2)))
+    assert np.isinf(info.value.value) and np.array_equal(info.value.point, [0.5, 0.5])
+
+
+def test_accumulator_modes():
+    """engine.accumulator (engine.py:181-253): per-stream partials merged in stream order with the device pair tree."""
+    acc = pb.accumulator(4)
+    acc.add(1, 2.0, stream=3)
+    acc.add(1, 0.5, stream=0)
+    acc.add_array(np.array([1.0, 1.0, 1.0, 1.0]), stream=7)
+    assert np.array_equal(acc.snapshot(), [1.0, 3.5, 1.0, 1.0])
+    un = pb.accumulator((2, 2), mode="unordered")
+    un.add((0, 1), 4.0)
+    un.add_array(np.ones((2, 2)), stream=9)
+    assert np.array_equal(un.snapshot(), [[1.0, 5.0], [1.0, 1.0]])
+    with pytest.raises(IndexError):
+        acc.add_array(np.ones(3))
+    with pytest.raises(ValueError):
+        pb.accumulator(4, mode="other")
+    parts = np.random.default_rng(0).standard_normal((5, 6))
+    det = pb.accumulator(6)
+    for k in (4, 0, 2, 1, 3):
+        det.add_array(parts[k], stream=k)
+    assert np.array_equal(det.snapshot(), po.tree_sum(parts, axis=0))
+
+
 def test_vsample_non_finite_report():
     f = pb.get_integrand("f2", 2)
     f.a2 = 0.0
@@ -391,6 +457,35 @@ def test_full_size_pass_properties_config4():
     assert np.array_equal(np.concatenate([gplo, gphi]), gpa)
     assert np.allclose(clo + chi, ca, rtol=1e-12, atol=0)
     assert lo.n_samples + hi.n_samples == a.n_samples
+
+
+@pytest.mark.parametrize("gid", [0, 77, 128, 255])
+def test_full_size_work_groups_against_oracle_config4(gid):
+    """BASELINE config 4 at its full size against the CPU oracle, one work-group at a time (a whole pass is
+    8.6e8 samples -- hours on the CPU -- but `_group_task` (mcubes.py:210-265) is independent per group: 128 logical
+    threads x s = 13122 sub-cubes x p = 2 samples).  Pins the digit path at m = 12^8, the segment cut of a logical
+    thread at the real s and the lane -> segment map at the real size.
+    First, an interior, the first of the upper half and the last group; (I, Var) partials to 1e-12, the group's
+    contribution table to 1e-12 of its row sums' scale, clamp counts identical."""
+    d, n = 8, 10**9
+    plan, grid = pb.make_plan(n, d), pb.init_grid(d)
+    assert (plan.n_threads, plan.n_groups, plan.group_size) == (32768, 256, 128)
+    oplan = po.make_plan(n, d)
+    seed = po.derive_seed(0, 0)
+    want = po.vsample("f3", oplan, np.array(grid.boundaries), seed=seed, groups=[gid])
+    t0, t1 = gid * plan.group_size, (gid + 1) * plan.group_size
+    it, contrib, gp = _native.mcubes_sample(pb.get_integrand("f3", d).device_spec(), plan, grid.boundaries, seed,
+                                            thread_range=(t0, t1), want_group_partials=True)
+    assert gp.shape == (1, 2)
+    wi, wv = want["group_partials"][0]
+    assert abs(gp[0, 0] - wi) <= REL_SUM * abs(wi)
+    assert abs(gp[0, 1] - wv) <= 1e-10 * abs(wv)
+    assert it.clamp_events == want["clamp_events"]
+    assert it.n_samples == plan.group_size * plan.s * plan.p
+    scale = np.abs(want["contributions"]).max(axis=1, keepdims=True)
+    assert np.all(np.abs(contrib - want["contributions"]) <= REL_SUM * scale)
+    # bins the group never reaches stay exactly empty
+    assert np.array_equal(contrib == 0.0, want["contributions"] == 0.0)
 
 
 def test_segmented_thread_shards_reassemble_bit_for_bit():

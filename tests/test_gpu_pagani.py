@@ -22,6 +22,9 @@ EXACT = ("f2", "sum")
 REL_I = 1e-12   # per-region integral, relative to max(|I|, region scale)
 REL_E = 1e-7    # per-region error estimate where it is above the cancellation floor
 REL_EST = 1e-10  # final estimates
+# split axes that may differ from the reference over ALL non-exact evaluate fixtures together (ties of the
+# fourth-difference indicator broken by rounding noise); measured on the B200: see the printed table
+MAX_DIFFERING_AXES = 40
 
 
 def rule_dict(r):
@@ -93,6 +96,7 @@ def test_f6_threshold_is_strict():
 # ------------------------------------------------------------------ evaluate vs the reference fixtures
 def test_evaluate_matches_reference_fixtures(golden):
     z = golden["_pagani_eval"]
+    differing = {}
     for tag, meta in golden["pagani_eval"].items():
         d = meta["d"]
         lefts, lengths = _regions(meta)
@@ -103,9 +107,19 @@ def test_evaluate_matches_reference_fixtures(golden):
         _check_regions(tag, meta["family"], got, z[f"{tag}_I"], z[f"{tag}_E"], z[f"{tag}_K"].astype(np.int64), exact,
                        volumes=np.prod(lengths, axis=1))
         if not exact:
-            # split axis: identical wherever the reference's own indicator is not a numerical tie
+            # split axis: identical wherever the reference's own indicator is not a numerical tie.  The number of
+            # differing axes per fixture is printed (pytest -s / the captured-output section of a failure), so a
+            # drift from 99.9 % to 99.1 % shows in the log long before it trips the bar.
             same = got.split_axes == z[f"{tag}_K"]
+            differing[tag] = (int((~same).sum()), int(same.size))
             assert same.mean() >= 0.99, (tag, same.mean())
+    print("split axes differing from the reference, per fixture (count / regions):")
+    for tag, (bad, n) in differing.items():
+        print(f"  {tag:24s} {bad:5d} / {n}")
+    print(f"  total {sum(b for b, _ in differing.values())} / {sum(n for _, n in differing.values())}")
+    # today's state, so that a regression shows as a failure, not only in the log: every fixture but the tie-ridden
+    # uniform f4/f5 tilings agrees on every region
+    assert sum(b for b, _ in differing.values()) <= MAX_DIFFERING_AXES, differing
 
 
 @pytest.mark.parametrize("fam", EXACT)
@@ -119,8 +133,10 @@ def test_evaluate_bit_exact_random_boxes(fam, d):
     _check_regions(f"{fam}{d}", fam, got, i, e, k, exact=True)
 
 
-@pytest.mark.parametrize("group", [1, 7, 16, 32, 33, 63, 64])
+@pytest.mark.parametrize("group", [1, 7, 16, 32, 33, 63, 64, 65, 100, 128, 149, 150, 1000])
 def test_schedule_width_is_bit_exact(group):
+    """Every schedule width the reference accepts (pagani.py:56,66: any G >= 1); f_eval(6) = 149, so 149/150/1000
+    cover "one point per virtual thread" and "more virtual threads than points"."""
     d = 6
     lefts, lengths = random_boxes(d, 128, seed=5)
     rule = pb.build_rule(d)
@@ -130,10 +146,20 @@ def test_schedule_width_is_bit_exact(group):
     _check_regions(f"G{group}", "f2", got, i, e, k, exact=True)
 
 
-def test_unsupported_schedule_width_is_an_error():
+@pytest.mark.parametrize("fam", ["f1", "f3", "f4"])
+def test_wide_schedule_on_transcendental_families(fam):
+    """G > 64 with exp/cos/pow: per-region values to 1e-12 against the oracle at the same width."""
+    d, group = 8, 200
+    lefts, lengths = random_boxes(d, 96, seed=21)
+    rule = pb.build_rule(d)
+    got = pb.pagani_kernel(pb.get_integrand(fam, d), pb.RegionList(lefts, lengths), rule, None, pb.PaganiConfig(group_size=group))
+    i, e, k = po.pagani_evaluate(fam, lefts, lengths, rule_dict(rule), group=group)
+    _check_regions(f"{fam}-G{group}", fam, got, i, e, k, exact=False, volumes=np.prod(lengths, axis=1))
+
+
+def test_bad_schedule_width_is_an_error():
     with pytest.raises(ValueError):
-        pb.pagani_kernel(pb.get_integrand("f2", 3), pb.uniform_split(3, 2), pb.build_rule(3), None,
-                         pb.PaganiConfig(group_size=128))
+        pb.PaganiConfig(group_size=0)
 
 
 @pytest.mark.parametrize("mode", ["two-level", "max-null", "max-pairwise"])
@@ -215,9 +241,28 @@ def test_tree_sum_edge_cases():
 
 
 # ------------------------------------------------------------------ refine vs the reference
+def _sweep_cases():
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sweep_refine.json")
+    with open(path) as fh:
+        return json.load(fh)["cases"]
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: f"{c['family']}d{c['d']}")
+def test_refine_sweep_config5_matches_reference(case):
+    """BASELINE config 5: the sweep cases the reference converges on at rel_tol 1e-3 (f1d6, f4d6, f5d6, f3d7, f3d8;
+    the d=5 ones and f3d6 are in test_refine_matches_reference).  Up to 15.5 M regions: identical iteration counts,
+    per-iteration active/leaf counts, regions_processed and stop reasons; estimates to 1e-10."""
+    _check_refine_case(case)
+
+
 @pytest.mark.parametrize("idx", range(15))
 def test_refine_matches_reference(golden, idx):
-    case = golden["pagani_refine"][idx]
+    _check_refine_case(golden["pagani_refine"][idx])
+
+
+def _check_refine_case(case):
     recs = []
     res = pb.refine(pb.get_integrand(case["family"], case["d"]), pb.PaganiConfig(rel_tol=case["rel_tol"], **case["cfg"]),
                     progress=recs.append)

@@ -195,6 +195,31 @@ def test_mcubes_run_matches_reference(golden):
             _close(golden, got["iter_integral"], fromhex(want["iter_integral"]), tol=1e-10)
 
 
+def _cube_cases():
+    import json
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "sample_cube.json")) as fh:
+        return json.load(fh)
+
+
+def test_sample_cube_matches_reference():
+    """mcubes.sample_cube (mcubes.py:143-164): RngStream-fed and table-fed sub-cubes from the reference."""
+    doc = _cube_cases()
+    for c in doc["cases"]:
+        plan = po.make_plan(c["n"], c["d"])
+        u = np.array([fromhex(v) for v in c["uniforms"]])
+        if c["kind"] == "stream":   # the stream position the reference took the uniforms from (integer-exact)
+            ctr = (c["cube"] % plan["s"]) * plan["p"] * c["d"] + np.arange(u.size)
+            assert np.array_equal(po.uniform(77, np.uint64(c["cube"] // plan["s"]), ctr.astype(np.uint64)), u)
+        s1, s2, bins, w = po.sample_cube(c["family"], c["cube"], plan, po.uniform_grid(c["d"]), u)
+        assert bins.tolist() == c["bins"]
+        want = (fromhex(c["s1"]), fromhex(c["s2"]), np.array([fromhex(v) for v in c["weights"]]))
+        if doc["numpy"] == np.__version__:
+            assert (s1, s2) == want[:2] and np.array_equal(w, want[2])
+        else:
+            assert abs(s1 - want[0]) <= 1e-13 * abs(want[0]) and abs(s2 - want[1]) <= 1e-13 * abs(want[1])
+            assert np.allclose(w, want[2], rtol=1e-13, atol=0)
+
+
 def test_update_variance_examples():
     # SPEC.md:386-387 through the same formulas the V-Sample pass uses
     def upd(s1, s2, p, m):
