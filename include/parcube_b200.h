@@ -178,6 +178,11 @@ typedef struct pcb_ctx pcb_ctx;
 pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out);
 void pcb_ctx_destroy(pcb_ctx* ctx);
 const char* pcb_last_error(const pcb_ctx* ctx);
+/* Scratch memory of a context (region lists, estimates, contribution tables) lives in the device's stream-ordered
+ * memory pool and is never handed back to the driver while the process lives; it grows on demand.  reserve() grows
+ * the pool to at least `bytes` up front, so that the first large call pays no driver allocation in its loop
+ * (a refine() to the default region cap 2^26 at d = 8 peaks at ~11 GB).  *reserved_out = pool size afterwards.   */
+pcb_status pcb_ctx_reserve(pcb_ctx* ctx, uint64_t bytes, uint64_t* reserved_out);
 /* name and SM count of the context's device, multiprocessor clock in kHz */
 pcb_status pcb_device_info(pcb_ctx* ctx, char* name, int name_len, int32_t* sm_count, int32_t* clock_khz);
 /* kernels launched by this context since creation (bench.py "gpu_launches") */
@@ -257,6 +262,40 @@ pcb_status pcb_pagani_shard_rebuild(pcb_ctx* ctx, int64_t keep_begin, int64_t ke
                                     const double* back_lefts, const double* back_lengths);
 pcb_status pcb_pagani_shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad);
 
+/* ---- the same steps with the collectives on DEVICE buffers (NCCL on the context's stream, no host staging) ----
+ *   deferred      on: init / evaluate / split only enqueue; the slice's non-finite flag travels in the packed row
+ *   pack          this rank's row of the iteration: non-finite flag, counts, and for the active (and, with_retired, the
+ *                 just-retired) integrals and errors the raw head / tail values around the 1024-aligned GLOBAL blocks plus
+ *                 the pair-tree sums of the complete blocks; `width` >= max over ranks of count/1024 + 1.  The host
+ *                 all-gathers `row` into `gathered` (world rows; == row for world 1) on `stream`
+ *   global_sums   finishes engine.tree_sum over the concatenated global arrays from the gathered rows, on the device,
+ *                 and returns (sum I, sum E, retired I, retired E) -- bit-identical to one device for any world size --
+ *                 and the lowest rank that saw a non-finite evaluation (-1: none).  One synchronisation
+ *   nonfinite     on that rank: the offending (local region, point, value, abscissa)
+ *   classify_dev  split mask + (split count, max error) as two doubles in *row; the host all-gathers them into
+ *                 *gathered (2*world doubles) and reads them
+ *   split_dev     split with the local count taken from that read
+ *   list_dev / rebuild_dev   the local list [d][ld] for rank-to-rank sends; new list = front ++ local[keep) ++ back
+ *                 with front/back received blocks laid out [2][d][n] (lefts, lengths)                            */
+typedef struct {
+  void* stream;
+  double* row;
+  double* gathered;
+  int64_t row_doubles;
+} pcb_pagani_shard_rows;
+pcb_status pcb_pagani_shard_deferred(pcb_ctx* ctx, int32_t on);
+pcb_status pcb_pagani_shard_pack(pcb_ctx* ctx, int64_t head_active, int64_t head_retired, int32_t with_retired, int64_t width,
+                                 int32_t world, pcb_pagani_shard_rows* out);
+pcb_status pcb_pagani_shard_global_sums(pcb_ctx* ctx, int32_t world, int64_t n_active_total, int64_t n_retired_total,
+                                        double sums[4], int32_t* bad_rank);
+pcb_status pcb_pagani_shard_nonfinite(pcb_ctx* ctx, pcb_nonfinite* bad);
+pcb_status pcb_pagani_shard_classify_dev(pcb_ctx* ctx, double budget, int32_t mode, double emax, int32_t world, double** row,
+                                         double** gathered);
+pcb_status pcb_pagani_shard_split_dev(pcb_ctx* ctx, int64_t n_split);
+pcb_status pcb_pagani_shard_list_dev(pcb_ctx* ctx, double** lefts, double** lengths, int64_t* n, int64_t* ld);
+pcb_status pcb_pagani_shard_rebuild_dev(pcb_ctx* ctx, int64_t keep_begin, int64_t keep_end, int64_t n_front,
+                                        const double* front_dev, int64_t n_back, const double* back_dev);
+
 /* ---- fixed-shape reductions: replaces engine.tree_sum (engine.py:69-86) --------------- */
 pcb_status pcb_tree_sum(pcb_ctx* ctx, int64_t n, const double* values, double* out);
 
@@ -306,6 +345,40 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
                           int32_t* n_done, pcb_mcubes_progress_fn progress, void* user,
                           double* contributions_out /* optional (iterations, d, n_bins) */,
                           double* final_boundaries, double* seconds_device, pcb_nonfinite* bad);
+
+/* ---- m-Cubes driver on a shard of the sub-cubes (multi-GPU; one context per rank) ----------------
+ * Same device-resident loop as pcb_mcubes_run with the logical threads sharded over `world` ranks on work-group
+ * boundaries (rank r owns groups [G*r/world, G*(r+1)/world); any partition draws the same samples,
+ * mcubes.py:224-232).  Nothing here waits for the device except wait() and end(); the host issues, per iteration,
+ *     pass(it);  all-gather of `row` into `gathered`;  all-reduce (sum) of `table` in place;  finish(it)
+ * with the two collectives ON `stream` (NCCL through torch.distributed in paper_2302_05730_b200/sharded.py; none
+ * for world == 1), and may enqueue iteration it+1 before it waits for the record of iteration it.
+ *   row       this rank's per-work-group (I, Var) partials (mcubes.py:255-259), zero padded to ceil(G/world) pairs,
+ *             then its first non-finite sample index and its clamp count (8-byte integers)
+ *   gathered  `world` rows in rank order; every rank finishes the reference's group-order pair tree
+ *             (mcubes.py:292-293) over all G pairs: (integral, variance) are bit-identical for any world size
+ *   table     the pass's (d, n_bins) contribution table (mcubes.py:294-298); after the all-reduce every rank refines
+ *             the identical grid                                                                          */
+typedef struct {
+  void* stream;        /* cudaStream_t of the context */
+  double* row;         /* device, row_doubles */
+  double* gathered;    /* device, world * row_doubles (== row when world == 1) */
+  double* table;       /* device, table_doubles */
+  int64_t row_doubles;
+  int64_t table_doubles;
+  int64_t thread_begin, thread_end; /* this rank's logical threads */
+} pcb_mcubes_shard_buffers;
+pcb_status pcb_mcubes_shard_begin(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, int32_t iterations,
+                                  uint64_t seed, int32_t rng_kind, int32_t adapt, double alpha, int32_t smoothing,
+                                  double rel_tol, double abs_tol, int32_t keep_tables, int32_t rank, int32_t world,
+                                  pcb_mcubes_shard_buffers* out);
+pcb_status pcb_mcubes_shard_pass(pcb_ctx* ctx, int32_t iteration);
+pcb_status pcb_mcubes_shard_finish(pcb_ctx* ctx, int32_t iteration);
+/* blocks until iteration's record arrives; *stop != 0: the run's tolerance is met (identical on every rank) */
+pcb_status pcb_mcubes_shard_wait(pcb_ctx* ctx, int32_t iteration, pcb_mcubes_iteration* out, int32_t* stop, pcb_nonfinite* bad);
+/* drains the stream; contributions_out (n_done, d, n_bins) needs keep_tables; final_boundaries (d, n_bins+1) */
+pcb_status pcb_mcubes_shard_end(pcb_ctx* ctx, int32_t n_done, double* contributions_out, double* final_boundaries,
+                                double* seconds_device);
 
 /* ---- RNG mirror: replaces mcubes._uniform / derive_seed (mcubes.py:51-60) -------------- */
 pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,

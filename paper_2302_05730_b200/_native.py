@@ -89,6 +89,16 @@ class McubesProgressC(C.Structure):
                 ("chi2_per_dof", C.c_double), ("iter_integral", C.c_double), ("iter_variance", C.c_double)]
 
 
+class McubesShardBuffersC(C.Structure):
+    _fields_ = [("stream", C.c_void_p), ("row", C.c_void_p), ("gathered", C.c_void_p), ("table", C.c_void_p),
+                ("row_doubles", C.c_int64), ("table_doubles", C.c_int64), ("thread_begin", C.c_int64),
+                ("thread_end", C.c_int64)]
+
+
+class PaganiShardRowsC(C.Structure):
+    _fields_ = [("stream", C.c_void_p), ("row", C.c_void_p), ("gathered", C.c_void_p), ("row_doubles", C.c_int64)]
+
+
 PAGANI_PROGRESS_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(PaganiProgressC))
 MCUBES_PROGRESS_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(McubesProgressC))
 
@@ -98,6 +108,7 @@ SIGNATURES = {
     "pcb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "pcb_ctx_destroy": (None, [C.c_void_p]),
     "pcb_last_error": (C.c_char_p, [C.c_void_p]),
+    "pcb_ctx_reserve": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "pcb_device_info": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pcb_launch_count": (C.c_int64, [C.c_void_p]),
     "pcb_measure_fp64_peak": (C.c_int, [C.c_void_p, _DP]),
@@ -130,6 +141,17 @@ SIGNATURES = {
     "pcb_pagani_shard_rebuild": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
                                            C.c_void_p, C.c_void_p]),
     "pcb_pagani_shard_evaluate": (C.c_int, [C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_pagani_shard_deferred": (C.c_int, [C.c_void_p, C.c_int32]),
+    "pcb_pagani_shard_pack": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32,
+                                        C.POINTER(PaganiShardRowsC)]),
+    "pcb_pagani_shard_global_sums": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, _DP, C.POINTER(C.c_int32)]),
+    "pcb_pagani_shard_nonfinite": (C.c_int, [C.c_void_p, C.POINTER(NonFiniteC)]),
+    "pcb_pagani_shard_classify_dev": (C.c_int, [C.c_void_p, C.c_double, C.c_int32, C.c_double, C.c_int32, C.POINTER(C.c_void_p),
+                                                C.POINTER(C.c_void_p)]),
+    "pcb_pagani_shard_split_dev": (C.c_int, [C.c_void_p, C.c_int64]),
+    "pcb_pagani_shard_list_dev": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int64)]),
+    "pcb_pagani_shard_rebuild_dev": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
     "pcb_mcubes_sample": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_void_p, C.c_uint64,
                                     C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.POINTER(McubesIterationC),
                                     C.c_void_p, C.c_void_p, C.POINTER(NonFiniteC)]),
@@ -141,6 +163,14 @@ SIGNATURES = {
                                  C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, C.POINTER(McubesIterationC),
                                  C.POINTER(C.c_int32), MCUBES_PROGRESS_FN, C.c_void_p, C.c_void_p, C.c_void_p, _DP,
                                  C.POINTER(NonFiniteC)]),
+    "pcb_mcubes_shard_begin": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(McubesPlanC), C.c_int32, C.c_uint64,
+                                         C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_double, C.c_double, C.c_int32,
+                                         C.c_int32, C.c_int32, C.POINTER(McubesShardBuffersC)]),
+    "pcb_mcubes_shard_pass": (C.c_int, [C.c_void_p, C.c_int32]),
+    "pcb_mcubes_shard_finish": (C.c_int, [C.c_void_p, C.c_int32]),
+    "pcb_mcubes_shard_wait": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(McubesIterationC), C.POINTER(C.c_int32),
+                                        C.POINTER(NonFiniteC)]),
+    "pcb_mcubes_shard_end": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, _DP]),
     "pcb_grid_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
     "pcb_debug_divide": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
@@ -221,6 +251,12 @@ class Context:
         sms, khz = C.c_int32(), C.c_int32()
         self.check(self.lib.pcb_device_info(self.handle, name, 256, C.byref(sms), C.byref(khz)))
         return name.value.decode(), sms.value, khz.value
+
+    def reserve(self, n_bytes: int) -> int:
+        """Grow the context's device memory pool to at least n_bytes now; returns the pool size."""
+        out = C.c_uint64()
+        self.check(self.lib.pcb_ctx_reserve(self.handle, int(n_bytes), C.byref(out)))
+        return int(out.value)
 
     def launch_count(self) -> int:
         return int(self.lib.pcb_launch_count(self.handle))
@@ -491,6 +527,63 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
     return [its[i] for i in range(done)], (None if contribs is None else contribs[:done]), final_b, seconds.value
 
 
+class DeviceArray:
+    """A float64 device buffer of the library as a `__cuda_array_interface__` object: torch.as_tensor(view, device=...)
+    aliases it without a copy, so the collectives of the sharded drivers run on the library's own buffers."""
+
+    def __init__(self, ptr: int, count: int):
+        self.ptr, self.count = int(ptr), int(count)
+        self.__cuda_array_interface__ = {"shape": (self.count,), "typestr": "<f8", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class McubesShardRun:
+    """One rank's side of a device-resident sharded m-Cubes run (pcb_mcubes_shard_*).  One live run per context."""
+
+    def __init__(self, spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, rng_kind: int, adapt: bool,
+                 alpha: float, smoothing: bool, rel_tol: float, abs_tol: float, keep_tables: bool, rank: int, world: int,
+                 device=None, ctx: "Context | None" = None):
+        self.ctx = ctx or context(device)
+        self.plan, self.n_bins, self.iterations, self.d = plan, int(n_bins), int(iterations), plan.d
+        self.keep_tables = bool(keep_tables)
+        fc, pc = spec.to_c(), plan_to_c(plan, n_bins)
+        self.buffers = McubesShardBuffersC()
+        with self.ctx.call_lock:
+            self.ctx.check(self.ctx.lib.pcb_mcubes_shard_begin(
+                self.ctx.handle, C.byref(fc), C.byref(pc), self.iterations, C.c_uint64(seed & (2**64 - 1)), int(rng_kind),
+                int(bool(adapt)), float(alpha), int(bool(smoothing)), float(rel_tol), float(abs_tol), int(self.keep_tables),
+                int(rank), int(world), C.byref(self.buffers)))
+        b = self.buffers
+        self.stream = int(b.stream or 0)
+        self.row = DeviceArray(b.row, b.row_doubles)
+        self.gathered = DeviceArray(b.gathered, b.row_doubles * world)
+        self.table = DeviceArray(b.table, b.table_doubles)
+        self.thread_range = (int(b.thread_begin), int(b.thread_end))
+
+    def enqueue_pass(self, it: int):
+        self.ctx.check(self.ctx.lib.pcb_mcubes_shard_pass(self.ctx.handle, int(it)))
+
+    def enqueue_finish(self, it: int):
+        self.ctx.check(self.ctx.lib.pcb_mcubes_shard_finish(self.ctx.handle, int(it)))
+
+    def wait(self, it: int):
+        """(record, stop) of iteration `it`; raises NonFiniteStatus on every rank alike."""
+        rec, stop, bad = McubesIterationC(), C.c_int32(), NonFiniteC()
+        self.ctx.check(self.ctx.lib.pcb_mcubes_shard_wait(self.ctx.handle, int(it), C.byref(rec), C.byref(stop), C.byref(bad)),
+                       bad, self.d)
+        return rec, bool(stop.value)
+
+    def end(self, n_done: int):
+        """(per-iteration tables or None, final boundaries, device seconds)."""
+        contribs = np.empty((n_done, self.d, self.n_bins)) if self.keep_tables else None
+        final_b = np.empty((self.d, self.n_bins + 1))
+        secs = C.c_double()
+        self.ctx.check(self.ctx.lib.pcb_mcubes_shard_end(self.ctx.handle, int(n_done), None if contribs is None else _ptr(contribs),
+                                                         _ptr(final_b), C.byref(secs)))
+        self.ctx.last_device_seconds = float(secs.value)
+        return contribs, final_b, secs.value
+
+
 def uniforms(seed: int, streams, counters, rng_kind: int = RNG_REFERENCE_HASH, device=None) -> np.ndarray:
     ctx = context(device)
     s = np.ascontiguousarray(np.broadcast_to(np.asarray(streams, dtype=np.uint64), np.broadcast(streams, counters).shape)).ravel()
@@ -590,6 +683,51 @@ class PaganiShard:
         out = C.c_double()
         self._call(self.ctx.lib.pcb_tree_sum, v.size, _ptr(v), C.byref(out))
         return out.value
+
+    # ---- device-collective mode (the product path of sharded.pagani_refine_sharded) --------------------------
+    def deferred(self, on: bool = True):
+        self._call(self.ctx.lib.pcb_pagani_shard_deferred, int(bool(on)))
+
+    def pack(self, head_active: int, head_retired: int, with_retired: bool, width: int, world: int):
+        """(stream, row, gathered) -- device views of this rank's packed row and of the all-gather target."""
+        rows = PaganiShardRowsC()
+        self._call(self.ctx.lib.pcb_pagani_shard_pack, int(head_active), int(head_retired), int(bool(with_retired)), int(width),
+                   int(world), C.byref(rows))
+        return int(rows.stream or 0), DeviceArray(rows.row, rows.row_doubles), DeviceArray(rows.gathered, rows.row_doubles * world)
+
+    def global_sums(self, world: int, n_active_total: int, n_retired_total: int):
+        sums, bad_rank = (C.c_double * 4)(), C.c_int32()
+        self._call(self.ctx.lib.pcb_pagani_shard_global_sums, int(world), int(n_active_total), int(n_retired_total), sums,
+                   C.byref(bad_rank))
+        return [sums[i] for i in range(4)], int(bad_rank.value)
+
+    def nonfinite(self):
+        """(local region, point index, value, abscissa) of this rank's first non-finite evaluation."""
+        bad = NonFiniteC()
+        with self.ctx.call_lock:
+            st = self.ctx.lib.pcb_pagani_shard_nonfinite(self.ctx.handle, C.byref(bad))
+        if st != PCB_NONFINITE:
+            self.ctx.check(st)
+        return int(bad.region_index), int(bad.point_index), float(bad.value), np.array(bad.point[: self.d])
+
+    def classify_dev(self, budget: float, mode: int, emax: float, world: int):
+        row, gathered = C.c_void_p(), C.c_void_p()
+        self._call(self.ctx.lib.pcb_pagani_shard_classify_dev, float(budget), int(mode), float(emax), int(world), C.byref(row),
+                   C.byref(gathered))
+        return DeviceArray(row.value, 2), DeviceArray(gathered.value, 2 * world)
+
+    def split_dev(self, n_split: int):
+        self._call(self.ctx.lib.pcb_pagani_shard_split_dev, int(n_split))
+
+    def list_dev(self):
+        """(lefts view, lengths view, n, ld): the local list, structure of arrays [d][ld] on the device."""
+        lefts, lengths, n, ld = C.c_void_p(), C.c_void_p(), C.c_int64(), C.c_int64()
+        self._call(self.ctx.lib.pcb_pagani_shard_list_dev, C.byref(lefts), C.byref(lengths), C.byref(n), C.byref(ld))
+        return DeviceArray(lefts.value, self.d * ld.value), DeviceArray(lengths.value, self.d * ld.value), n.value, ld.value
+
+    def rebuild_dev(self, keep_begin: int, keep_end: int, n_front: int, front_ptr: int, n_back: int, back_ptr: int):
+        self._call(self.ctx.lib.pcb_pagani_shard_rebuild_dev, int(keep_begin), int(keep_end), int(n_front),
+                   C.c_void_p(front_ptr or None), int(n_back), C.c_void_p(back_ptr or None))
 
 
 def bench_invoke(spec: DeviceSpec, points: np.ndarray, blocks: int, threads: int, repetitions: int, device=None):

@@ -91,6 +91,12 @@ pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out) {
   ctx->clock_khz = khz;
   std::strncpy(ctx->name, prop.name, sizeof(ctx->name) - 1);
   PCB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  {  // scratch memory: the device's stream-ordered pool, never trimmed (DevBuf in pcb_host.h)
+    cudaMemPool_t pool;
+    PCB_CUDA_TRY(ctx, cudaDeviceGetDefaultMemPool(&pool, device_ordinal));
+    unsigned long long keep = ~0ULL;
+    PCB_CUDA_TRY(ctx, cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pinned, 1 << 16));
   PCB_CUDA_TRY(ctx, ctx->scalars.ensure(64 * sizeof(double)));
   return PCB_OK;
@@ -100,8 +106,10 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) {
+    ctx->release_buffers();          // stream-ordered frees need the stream
     cudaStreamSynchronize(ctx->stream);
     cudaStreamDestroy(ctx->stream);
+    ctx->stream = nullptr;
   }
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
@@ -115,6 +123,26 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
     cudaEventDestroy(sp.b);
   }
   delete ctx;
+}
+
+pcb_status pcb_ctx_reserve(pcb_ctx* ctx, uint64_t bytes, uint64_t* reserved_out) {
+  if (!ctx) return PCB_INVALID;
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cudaMemPool_t pool;
+  PCB_CUDA_TRY(ctx, cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+  unsigned long long have = 0;
+  PCB_CUDA_TRY(ctx, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+  if (bytes > have) {
+    // one block of the missing size, released at once: the pool keeps the backing (release threshold = never) and
+    // serves the context's later requests from it without going to the driver
+    void* p = nullptr;
+    PCB_CUDA_TRY(ctx, cudaMallocAsync(&p, (size_t)(bytes - have), ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaFreeAsync(p, ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+  }
+  if (reserved_out) *reserved_out = have;
+  return PCB_OK;
 }
 
 const char* pcb_last_error(const pcb_ctx* ctx) { return ctx ? ctx->err.c_str() : "context is NULL"; }

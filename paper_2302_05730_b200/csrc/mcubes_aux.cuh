@@ -159,6 +159,10 @@ struct ReduceArgs {
   long long n_local_threads;
   double* group_out;
   unsigned long long* timeline;  // debug stamps or NULL
+  // sharded runs: the pass scalars (first non-finite sample, clamp count) are copied behind the group pairs of this
+  // rank's packed row, which the ranks then all-gather (NULL otherwise)
+  const unsigned long long* pass_scalars;
+  unsigned long long* row_tail;
 };
 __global__ void __launch_bounds__(kReduceThreads) reduce_kernel(const __grid_constant__ ReduceArgs a) {
   pdl_launch_dependents();
@@ -183,6 +187,10 @@ __global__ void __launch_bounds__(kReduceThreads) reduce_kernel(const __grid_con
   raw_stamp(ph, (int)blockIdx.x == a.merge_ctas - 1, 2);
   raw_stamp(ph, (int)blockIdx.x == a.merge_ctas, 4);
   raw_stamp(ph, blockIdx.x == gridDim.x - 1, 6);
+  if (a.row_tail && blockIdx.x == 0 && threadIdx.x == 0) {
+    a.row_tail[0] = a.pass_scalars[0];
+    a.row_tail[1] = a.pass_scalars[1];
+  }
   if ((int)blockIdx.x < a.merge_ctas) {
     merge_hist_cta(blockIdx.x, a.block_hist, a.nblocks, a.nbins_total, a.contrib, a.contrib_copy, s_dyn, s_stage);
     raw_stamp(ph, blockIdx.x == 0, 1);
@@ -198,10 +206,19 @@ __global__ void __launch_bounds__(kReduceThreads) reduce_kernel(const __grid_con
 // final reduction of the per-work-group (I, E) pairs in group order with the pair tree of engine.tree_sum
 // (mcubes.py:292-293), for up to 1024 groups in one CTA; returns (integral, variance sum) on thread 0.
 // s: [2][1024] doubles; blockDim.x >= 512.
-__device__ __forceinline__ void group_pairs_tree_cta(const double* __restrict__ pairs, int n, double* s, double& integral, double& variance) {
+// `world` > 0: the pairs come from the all-gathered rows of a sharded run -- rank r owns groups
+// [n*r/world, n*(r+1)/world) and its row starts at pairs + r*row_stride (group_shards in sharded.py).
+__device__ __forceinline__ void group_pairs_tree_cta(const double* __restrict__ pairs, int n, double* s, double& integral, double& variance,
+                                                     int world = 0, long long row_stride = 0) {
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) {
-    s[i] = i < n ? pairs[2 * i] : 0.0;
-    s[1024 + i] = i < n ? pairs[2 * i + 1] : 0.0;
+    const double* src = pairs + 2 * i;
+    if (world > 0 && i < n) {
+      const int r = (int)((((long long)i + 1) * world - 1) / n);          // owner of group i
+      const long long first = (long long)n * r / world;
+      src = pairs + r * row_stride + 2 * (i - first);
+    }
+    s[i] = i < n ? src[0] : 0.0;
+    s[1024 + i] = i < n ? src[1] : 0.0;
   }
   __syncthreads();
   for (int half = 512; half >= 1; half >>= 1) {
@@ -591,6 +608,10 @@ struct FinishArgs {
   McRecord* record;             // pinned host memory (nullptr: leave the results in scalars only)
   unsigned long long seq;
   unsigned long long* timeline; // debug stamps or NULL
+  // sharded runs: group_pairs points at the all-gathered rows (world rows of row_stride doubles: the rank's group
+  // pairs, then its first-non-finite index and clamp count); world = 0 otherwise
+  int world;
+  long long row_stride;
 };
 
 __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ FinishArgs a) {
@@ -612,7 +633,7 @@ __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ Fin
   double integral, variance;
   double* sc_d = reinterpret_cast<double*>(a.scalars);
   if (a.n_groups > 0) {
-    group_pairs_tree_cta(a.group_pairs, a.n_groups, sh, integral, variance);
+    group_pairs_tree_cta(a.group_pairs, a.n_groups, sh, integral, variance, a.world, a.row_stride);
   } else {
     integral = sc_d[2];
     variance = sc_d[3];
@@ -620,7 +641,16 @@ __global__ void __launch_bounds__(512) finish_kernel(const __grid_constant__ Fin
   if (threadIdx.x != 0) return;
   sc_d[2] = integral;
   sc_d[3] = variance;
-  const unsigned long long bad = a.scalars[0], clamps = a.scalars[1];
+  unsigned long long bad = a.scalars[0], clamps = a.scalars[1];
+  if (a.world > 0) {   // every rank takes the same minimum / sum over the gathered rows
+    bad = ~0ULL;
+    clamps = 0ULL;
+    for (int r = 0; r < a.world; ++r) {
+      const unsigned long long* tail = reinterpret_cast<const unsigned long long*>(a.group_pairs + (r + 1) * a.row_stride) - 2;
+      bad = tail[0] < bad ? tail[0] : bad;
+      clamps += tail[1];
+    }
+  }
   int stop = bad != ~0ULL;
   if (a.hist_i) {
     const double var = fmax(variance, 0.0);

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -149,7 +150,67 @@ struct PassTail {
   McRecord* record = nullptr;          // pinned
   unsigned long long seq = 0;
   unsigned long long* timeline = nullptr;  // device; debug
+  // sharded runs (pcb_mcubes_shard_*): the rank's packed row replaces ctx->mc_group, the end-of-pass launch is
+  // enqueued separately (behind the collectives) and reads the gathered rows
+  double* row = nullptr;               // device: [2 * width] group pairs, then bad, clamps
+  long long row_doubles = 0;
+  bool defer_finish = false;
+  const double* gathered = nullptr;    // device: world rows
+  int world = 0;
+  long long total_groups = 0;
 };
+
+// End-of-pass launch: group-order tree over the work-groups, grid refinement, iteration record, stop decision.
+static pcb_status enqueue_finish(pcb_ctx* ctx, const pcb_mcubes_plan* plan, const PassTail& tail, long long n_groups) {
+  const int d = plan->d, nb = plan->n_bins;
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>() + kMcSlot;
+  double* sc = ctx->scalars.as<double>() + kMcSlot;
+  FinishArgs fa;
+  fa.n_groups = (int)n_groups;
+  fa.group_pairs = ctx->mc_group.as<double>();
+  fa.world = 0;
+  fa.row_stride = 0;
+  if (tail.gathered) {
+    if (tail.total_groups > 1024) return fail(ctx, PCB_INVALID, "sharded mcubes_run supports at most 1024 work-groups (%lld requested)", tail.total_groups);
+    fa.n_groups = (int)tail.total_groups;
+    fa.group_pairs = tail.gathered;
+    fa.world = tail.world;
+    fa.row_stride = tail.row_doubles;
+  } else if (n_groups > 1024) {  // engine.reduce in group order over more groups than one CTA holds (never with the default plans)
+    if (tail.stop) return fail(ctx, PCB_INVALID, "mcubes_run supports at most 1024 work-groups (%lld requested)", n_groups);
+    double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
+    double* ge = gi + n_groups;
+    deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
+    ctx->launches++;
+    PCB_CUDA_TRY(ctx, cudaGetLastError());
+    PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));
+    PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
+    fa.n_groups = 0;
+  }
+  fa.refine.d = d; fa.refine.n = nb; fa.refine.alpha = tail.alpha; fa.refine.smoothing = tail.smoothing;
+  fa.refine.boundaries = tail.bounds_in; fa.refine.contrib = ctx->mc_contrib.as<double>(); fa.refine.new_boundaries = tail.bounds_out;
+  fa.n_refine = tail.refine ? d : 0;
+  fa.stop = tail.stop;
+  fa.scalars = sc_u;
+  fa.hist_i = tail.hist_i;
+  fa.hist_v = tail.hist_v;
+  fa.iteration = tail.iteration;
+  fa.rel_tol = tail.rel_tol;
+  fa.abs_tol = tail.abs_tol;
+  fa.record = tail.record;
+  fa.seq = tail.seq;
+  fa.timeline = tail.timeline;
+  fa.refine.phase_tl = (tail.timeline && tail.iteration == 1) ? tail.timeline + 200 : nullptr;
+  const size_t finish_smem = std::max<size_t>(refine_smem_doubles(nb), 2048) * sizeof(double);
+  if (finish_smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
+  PCB_TRY(grant_smem(ctx, (const void*)&finish_kernel, finish_smem));
+  {
+    void* args[] = {&fa};
+    PCB_CUDA_TRY(ctx, launch_pdl((const void*)&finish_kernel, dim3(fa.n_refine + 1), dim3(512), args, finish_smem, ctx->stream));
+    ctx->launches++;
+  }
+  return PCB_OK;
+}
 
 // Enqueue one V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries; nothing
 // here waits for the device.  Leaves: contributions in ctx->mc_contrib (d*nb), per-group (I, Var) in
@@ -242,8 +303,10 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
   r.group_size = plan->group_size;
   r.pow2 = pow2;
   r.n_local_threads = nt;
-  r.group_out = ctx->mc_group.as<double>();
+  r.group_out = tail.row ? tail.row : ctx->mc_group.as<double>();
   r.timeline = tail.timeline;
+  r.pass_scalars = sc_u;
+  r.row_tail = tail.row ? reinterpret_cast<unsigned long long*>(tail.row + tail.row_doubles - 2) : nullptr;
   const size_t reduce_smem = reduce_smem_bytes(pow2);
   PCB_TRY(grant_smem(ctx, (const void*)&reduce_kernel, reduce_smem));
   {
@@ -253,44 +316,9 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
     ctx->launches++;
   }
 
-  FinishArgs fa;
-  fa.n_groups = (int)n_groups;
-  if (n_groups > 1024) {  // engine.reduce in group order over more groups than one CTA holds (never with the default plans)
-    if (tail.stop) return fail(ctx, PCB_INVALID, "mcubes_run supports at most 1024 work-groups (%lld requested)", n_groups);
-    double* gi = ctx->mc_group.as<double>() + 2 * n_groups;
-    double* ge = gi + n_groups;
-    deinterleave2_kernel<<<(unsigned)((n_groups + 255) / 256), 256, 0, ctx->stream>>>(ctx->mc_group.as<double>(), (int)n_groups, gi, ge);
-    ctx->launches++;
-    PCB_CUDA_TRY(ctx, cudaGetLastError());
-    PCB_TRY(tree_sum_dev(ctx, gi, n_groups, sc + M_INTEGRAL));
-    PCB_TRY(tree_sum_dev(ctx, ge, n_groups, sc + M_VARIANCE));
-    fa.n_groups = 0;
-  }
-  fa.refine.d = d; fa.refine.n = nb; fa.refine.alpha = tail.alpha; fa.refine.smoothing = tail.smoothing;
-  fa.refine.boundaries = tail.bounds_in; fa.refine.contrib = ctx->mc_contrib.as<double>(); fa.refine.new_boundaries = tail.bounds_out;
-  fa.n_refine = tail.refine ? d : 0;
-  fa.stop = tail.stop;
-  fa.group_pairs = ctx->mc_group.as<double>();
-  fa.scalars = sc_u;
-  fa.hist_i = tail.hist_i;
-  fa.hist_v = tail.hist_v;
-  fa.iteration = tail.iteration;
-  fa.rel_tol = tail.rel_tol;
-  fa.abs_tol = tail.abs_tol;
-  fa.record = tail.record;
-  fa.seq = tail.seq;
-  fa.timeline = tail.timeline;
-  fa.refine.phase_tl = (tail.timeline && tail.iteration == 1) ? tail.timeline + 200 : nullptr;
-  const size_t finish_smem = std::max<size_t>(refine_smem_doubles(nb), 2048) * sizeof(double);
-  if (finish_smem > ctx->smem_optin) return fail(ctx, PCB_INVALID, "n_bins %d too large for on-device refinement", nb);
-  PCB_TRY(grant_smem(ctx, (const void*)&finish_kernel, finish_smem));
-  {
-    void* args[] = {&fa};
-    PCB_CUDA_TRY(ctx, launch_pdl((const void*)&finish_kernel, dim3(fa.n_refine + 1), dim3(512), args, finish_smem, ctx->stream));
-    ctx->launches++;
-  }
   if (n_groups_out) *n_groups_out = n_groups;
-  return PCB_OK;
+  if (tail.defer_finish) return PCB_OK;
+  return enqueue_finish(ctx, plan, tail, n_groups);
 }
 
 static pcb_status arm_pass_scalars(pcb_ctx* ctx) {
@@ -619,6 +647,7 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
         }
       }
     }
+    std::atomic_thread_fence(std::memory_order_acquire);   // the record's fields are read after its sequence word
     return PCB_OK;
   };
 
@@ -725,6 +754,228 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   if (final_boundaries || contributions_out) PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (final_boundaries) std::memcpy(final_boundaries, out_bounds_host, bbytes);
   if (contributions_out) std::memcpy(contributions_out, out_tables_host, (size_t)done * tbytes);
+  return PCB_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// m-Cubes run on a shard of the logical threads (multi-GPU, one context per rank).  The loop stays device-resident
+// exactly like pcb_mcubes_run; the two collectives of an iteration run on the context's stream, between
+//   pass(it)    V-Sample over this rank's work-groups + table merge + the rank's packed row, and
+//   finish(it)  group-order tree over ALL groups from the gathered rows, grid refinement from the all-reduced
+//               table (identical on every rank), iteration record, stop decision.
+// ------------------------------------------------------------------------------------------------
+static __global__ void shard_init_row_kernel(double* row, long long row_doubles) {
+  for (long long i = threadIdx.x; i < row_doubles - 2; i += blockDim.x) row[i] = 0.0;
+  if (threadIdx.x == 0) {
+    unsigned long long* tail = reinterpret_cast<unsigned long long*>(row + row_doubles - 2);
+    tail[0] = ~0ULL;   // no non-finite sample
+    tail[1] = 0ULL;    // no clamp events
+  }
+}
+
+pcb_status pcb_mcubes_shard_begin(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan, int32_t iterations,
+                                  uint64_t seed, int32_t rng_kind, int32_t adapt, double alpha, int32_t smoothing, double rel_tol,
+                                  double abs_tol, int32_t keep_tables, int32_t rank, int32_t world, pcb_mcubes_shard_buffers* out) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  PCB_TRY(validate_plan(ctx, f, plan));
+  if (iterations < 1) return fail(ctx, PCB_INVALID, "iterations must be >= 1");
+  if (!out || world < 1 || rank < 0 || rank >= world) return fail(ctx, PCB_INVALID, "mcubes_shard_begin: bad rank/world or NULL buffers");
+  if (rng_kind != PCB_RNG_REFERENCE_HASH && rng_kind != PCB_RNG_PHILOX) return fail(ctx, PCB_INVALID, "mcubes_run: bad rng kind");
+  if (alpha < 0) return fail(ctx, PCB_INVALID, "alpha must be >= 0");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->mc_shard;
+  S = pcb_ctx::McShard();
+  const int d = plan->d, nb = plan->n_bins;
+  const long long n_threads = (plan->m + plan->s - 1) / plan->s;
+  S.f = *f; S.plan = *plan;
+  S.iterations = iterations; S.rng_kind = rng_kind; S.adapt = adapt; S.smoothing = smoothing;
+  S.alpha = alpha; S.rel_tol = rel_tol; S.abs_tol = abs_tol > 0 ? abs_tol : 0.0;
+  S.seed = seed; S.rank = rank; S.world = world; S.keep_tables = keep_tables;
+  S.n_groups = (n_threads + plan->group_size - 1) / plan->group_size;
+  if (S.n_groups > 1024) return fail(ctx, PCB_INVALID, "sharded mcubes_run supports at most 1024 work-groups (%lld requested)", S.n_groups);
+  // contiguous, near-equal ranges of work-groups per rank (sharded.group_shards)
+  const long long g0 = S.n_groups * rank / world, g1 = S.n_groups * (rank + 1) / world;
+  S.g_count = g1 - g0;
+  S.t_begin = g0 * plan->group_size;
+  S.t_end = std::min<long long>(g1 * plan->group_size, n_threads);
+  S.width = (S.n_groups + world - 1) / world;
+  S.row_doubles = 2 * S.width + 2;
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double), tbytes = (size_t)d * nb * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[0].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_bounds[1].ensure(bbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_contrib.ensure(tbytes));
+  PCB_CUDA_TRY(ctx, ctx->mc_state.ensure(16 + 2 * (size_t)iterations * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->mc_row.ensure((size_t)S.row_doubles * sizeof(double)));
+  if (world > 1) PCB_CUDA_TRY(ctx, ctx->mc_gathered.ensure((size_t)world * S.row_doubles * sizeof(double)));
+  if (keep_tables) PCB_CUDA_TRY(ctx, ctx->mc_tables.ensure((size_t)iterations * tbytes));
+  const size_t out_bytes = (keep_tables ? (size_t)iterations * tbytes : 0) + bbytes;
+  if (ctx->mc_out_cap < out_bytes) {
+    if (ctx->mc_out_pinned) cudaFreeHost(ctx->mc_out_pinned);
+    ctx->mc_out_pinned = nullptr;
+    ctx->mc_out_cap = 0;
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->mc_out_pinned, out_bytes + out_bytes / 4));
+    ctx->mc_out_cap = out_bytes + out_bytes / 4;
+  }
+  if (ctx->mc_records_cap < (size_t)iterations) {
+    if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
+    ctx->mc_records = nullptr;
+    ctx->mc_records_cap = 0;
+    const size_t cap = std::max<size_t>(64, (size_t)iterations);
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->mc_records, cap * sizeof(McRecord)));
+    std::memset(ctx->mc_records, 0, cap * sizeof(McRecord));
+    ctx->mc_records_cap = cap;
+  }
+  while (ctx->mc_events.size() < 2) {
+    cudaEvent_t ev;
+    PCB_CUDA_TRY(ctx, cudaEventCreate(&ev));
+    ctx->mc_events.push_back(ev);
+  }
+  S.token = ++ctx->mc_run_token;
+  PCB_TRY(grant_smem(ctx, (const void*)&run_init_kernel, 0));
+  run_init_kernel<<<d, 256, 0, ctx->stream>>>(nb, ctx->mc_bounds[0].as<double>(), ctx->mc_state.as<int>(),
+                                               ctx->scalars.as<unsigned long long>() + kMcSlot);
+  shard_init_row_kernel<<<1, 256, 0, ctx->stream>>>(ctx->mc_row.as<double>(), S.row_doubles);
+  ctx->launches += 2;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  for (int k = 0; k < 3; ++k) S.span_mark[k] = ctx->spans[k].size();
+  PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[0], ctx->stream));
+  S.live = true;
+  out->stream = (void*)ctx->stream;
+  out->row = ctx->mc_row.as<double>();
+  out->gathered = world > 1 ? ctx->mc_gathered.as<double>() : ctx->mc_row.as<double>();
+  out->table = ctx->mc_contrib.as<double>();
+  out->row_doubles = S.row_doubles;
+  out->table_doubles = (int64_t)d * nb;
+  out->thread_begin = S.t_begin;
+  out->thread_end = S.t_end;
+  return PCB_OK;
+}
+
+static PassTail shard_tail(pcb_ctx* ctx, int it) {
+  auto& S = ctx->mc_shard;
+  const int d = S.plan.d, nb = S.plan.n_bins;
+  PassTail tail;
+  tail.iteration = it;
+  tail.stop = ctx->mc_state.as<int>();
+  tail.refine = S.adapt != 0;
+  tail.alpha = S.alpha;
+  tail.smoothing = S.smoothing;
+  const int cur = S.adapt ? (it & 1) : 0;
+  tail.bounds_in = ctx->mc_bounds[cur].as<double>();
+  tail.bounds_out = ctx->mc_bounds[cur ^ 1].as<double>();
+  tail.contrib_copy = nullptr;   // the per-iteration table is the all-reduced one: copied by finish()
+  tail.hist_i = reinterpret_cast<double*>(ctx->mc_state.as<char>() + 16);
+  tail.hist_v = tail.hist_i + S.iterations;
+  tail.rel_tol = S.rel_tol;
+  tail.abs_tol = S.abs_tol;
+  tail.record = static_cast<McRecord*>(ctx->mc_records) + it;
+  tail.seq = (S.token << 20) | (unsigned long long)(it + 1);
+  tail.row = ctx->mc_row.as<double>();
+  tail.row_doubles = S.row_doubles;
+  tail.defer_finish = true;
+  tail.gathered = S.world > 1 ? ctx->mc_gathered.as<double>() : ctx->mc_row.as<double>();
+  tail.world = S.world;
+  tail.total_groups = S.n_groups;
+  (void)d; (void)nb;
+  return tail;
+}
+
+pcb_status pcb_mcubes_shard_pass(pcb_ctx* ctx, int32_t iteration) {
+  if (!ctx || !ctx->mc_shard.live) return fail(ctx, PCB_INVALID, "no live m-Cubes shard run");
+  auto& S = ctx->mc_shard;
+  if (iteration < 0 || iteration >= S.iterations) return fail(ctx, PCB_INVALID, "iteration %d outside [0, %d)", iteration, S.iterations);
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  if (S.g_count == 0) {   // nothing to sample here: the row keeps (no groups, bad = none, clamps = 0) and the table this rank
+                          // adds to the all-reduce is empty (the buffer holds the previous iteration's global sum)
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(ctx->mc_contrib.p, 0, (size_t)S.plan.d * S.plan.n_bins * sizeof(double), ctx->stream));
+    return PCB_OK;
+  }
+  const PassTail tail = shard_tail(ctx, iteration);
+  const unsigned long long it_seed = derive_seed(S.seed, (unsigned long long)iteration);   // mcubes.py:58-60, 359
+  return enqueue_pass(ctx, &S.f, &S.plan, tail.bounds_in, it_seed, S.rng_kind, nullptr, 1, S.t_begin, S.t_end, tail, nullptr);
+}
+
+pcb_status pcb_mcubes_shard_finish(pcb_ctx* ctx, int32_t iteration) {
+  if (!ctx || !ctx->mc_shard.live) return fail(ctx, PCB_INVALID, "no live m-Cubes shard run");
+  auto& S = ctx->mc_shard;
+  if (iteration < 0 || iteration >= S.iterations) return fail(ctx, PCB_INVALID, "iteration %d outside [0, %d)", iteration, S.iterations);
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const PassTail tail = shard_tail(ctx, iteration);
+  if (S.keep_tables) {
+    const size_t tbytes = (size_t)S.plan.d * S.plan.n_bins * sizeof(double);
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(ctx->mc_tables.as<char>() + (size_t)iteration * tbytes, ctx->mc_contrib.p, tbytes,
+                                      cudaMemcpyDeviceToDevice, ctx->stream));
+  }
+  return enqueue_finish(ctx, &S.plan, tail, S.n_groups);
+}
+
+pcb_status pcb_mcubes_shard_wait(pcb_ctx* ctx, int32_t iteration, pcb_mcubes_iteration* out, int32_t* stop, pcb_nonfinite* bad) {
+  if (!ctx || !ctx->mc_shard.live) return fail(ctx, PCB_INVALID, "no live m-Cubes shard run");
+  auto& S = ctx->mc_shard;
+  if (iteration < 0 || iteration >= S.iterations || !out || !stop) return fail(ctx, PCB_INVALID, "mcubes_shard_wait: bad arguments");
+  const unsigned long long want = (S.token << 20) | (unsigned long long)(iteration + 1);
+  const McRecord* r = static_cast<McRecord*>(ctx->mc_records) + iteration;
+  for (unsigned spin = 0; *(volatile unsigned long long*)&r->seq != want; ++spin) {
+    if ((spin & 0xfff) == 0xfff) {
+      cudaError_t e = cudaStreamQuery(ctx->stream);
+      if (e != cudaErrorNotReady && *(volatile unsigned long long*)&r->seq != want) {
+        if (e == cudaSuccess) return fail(ctx, PCB_CUDA, "mcubes shard run: iteration %d finished without publishing its record", iteration);
+        (void)cudaGetLastError();
+        return fail(ctx, PCB_CUDA, "mcubes shard run: %s", cudaGetErrorString(e));
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const McRecord rec = {r->integral, r->variance, r->clamps, r->bad, r->stop, 0, 0};
+  if (rec.bad != ~0ULL) {
+    cudaStreamSynchronize(ctx->stream);
+    S.live = false;
+    return report_bad_sample(ctx, &S.plan, rec.bad, bad);
+  }
+  out->integral = rec.integral;
+  out->variance = std::fmax(rec.variance, 0.0);
+  out->n_samples = S.plan.m * S.plan.p;
+  out->clamp_events = (int64_t)rec.clamps;
+  *stop = rec.stop;
+  return PCB_OK;
+}
+
+pcb_status pcb_mcubes_shard_end(pcb_ctx* ctx, int32_t n_done, double* contributions_out, double* final_boundaries,
+                                double* seconds_device) {
+  if (!ctx || !ctx->mc_shard.live) return fail(ctx, PCB_INVALID, "no live m-Cubes shard run");
+  auto& S = ctx->mc_shard;
+  S.live = false;
+  if (n_done < 0 || n_done > S.iterations) return fail(ctx, PCB_INVALID, "mcubes_shard_end: n_done outside the run");
+  if (contributions_out && !S.keep_tables) return fail(ctx, PCB_INVALID, "mcubes_shard_end: the run was started without keep_tables");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  PCB_CUDA_TRY(ctx, cudaEventRecord(ctx->mc_events[1], ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // drains the at most one speculative no-op iteration
+  for (int k = 0; k < 3; ++k) {   // profiling spans of passes that never ran are not launches of the hot kernel
+    auto& v = ctx->spans[k];
+    size_t keep = S.span_mark[k];
+    for (size_t i = S.span_mark[k]; i < v.size(); ++i) {
+      if (v[i].tag < n_done) v[keep++] = v[i];
+      else ctx->span_pool.push_back(v[i]);
+    }
+    v.resize(keep);
+  }
+  float ms = 0;
+  PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[1]));
+  if (seconds_device) *seconds_device = ms * 1e-3;
+  const int d = S.plan.d, nb = S.plan.n_bins;
+  const size_t bbytes = (size_t)d * (nb + 1) * sizeof(double), tbytes = (size_t)d * nb * sizeof(double);
+  double* out_bounds_host = static_cast<double*>(ctx->mc_out_pinned);
+  double* out_tables_host = out_bounds_host + (size_t)d * (nb + 1);
+  if (final_boundaries) {
+    const int cur = S.adapt ? (n_done & 1) : 0;
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_bounds_host, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  if (contributions_out && n_done > 0)
+    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_tables_host, ctx->mc_tables.p, (size_t)n_done * tbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (final_boundaries || contributions_out) PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (final_boundaries) std::memcpy(final_boundaries, out_bounds_host, bbytes);
+  if (contributions_out && n_done > 0) std::memcpy(contributions_out, out_tables_host, (size_t)n_done * tbytes);
   return PCB_OK;
 }
 

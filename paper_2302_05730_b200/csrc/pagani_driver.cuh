@@ -291,6 +291,100 @@ __device__ __forceinline__ double tree1024(double v, double* s_warp /* [32] */) 
   return t;
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// Sharded refinement (multi-GPU): the global tree sums of refine (pagani.py:336-337, 371-372) from per-rank pieces.
+// The ordered global list is the concatenation of the ranks' slices.  Every rank packs ONE row per iteration:
+//   header   [0] first non-finite evaluation of its slice (8-byte integer, ~0 = none), [1] n_active, [2] n_retired
+//   section  x 4 (active integrals, active errors, retired integrals, retired errors):
+//            counts [4] = n_head, n_blocks, n_tail, 0;  head[1024]: raw values before the first 1024-aligned GLOBAL
+//            index;  tail[1024]: raw values behind the last complete aligned block;  blocks[width]: pair-tree sums
+//            of the complete aligned 1024-blocks (tree_level_kernel)
+// The rows are all-gathered and every rank rebuilds the ordered list of 1024-block sums (a block that straddles
+// ranks is re-assembled from one tail and the following heads) and finishes the tree: bit-identical to a
+// single-device tree_sum over the concatenation, for any number of ranks.
+// ------------------------------------------------------------------------------------------------------------
+__host__ __device__ inline long long shard_section_doubles(long long width) { return 4 + 2 * kTreeSpan + width; }
+__host__ __device__ inline long long shard_row_doubles(long long width) { return 4 + 4 * shard_section_doubles(width); }
+
+struct ShardPackArgs {
+  double* row;
+  long long width;
+  const double* src[4];
+  long long n[4];        // elements of the section on this rank (0: empty section)
+  long long head[4];     // (-global offset) mod 1024
+  const unsigned long long* bad;
+};
+
+// grid = 4 sections: raw head / tail values and the counts (the block sums are written by tree_level_kernel)
+__global__ void __launch_bounds__(kTreeSpan) shard_pack_kernel(const __grid_constant__ ShardPackArgs a) {
+  const int s = blockIdx.x, t = threadIdx.x;
+  double* sec = a.row + 4 + (long long)s * shard_section_doubles(a.width);
+  const long long n = a.n[s];
+  const long long h = a.head[s] < n ? a.head[s] : n;
+  const long long nb = (n - h) / kTreeSpan, tail = n - h - nb * kTreeSpan;
+  sec[4 + t] = t < h ? a.src[s][t] : 0.0;
+  sec[4 + kTreeSpan + t] = t < tail ? a.src[s][h + nb * kTreeSpan + t] : 0.0;
+  if (t == 0) {
+    sec[0] = (double)h;
+    sec[1] = (double)nb;
+    sec[2] = (double)tail;
+    sec[3] = 0.0;
+    if (s == 0) {
+      *reinterpret_cast<unsigned long long*>(a.row) = *a.bad;
+      a.row[1] = (double)a.n[0];
+      a.row[2] = (double)a.n[2];
+      a.row[3] = 0.0;
+    }
+  }
+}
+
+struct ShardAssembleArgs {
+  const double* gathered;   // world rows
+  int world;
+  long long row_doubles, width;
+  double* lists[4];         // per section: the ordered 1024-block sums of the GLOBAL array
+};
+
+// grid = (world, 4): CTA (r, s) places rank r's complete-block sums of section s at their global block indices and,
+// when r has a tail, re-assembles the block that starts with it (its tail, then the heads of the following ranks)
+__global__ void __launch_bounds__(kTreeSpan) shard_assemble_kernel(const __grid_constant__ ShardAssembleArgs a) {
+  __shared__ double s_warp[32];
+  const int r = blockIdx.x, s = blockIdx.y, t = threadIdx.x;
+  auto section = [&](int q) { return a.gathered + (long long)q * a.row_doubles + 4 + (long long)s * shard_section_doubles(a.width); };
+  long long off = 0;   // global element offset of rank r's slice of this section
+  for (int q = 0; q < r; ++q) {
+    const double* c = section(q);
+    off += (long long)c[0] + (long long)c[1] * kTreeSpan + (long long)c[2];
+  }
+  const double* me = section(r);
+  const long long h = (long long)me[0], nb = (long long)me[1], tail = (long long)me[2];
+  const long long first_block = (off + h) / kTreeSpan;
+  double* list = a.lists[s];
+  for (long long i = t; i < nb; i += kTreeSpan) list[first_block + i] = me[4 + 2 * kTreeSpan + i];
+  if (tail == 0) return;
+  double leaf = 0.0;
+  if (t < tail) {
+    leaf = me[4 + kTreeSpan + t];
+  } else {
+    long long pos = tail;
+    for (int q = r + 1; q < a.world && pos < kTreeSpan; ++q) {
+      const double* c = section(q);
+      const long long hq = (long long)c[0];
+      if (t < pos + hq) { leaf = c[4 + (t - pos)]; break; }
+      pos += hq;
+      if ((long long)c[1] > 0 || (long long)c[2] > 0) break;   // rank q reaches beyond this block: it ends here
+    }
+  }
+  const double sum = tree1024(leaf, s_warp);
+  if (t == 0) list[first_block + nb] = sum;
+}
+
+// (split count, largest error) of the local list, as the two doubles the ranks all-gather
+__global__ void shard_pack_counts_kernel(const unsigned long long* n_split, const double* emax, double* row) {
+  row[0] = (double)*n_split;
+  row[1] = *emax;
+}
+
 __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_constant__ ShortIterArgs a) {
   __shared__ double s_warp[32];
   __shared__ unsigned int s_cnt[32];
@@ -304,6 +398,7 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
   const double sum_e = tree1024(my_e, s_warp);
   const double estimate = a.fin_i + sum_i, errorest = a.fin_e + sum_e;
   const unsigned long long bad = *a.bad;
+  __syncthreads();   // every thread holds the flag before thread 0 may re-arm it below: `action` is CTA-uniform
   int action = 0;
   if (bad != ~0ULL) action = 4;   // the host raises; nothing else matters
   else if (errorest <= tolerance_target(a.rel_tol, a.abs_tol, estimate)) action = 1;

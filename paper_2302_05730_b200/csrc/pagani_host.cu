@@ -5,6 +5,7 @@
 #include "pcb_host.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -364,6 +365,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
           }
         }
       }
+      std::atomic_thread_fence(std::memory_order_acquire);   // the record's fields are read after its sequence word
       if (srec->action == 4)
         return fetch_nonfinite_pagani(ctx, f, rule, ld, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(), srec->bad, bad);
       estimate = srec->estimate;
@@ -511,7 +513,11 @@ static int grid_for(long long n) { return (int)std::max<long long>(1, std::min<l
 static pcb_status shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad) {
   auto& S = ctx->shard;
   S.classified = false;
-  if (S.n == 0) return PCB_OK;
+  if (S.n == 0) {
+    if (S.deferred)   // an empty slice reports "no non-finite evaluation"
+      PCB_CUDA_TRY(ctx, cudaMemsetAsync(ctx->scalars.as<unsigned long long>() + S_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+    return PCB_OK;
+  }
   PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)S.n * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)S.n * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)S.n * sizeof(int32_t)));
@@ -519,6 +525,7 @@ static pcb_status shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad) {
   PCB_CUDA_TRY(ctx, cudaMemsetAsync(bad_dev, 0xFF, sizeof(unsigned long long), ctx->stream));
   PCB_TRY(evaluate_launch(ctx, &S.f, &S.rule, &S.cfg, S.n, S.ld, ctx->lefts[S.cur].as<double>(), ctx->lengths[S.cur].as<double>(),
                           ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), bad_dev));
+  if (S.deferred) return PCB_OK;   // the flag is packed into the next row (pcb_pagani_shard_pack)
   PCB_TRY(read_scalars(ctx, S_BAD, 1));
   const unsigned long long flat = ((unsigned long long*)ctx->pinned)[S_BAD];
   if (flat != ~0ULL)
@@ -534,7 +541,9 @@ pcb_status pcb_pagani_shard_init(pcb_ctx* ctx, const pcb_integrand* f, const pcb
   if (g < 1 || first < 0 || count < 0) return fail(ctx, PCB_INVALID, "shard_init: bad tiling slice");
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   auto& S = ctx->shard;
+  const bool deferred = S.deferred;   // set by pcb_pagani_shard_deferred before init
   S = pcb_ctx::Shard();
+  S.deferred = deferred;
   S.live = true;
   S.f = *f; S.rule = *rule; S.cfg = *cfg;
   S.n = count;
@@ -661,7 +670,7 @@ pcb_status pcb_pagani_shard_split(pcb_ctx* ctx) {
   S.ld = ld_out;
   S.cur = nxt;
   S.classified = false;
-  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  if (!S.deferred) PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return PCB_OK;
 }
 
@@ -734,6 +743,188 @@ pcb_status pcb_pagani_shard_evaluate(pcb_ctx* ctx, pcb_nonfinite* bad) {
   if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   return shard_evaluate(ctx, bad);
+}
+
+// ---- device-collective mode: the pieces of an iteration stay in device buffers that the ranks exchange with NCCL ----
+pcb_status pcb_pagani_shard_deferred(pcb_ctx* ctx, int32_t on) {
+  if (!ctx) return PCB_INVALID;
+  ctx->shard.deferred = on != 0;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_pack(pcb_ctx* ctx, int64_t head_active, int64_t head_retired, int32_t with_retired, int64_t width,
+                                 int32_t world, pcb_pagani_shard_rows* out) {
+  if (!ctx || !ctx->shard.live || !out) return fail(ctx, PCB_INVALID, "no live shard");
+  if (head_active < 0 || head_active >= kTreeSpan || head_retired < 0 || head_retired >= kTreeSpan || width < 1 || world < 1)
+    return fail(ctx, PCB_INVALID, "shard_pack: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  const long long n_ret = with_retired ? S.n_ret : 0;
+  if (S.n / kTreeSpan + 1 > width || n_ret / kTreeSpan + 1 > width) return fail(ctx, PCB_INVALID, "shard_pack: width %lld too small", (long long)width);
+  const long long row_doubles = shard_row_doubles(width);
+  PCB_CUDA_TRY(ctx, ctx->pg_row.ensure((size_t)row_doubles * sizeof(double)));
+  if (world > 1) PCB_CUDA_TRY(ctx, ctx->pg_gathered.ensure((size_t)world * row_doubles * sizeof(double)));
+  S.width = width;
+  ShardPackArgs pa;
+  pa.row = ctx->pg_row.as<double>();
+  pa.width = width;
+  pa.src[0] = ctx->est_i.as<double>(); pa.src[1] = ctx->est_e.as<double>();
+  pa.src[2] = ctx->ret_i.as<double>(); pa.src[3] = ctx->ret_e.as<double>();
+  pa.n[0] = pa.n[1] = S.n;
+  pa.n[2] = pa.n[3] = n_ret;
+  pa.head[0] = pa.head[1] = head_active;
+  pa.head[2] = pa.head[3] = head_retired;
+  pa.bad = ctx->scalars.as<unsigned long long>() + S_BAD;
+  shard_pack_kernel<<<4, kTreeSpan, 0, ctx->stream>>>(pa);
+  ctx->launches++;
+  for (int s = 0; s < 4; ++s) {
+    const long long n = pa.n[s], h = std::min<long long>(pa.head[s], n), nb = (n - h) / kTreeSpan;
+    if (nb > 0) {
+      double* blocks = pa.row + 4 + (long long)s * shard_section_doubles(width) + 4 + 2 * kTreeSpan;
+      tree_level_kernel<<<(unsigned)nb, kTreeBlock, 0, ctx->stream>>>(pa.src[s] + h, nb * kTreeSpan, blocks);
+      ctx->launches++;
+    }
+  }
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  out->stream = (void*)ctx->stream;
+  out->row = ctx->pg_row.as<double>();
+  out->gathered = world > 1 ? ctx->pg_gathered.as<double>() : ctx->pg_row.as<double>();
+  out->row_doubles = row_doubles;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_global_sums(pcb_ctx* ctx, int32_t world, int64_t n_active_total, int64_t n_retired_total,
+                                        double sums[4], int32_t* bad_rank) {
+  if (!ctx || !ctx->shard.live || !sums || !bad_rank) return fail(ctx, PCB_INVALID, "no live shard");
+  if (world < 1 || world > 1024 || n_active_total < 0 || n_retired_total < 0) return fail(ctx, PCB_INVALID, "shard_global_sums: bad arguments");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  const long long row_doubles = shard_row_doubles(S.width);
+  const double* gathered = world > 1 ? ctx->pg_gathered.as<double>() : ctx->pg_row.as<double>();
+  const long long totals[4] = {n_active_total, n_active_total, n_retired_total, n_retired_total};
+  const long long cap = std::max<long long>(1, (std::max(n_active_total, n_retired_total) + kTreeSpan - 1) / kTreeSpan);
+  PCB_CUDA_TRY(ctx, ctx->pg_lists.ensure((size_t)4 * cap * sizeof(double)));
+  ShardAssembleArgs aa;
+  aa.gathered = gathered;
+  aa.world = world;
+  aa.row_doubles = row_doubles;
+  aa.width = S.width;
+  for (int s = 0; s < 4; ++s) aa.lists[s] = ctx->pg_lists.as<double>() + (size_t)s * cap;
+  shard_assemble_kernel<<<dim3((unsigned)world, 4), kTreeSpan, 0, ctx->stream>>>(aa);
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  double* sc = ctx->scalars.as<double>();
+  const int slot[4] = {S_SUM_I, S_SUM_E, S_RET_I, S_RET_E};
+  for (int s = 0; s < 4; ++s)
+    PCB_TRY(tree_sum_dev(ctx, aa.lists[s], (totals[s] + kTreeSpan - 1) / kTreeSpan, sc + slot[s]));
+  // the ranks' non-finite flags: header word 0 of every row
+  unsigned long long* flags = (unsigned long long*)ctx->pinned + 64;
+  PCB_CUDA_TRY(ctx, cudaMemcpy2DAsync(flags, sizeof(unsigned long long), gathered, (size_t)row_doubles * sizeof(double),
+                                      sizeof(unsigned long long), (size_t)world, cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_TRY(read_scalars(ctx, 0, 8));
+  const double* host = (const double*)ctx->pinned;
+  for (int s = 0; s < 4; ++s) sums[s] = host[slot[s]];
+  *bad_rank = -1;
+  for (int r = 0; r < world; ++r)
+    if (flags[r] != ~0ULL) { *bad_rank = r; break; }
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_nonfinite(pcb_ctx* ctx, pcb_nonfinite* bad) {
+  if (!ctx || !ctx->shard.live || !bad) return fail(ctx, PCB_INVALID, "no live shard");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  PCB_TRY(read_scalars(ctx, S_BAD, 1));
+  const unsigned long long flat = ((unsigned long long*)ctx->pinned)[S_BAD];
+  if (flat == ~0ULL) return fail(ctx, PCB_INVALID, "shard_nonfinite: this rank holds no non-finite evaluation");
+  return fetch_nonfinite_pagani(ctx, &S.f, &S.rule, S.ld, ctx->lefts[S.cur].as<double>(), ctx->lengths[S.cur].as<double>(), flat, bad);
+}
+
+pcb_status pcb_pagani_shard_classify_dev(pcb_ctx* ctx, double budget, int32_t mode, double emax, int32_t world, double** row,
+                                         double** gathered) {
+  if (!ctx || !ctx->shard.live || !row || !gathered || world < 1) return fail(ctx, PCB_INVALID, "no live shard");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  auto& S = ctx->shard;
+  S.n_split = 0;
+  S.classified = true;
+  PCB_CUDA_TRY(ctx, ctx->pg_rowb.ensure((size_t)(2 + 2 * world) * sizeof(double)));
+  double* sc = ctx->scalars.as<double>();
+  unsigned long long* sc_u = ctx->scalars.as<unsigned long long>();
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc + S_EMAX, 0, sizeof(double), ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc_u + S_NSPLIT, 0, sizeof(unsigned long long), ctx->stream));
+  if (S.n > 0) {
+    const long long nblk = (S.n + kScanBlock - 1) / kScanBlock;
+    PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)S.n));
+    PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));
+    PCB_CUDA_TRY(ctx, ctx->offsets.ensure((size_t)nblk * sizeof(unsigned long long)));
+    ClassifyArgs ca;
+    ca.n = S.n; ca.ld = S.ld; ca.d = S.f.d; ca.mode = mode; ca.budget = budget; ca.emax = emax;
+    ca.lengths = ctx->lengths[S.cur].as<double>();
+    ca.errors = ctx->est_e.as<double>();
+    ca.flags = ctx->flags.as<unsigned char>();
+    ca.block_counts = ctx->counts.as<unsigned int>();
+    classify_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(ca);
+    scan_counts_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->counts.as<unsigned int>(), (int)nblk, ctx->offsets.as<unsigned long long>(),
+                                                    sc_u + S_NSPLIT);
+    max_kernel<<<(unsigned)std::min<long long>((S.n + 255) / 256, 1024), 256, 0, ctx->stream>>>(ctx->est_e.as<double>(), S.n, sc + S_EMAX);
+    ctx->launches += 3;
+  }
+  shard_pack_counts_kernel<<<1, 1, 0, ctx->stream>>>(sc_u + S_NSPLIT, sc + S_EMAX, ctx->pg_rowb.as<double>());
+  ctx->launches++;
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  *row = ctx->pg_rowb.as<double>();
+  *gathered = world > 1 ? ctx->pg_rowb.as<double>() + 2 : ctx->pg_rowb.as<double>();
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_split_dev(pcb_ctx* ctx, int64_t n_split) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  if (!S.classified) return fail(ctx, PCB_INVALID, "shard_split needs a preceding shard_classify");
+  if (n_split < 0 || n_split > S.n) return fail(ctx, PCB_INVALID, "shard_split_dev: split count outside the local list");
+  S.n_split = n_split;
+  return pcb_pagani_shard_split(ctx);
+}
+
+pcb_status pcb_pagani_shard_list_dev(pcb_ctx* ctx, double** lefts, double** lengths, int64_t* n, int64_t* ld) {
+  if (!ctx || !ctx->shard.live || !lefts || !lengths || !n || !ld) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  *lefts = ctx->lefts[S.cur].as<double>();
+  *lengths = ctx->lengths[S.cur].as<double>();
+  *n = S.n;
+  *ld = S.ld;
+  return PCB_OK;
+}
+
+pcb_status pcb_pagani_shard_rebuild_dev(pcb_ctx* ctx, int64_t keep_begin, int64_t keep_end, int64_t n_front, const double* front_dev,
+                                        int64_t n_back, const double* back_dev) {
+  if (!ctx || !ctx->shard.live) return fail(ctx, PCB_INVALID, "no live shard");
+  auto& S = ctx->shard;
+  if (keep_begin < 0 || keep_end > S.n || keep_begin > keep_end || n_front < 0 || n_back < 0)
+    return fail(ctx, PCB_INVALID, "shard_rebuild_dev: bad ranges");
+  if ((n_front > 0 && !front_dev) || (n_back > 0 && !back_dev)) return fail(ctx, PCB_INVALID, "shard_rebuild_dev: NULL rows");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = S.f.d, nxt = S.cur ^ 1;
+  const long long keep = keep_end - keep_begin, n_new = n_front + keep + n_back;
+  if (n_front == 0 && n_back == 0 && keep_begin == 0 && keep_end == S.n) return PCB_OK;  // nothing moves
+  const long long ld_new = round_up(std::max<long long>(n_new, 1), 32);
+  PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_new * d * sizeof(double)));
+  PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_new * d * sizeof(double)));
+  auto place = [&](long long n, long long ld_src, long long src_off, const double* l_src, const double* h_src, long long dst_off) {
+    if (n == 0) return;
+    soa_copy_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, n, ld_src, src_off, l_src, ld_new, dst_off, ctx->lefts[nxt].as<double>());
+    soa_copy_kernel<<<grid_for(n), 256, 0, ctx->stream>>>(d, n, ld_src, src_off, h_src, ld_new, dst_off, ctx->lengths[nxt].as<double>());
+    ctx->launches += 2;
+  };
+  // received blocks are [2][d][n]: lefts then lengths, structure of arrays with leading dimension n
+  place(n_front, n_front, 0, front_dev, front_dev + (size_t)d * n_front, 0);
+  place(keep, S.ld, keep_begin, ctx->lefts[S.cur].as<double>(), ctx->lengths[S.cur].as<double>(), n_front);
+  place(n_back, n_back, 0, back_dev, back_dev + (size_t)d * n_back, n_front + keep);
+  PCB_CUDA_TRY(ctx, cudaGetLastError());
+  S.cur = nxt;
+  S.n = n_new;
+  S.ld = ld_new;
+  return PCB_OK;
 }
 
 // quadrature.apply_rules for a single region: generic table, plain pair tree over all points.

@@ -16,12 +16,22 @@
 
 namespace pcb {
 
+// Device scratch buffer of a context.  Memory comes from the device's stream-ordered pool on the context's stream
+// (cudaMallocAsync / cudaFreeAsync; the pool's release threshold is raised to "never" at context creation), so
+// growing a buffer in the middle of a refinement neither synchronises the device nor returns memory to the
+// driver: a released block is reused by the next request of the same stream -- in this call or in the next one.
+// (Round 1 used cudaFree + cudaMalloc here: a device-wide synchronisation and a driver allocation per growth step,
+// up to 17x on a cold refine().)
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  const cudaStream_t* stream = nullptr;   // the owning context's stream (set by pcb_ctx's constructor)
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (stream && *stream) cudaFreeAsync(p, *stream);
+      else cudaFree(p);
+    }
     p = nullptr;
     cap = 0;
   }
@@ -30,10 +40,11 @@ struct DevBuf {
     if (bytes <= cap) return cudaSuccess;
     release();
     size_t want = bytes + bytes / 8 + 256;
-    cudaError_t e = cudaMalloc(&p, want);
+    auto get = [&](size_t n) { return (stream && *stream) ? cudaMallocAsync(&p, n, *stream) : cudaMalloc(&p, n); };
+    cudaError_t e = get(want);
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
-      e = cudaMalloc(&p, bytes);
+      e = get(bytes);
       want = bytes;
     }
     if (e == cudaSuccess) cap = want;
@@ -73,7 +84,10 @@ struct pcb_ctx {
     int cur = 0;
     long long n = 0, ld = 0, n_ret = 0, n_split = 0;
     bool classified = false;
+    bool deferred = false;   // device-collective mode: init/evaluate enqueue only; the non-finite flag travels in the packed row
+    long long width = 0;     // block-sum capacity of the current packed row
   } shard;
+  pcb::DevBuf pg_row, pg_gathered, pg_lists, pg_rowb;
   // roofline profiling (pcb_profile_begin/end)
   bool profiling = false;
   struct Span { cudaEvent_t a, b; double units; int tag; };
@@ -89,6 +103,33 @@ struct pcb_ctx {
   unsigned long long mc_run_token = 0;
   std::vector<cudaEvent_t> mc_events;
   std::map<std::array<long long, 6>, unsigned long long> mc_multipliers;  // lane -> segment map, per plan
+  // sharded m-Cubes run (pcb_mcubes_shard_*): state between begin and end
+  struct McShard {
+    bool live = false;
+    pcb_integrand f;
+    pcb_mcubes_plan plan;
+    int iterations = 0, rng_kind = 0, adapt = 1, smoothing = 1, rank = 0, world = 1, keep_tables = 0;
+    double alpha = 1.5, rel_tol = 0.0, abs_tol = 0.0;
+    unsigned long long seed = 0, token = 0;
+    long long t_begin = 0, t_end = 0, n_groups = 0, g_count = 0, width = 0, row_doubles = 0;
+    size_t span_mark[3] = {0, 0, 0};
+  } mc_shard;
+  pcb::DevBuf mc_row, mc_gathered;
+
+  std::vector<pcb::DevBuf*> buffers() {
+    return {&lefts[0], &lefts[1], &lengths[0], &lengths[1], &est_i, &est_e, &est_k, &flags, &counts, &offsets,
+            &ret_i, &ret_e, &tree[0], &tree[1], &scalars, &rows_a, &rows_b, &k64, &mc_bounds[0], &mc_bounds[1],
+            &mc_hist, &mc_contrib, &mc_seg, &mc_group, &mc_tmp, &mc_inject, &mc_state, &mc_tables, &mc_timeline, &mc_row,
+            &mc_gathered, &pg_row, &pg_gathered, &pg_lists, &pg_rowb};
+  }
+  pcb_ctx() {
+    for (pcb::DevBuf* b : buffers()) b->stream = &stream;
+  }
+  void release_buffers() {
+    for (pcb::DevBuf* b : buffers()) b->release();
+  }
+  pcb_ctx(const pcb_ctx&) = delete;
+  pcb_ctx& operator=(const pcb_ctx&) = delete;
 };
 
 namespace pcb {

@@ -20,8 +20,16 @@ partition reproduces the reference's sample set.  Per iteration the ranks exchan
 and then run the identical grid refinement.  Messages are <= 32 KB + 4 KB: latency-bound,
 NCCL over NVLink/NVSwitch (or gloo on CPU in the tests).
 
-The compute backend is injectable so the CPU test-suite can drive this logic with the
-oracle under gloo; the product backend below is the CUDA library and nothing else.
+Product path: the collectives run on DEVICE buffers of the library, on the library's own stream
+(torch.cuda.ExternalStream), so nothing is staged through the host and the m-Cubes loop stays
+device-resident -- per iteration one all-gather of a (2*ceil(G/W)+2)-double row and one all-reduce
+of the table, enqueued between `pass` and `finish` of pcb_mcubes_shard_*; the host enqueues
+iteration it+1 before it polls the record of iteration it.  PAGANI: one all-gather of the packed
+tree pieces and one of (split count, max error) per iteration, region rows move rank-to-rank
+with NCCL send/recv straight between the device lists.
+
+The compute backend is injectable so the CPU test-suite can drive the partition logic with the
+oracle under gloo (host arrays); the product backend is the CUDA library and nothing else.
 """
 
 from __future__ import annotations
@@ -84,6 +92,30 @@ class Comm:
     def barrier(self):
         self._dist.barrier(group=self.group)
 
+    # ---- tensor-level collectives: operate in place on the tensors given (device buffers of the library under NCCL,
+    #      CPU tensors under gloo), ordered on the current torch stream, no host staging
+    def all_gather_into(self, out, inp):
+        """out[r*n:(r+1)*n] = inp of rank r (n = inp.numel()); out may alias inp at its own slot."""
+        if self.world == 1 and out.data_ptr() == inp.data_ptr() and self._dist.get_backend(self.group) != "nccl":
+            return
+        self._dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def all_reduce_sum_(self, t):
+        self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self.group)
+
+    def all_reduce_max_(self, t):
+        self._dist.all_reduce(t, op=self._dist.ReduceOp.MAX, group=self.group)
+
+    def exchange_tensors(self, sends: dict, recvs: dict):
+        """Point-to-point exchange of device tensors: sends[r] = tensor for rank r, recvs[r] = preallocated tensor to
+        fill from rank r (NCCL send/recv, one batched group)."""
+        dist = self._dist
+        ops = [dist.P2POp(dist.isend, t, r, group=self.group) for r, t in sends.items()]
+        ops += [dist.P2POp(dist.irecv, t, r, group=self.group) for r, t in recvs.items()]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
     def exchange_rows(self, sends: dict, recvs: dict, d: int) -> dict:
         """Point-to-point exchange of region rows: sends[r] = (lefts, lengths) for rank r, recvs[r] = row
         count expected from rank r.  Returns {r: (lefts, lengths)}.  (NCCL send/recv on GPUs, gloo on CPU.)"""
@@ -126,22 +158,83 @@ def mcubes_iteration_sharded(spec, plan, boundaries, seed, comm, backend, rng_ki
     return integral, variance, packed[:-1].reshape(contrib.shape), int(round(packed[-1]))
 
 
+def _device_tensor(view, device):
+    import torch
+
+    return torch.as_tensor(view, device=torch.device("cuda", device))
+
+
+def _mcubes_run_device(spec, plan, iterations, comm, params, seed, n_bins, adapt, progress, rel_tol, abs_tol, rng_kind,
+                       device, force_collectives, ctx=None):
+    """The product path: device-resident loop, collectives on the library's buffers and stream."""
+    import torch
+
+    run = _native.McubesShardRun(spec, plan, n_bins, iterations, seed, rng_kind, adapt, params.alpha, params.smoothing,
+                                 0.0 if rel_tol is None else float(rel_tol), 0.0 if abs_tol is None else float(abs_tol),
+                                 True, comm.rank, comm.world, device=device, ctx=ctx)
+    dev = run.ctx.device
+    row, gathered, table = (_device_tensor(v, dev) for v in (run.row, run.gathered, run.table))
+    collect = comm.world > 1 or force_collectives
+    history, records = [], []
+
+    def enqueue(it):
+        run.enqueue_pass(it)
+        if collect:
+            comm.all_gather_into(gathered, row)
+            comm.all_reduce_sum_(table)
+        run.enqueue_finish(it)
+
+    with torch.cuda.stream(torch.cuda.ExternalStream(run.stream, device=torch.device("cuda", dev))):
+        enqueue(0)
+        enqueued = 1
+        for it in range(iterations):
+            if enqueued < iterations:      # the device never waits for the host: iteration it+1 is already queued
+                enqueue(enqueued)
+                enqueued += 1
+            rec, stop = run.wait(it)
+            records.append((rec.integral, rec.variance, int(rec.n_samples), int(rec.clamp_events)))
+            if progress is not None:
+                est, err, chi2 = combine_iterations([McubesIterationResult(i, v, None, ns, c) for i, v, ns, c in records])
+                progress({"iteration": it, "estimate": est, "errorest": err, "chi2_per_dof": chi2,
+                          "iter_integral": rec.integral, "iter_sd": math.sqrt(rec.variance)})
+            if stop:
+                break
+        contribs, _final_b, _secs = run.end(len(records))
+    for k, (i, v, ns, c) in enumerate(records):
+        history.append(McubesIterationResult(i, v, _table(plan.d, n_bins, contribs[k]), ns, c))
+    est, err, chi2 = combine_iterations(history)
+    return MonteCarloResult(est, err, chi2, history, plan)
+
+
 def mcubes_run_sharded(f, n, d, iterations, comm, backend=None, params=None, seed=0, n_bins=500, group_size=128,
-                       target_groups=256, adapt=True, progress=None, rel_tol=None, rng="reference-hash", abs_tol=None):
+                       target_groups=256, adapt=True, progress=None, rel_tol=None, rng="reference-hash", abs_tol=None,
+                       device=None, force_collectives=False, ctx=None):
     """mcubes.run (mcubes.py:332-382) with the sub-cubes sharded over comm.world GPUs.
 
-    Every rank returns the same MonteCarloResult; (integral, variance) per iteration are
-    bit-identical to the single-GPU run, the contribution tables agree to summation order.
+    Every rank returns the same MonteCarloResult.  (integral, variance) of iteration 0 are bit-identical to the
+    single-GPU run for any GPU count (same samples, same per-group partials, same group-order tree); the
+    contribution tables agree to summation order (an all-reduce instead of the single-GPU merge order), so the
+    refined grids and hence iterations >= 1 agree to rounding.  A non-finite sample raises the same
+    GroupTaskError on every rank (the flag travels in the gathered rows).
+
+    `backend=None` is the product path (CUDA library, device-resident loop, collectives on device buffers; `ctx`
+    selects the library context, default the process-wide one of `device`; `force_collectives` issues the
+    collectives even for one rank); an injected backend (the CPU test-suite's oracle) takes the host-array path below.
     """
-    from .stratified import RNG_KINDS
+    from .stratified import RNG_KINDS, _raise_nonfinite
 
     if iterations < 1:
         raise ValueError("iterations must be >= 1")
-    backend = backend or CudaBackend()
     params = params or GridRefineParams()
     plan = make_plan(n, d, group_size=group_size, target_groups=target_groups)
-    boundaries = np.array(init_grid(d, n_bins).boundaries)
     spec = f.device_spec() if hasattr(f, "device_spec") else f
+    if backend is None:
+        try:
+            return _mcubes_run_device(spec, plan, iterations, comm, params, seed, n_bins, adapt, progress, rel_tol, abs_tol,
+                                      RNG_KINDS[rng], device, force_collectives, ctx)
+        except _native.NonFiniteStatus as exc:
+            _raise_nonfinite(exc, plan)
+    boundaries = np.array(init_grid(d, n_bins).boundaries)
     history = []
     for it in range(iterations):
         integral, variance, contrib, clamps = mcubes_iteration_sharded(
@@ -237,11 +330,163 @@ def rebalance(comm, shard, counts):
     return [b - a for a, b in target]
 
 
-def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None):
+def rebalance_device(comm, shard, counts, device):
+    """rebalance() with the rows travelling device to device: slices of the local structure-of-arrays list are sent
+    as [2][d][n] blocks (lefts, lengths) and the new list is assembled on the device (pcb_pagani_shard_rebuild_dev)."""
+    import torch
+
+    offsets, total = _offsets(counts)
+    me, world = comm.rank, comm.world
+    target = _even_ranges(total, world)
+    if all(offsets[r] == target[r][0] and counts[r] == target[r][1] - target[r][0] for r in range(world)):
+        return counts
+    my0, my1 = offsets[me], offsets[me] + counts[me]
+    t0, t1 = target[me]
+    d = shard.d
+    sends, recvs = {}, {}
+    if my1 > my0:
+        lv, hv, _n, ld = shard.list_dev()
+        lefts = _device_tensor(lv, device).view(d, ld)
+        lengths = _device_tensor(hv, device).view(d, ld)
+    for r in range(world):           # my rows that belong to rank r
+        a, b = max(my0, target[r][0]), min(my1, target[r][1])
+        if r != me and a < b:
+            sends[r] = torch.stack([lefts[:, a - my0:b - my0], lengths[:, a - my0:b - my0]]).contiguous()
+    for r in range(world):           # rows of rank r that belong to me
+        a, b = max(offsets[r], t0), min(offsets[r] + counts[r], t1)
+        if r != me and a < b:
+            recvs[r] = torch.empty((2, d, b - a), dtype=torch.float64, device=torch.device("cuda", device))
+    comm.exchange_tensors(sends, recvs)
+    keep0, keep1 = max(my0, t0), min(my1, t1)
+
+    def cat(parts):
+        if not parts:
+            return None
+        return parts[0] if len(parts) == 1 else torch.cat(parts, dim=2).contiguous()
+
+    front = cat([recvs[r] for r in sorted(recvs) if r < me])
+    back = cat([recvs[r] for r in sorted(recvs) if r > me])
+    kb, ke = (keep0 - my0, keep1 - my0) if keep0 < keep1 else (0, 0)
+    shard.rebuild_dev(kb, ke, 0 if front is None else front.shape[2], 0 if front is None else front.data_ptr(),
+                      0 if back is None else back.shape[2], 0 if back is None else back.data_ptr())
+    return [b - a for a, b in target]
+
+
+def _pagani_refine_device(f, cfg, comm, shard, progress, force_collectives):
+    """The product path: every per-iteration exchange is a collective on device buffers of the library, issued on the
+    library's stream; the host reads four sums and 2*world small numbers per iteration (the same two round trips the
+    single-GPU driver makes)."""
+    import torch
+
+    from .cubature import IntegralResult
+    from .domain import BudgetExceededError, NonFiniteEvaluationError
+    from .execution import GroupTaskError
+
+    d, world, me = shard.d, comm.world, comm.rank
+    dev = shard.ctx.device
+    collect = world > 1 or force_collectives
+    g = 1
+    while g**d < cfg.initial_regions:
+        g += 1
+    n0 = g**d
+    if n0 > cfg.region_cap:
+        raise BudgetExceededError(f"uniform split needs {n0} regions, cap is {cfg.region_cap}")
+    shard.deferred(True)
+    first, last = _even_ranges(n0, world)[me]
+    counts = [b - a for a, b in _even_ranges(n0, world)]
+    fin_i = fin_e = 0.0
+    fin_count, processed = 0, n0
+    history, converged, reason = [], False, ""
+    ret_counts = None
+    abs_tol = getattr(cfg, "abs_tol", 0.0)
+    stream = None
+
+    def on_stream():
+        return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", dev)))
+
+    try:
+        shard.init(g, first, last - first)
+        for iteration in range(cfg.max_iterations + 1):
+            with_ret = ret_counts is not None
+            offs, n_active = _offsets(counts)
+            head_a = (-offs[me]) % TREE_SPAN
+            head_r = (-_offsets(ret_counts)[0][me]) % TREE_SPAN if with_ret else 0
+            width = max(max(counts), max(ret_counts) if with_ret else 0) // TREE_SPAN + 1
+            stream, row, gathered = shard.pack(head_a, head_r, with_ret, width, world)
+            if collect:
+                with on_stream():
+                    comm.all_gather_into(_device_tensor(gathered, dev), _device_tensor(row, dev))
+            sums, bad_rank = shard.global_sums(world, n_active, sum(ret_counts) if with_ret else 0)
+            if bad_rank >= 0:
+                # the owner looks the evaluation up; every rank raises the single-GPU error (pagani.py:206-209)
+                detail = np.zeros(3 + d)
+                if bad_rank == me:
+                    region, point, value, x = shard.nonfinite()
+                    detail[:3] = offs[me] + region, point, value
+                    detail[3:] = x
+                detail = comm.allgather(detail)[bad_rank] if world > 1 else detail
+                cause = NonFiniteEvaluationError(detail[3:], float(detail[2]), region_index=int(detail[0]))
+                raise GroupTaskError(int(detail[0]) // cfg.chunk, cause) from cause
+            if with_ret:                                    # fin += tree_sum(act[~mask]) of the last split
+                fin_i += sums[2]
+                fin_e += sums[3]
+                ret_counts = None
+            estimate = fin_i + sums[0]
+            errorest = fin_e + sums[1]
+            history.append((estimate, errorest, fin_count + n_active))
+            if progress is not None:
+                progress({"iteration": iteration, "n_regions": fin_count + n_active, "active": n_active,
+                          "estimate": estimate, "errorest": errorest})
+            rel_target = cfg.rel_tol * abs(estimate)
+            if errorest <= (abs_tol if abs_tol > rel_target else rel_target):
+                converged, reason = True, "tolerance met"
+                break
+            if iteration == cfg.max_iterations:
+                reason = "max iterations reached"
+                break
+            if n_active == 0:
+                reason = "no active regions left"
+                break
+            budget = 0.8 * abs_tol if abs_tol > rel_target else 0.8 * cfg.rel_tol * abs(estimate)
+
+            def classify(mode, emax):
+                rowb, gatheredb = shard.classify_dev(budget, mode, emax, world)
+                with on_stream():
+                    gt = _device_tensor(gatheredb, dev)
+                    if collect:
+                        comm.all_gather_into(gt, _device_tensor(rowb, dev))
+                    vals = gt.cpu().numpy().reshape(world, 2)
+                return [int(round(v)) for v in vals[:, 0]], float(vals[:, 1].max())
+
+            split_counts, emax = classify(0, 0.0)
+            if sum(split_counts) == 0:                      # force progress on the globally worst regions
+                split_counts, _ = classify(1, emax)
+            n_split = sum(split_counts)
+            if processed + 2 * n_split > cfg.region_cap:
+                reason = "region cap reached"
+                break
+            shard.split_dev(split_counts[me])
+            ret_counts = [c - s for c, s in zip(counts, split_counts)]
+            fin_count += n_active - n_split
+            processed += 2 * n_split
+            with on_stream():
+                counts = rebalance_device(comm, shard, [2 * s for s in split_counts], dev)
+            shard.evaluate()
+    finally:
+        shard.deferred(False)
+    return IntegralResult(estimate, errorest, len(history) - 1, processed, converged, history, reason)
+
+
+def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None, force_collectives=False, host_staged=False):
     """refine (pagani.py:300-391) with the region list sharded over comm.world GPUs.
 
     Every rank returns the same IntegralResult; histories are bit-identical to the single-GPU run
-    for any world size (same per-region values, same global pair trees, same classification).
+    for any world size (same per-region values, same global pair trees, same classification).  A non-finite
+    evaluation raises the single-GPU GroupTaskError on every rank.
+
+    Product path (`shard` a `_native.PaganiShard` or None): collectives on device buffers, see
+    `_pagani_refine_device`.  A shard object without the device entry points (the CPU test-suite's oracle shard) or
+    `host_staged=True` takes the host-array path below, which exchanges the same pieces as numpy arrays.
     """
     from .cubature import IntegralResult, PaganiConfig
     from .rules import build_rule, orbit_form
@@ -249,6 +494,8 @@ def pagani_refine_sharded(f, cfg, comm, shard=None, rule=None, progress=None):
     cfg = cfg or PaganiConfig()
     if shard is None:
         shard = _native.PaganiShard(f.device_spec(), orbit_form(rule or build_rule(f.d)), cfg)
+    if isinstance(shard, _native.PaganiShard) and not host_staged:
+        return _pagani_refine_device(f, cfg, comm, shard, progress, force_collectives)
     d = shard.d
     g = 1
     while g**d < cfg.initial_regions:

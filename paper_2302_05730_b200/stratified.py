@@ -15,7 +15,7 @@ import numpy as np
 from . import _native
 from .domain import Integrand, NonFiniteEvaluationError, _Frozen, check_dimension
 from .execution import ExecConfig, GroupTaskError
-from .vegas import BinContributions, GridRefineParams, VegasGrid, init_grid
+from .vegas import BinContributions, GridRefineParams, VegasGrid, check_grid_shape, init_grid
 
 _MASK64 = (1 << 64) - 1
 _GOLDEN = 0x9E3779B97F4A7C15
@@ -239,7 +239,7 @@ def run(f: Integrand, n, d: int, iterations: int, params: GridRefineParams | Non
         raise ValueError("plan, grid, and integrand dimensions must agree")
     params = params or GridRefineParams()
     plan = make_plan(n, d, group_size=group_size, target_groups=target_groups)
-    init_grid(d, n_bins)  # argument validation as in the reference
+    check_grid_shape(d, n_bins)  # argument validation as in the reference's init_grid
     try:
         its, contribs, _final_b, _secs = _native.mcubes_run(
             f.device_spec(), plan, n_bins, iterations, seed, RNG_KINDS[rng], adapt, params.alpha, params.smoothing,

@@ -63,12 +63,19 @@ class GridRefineParams(_Frozen):
         self._put("smoothing", bool(smoothing))
 
 
-def init_grid(d: int, n_bins: int = DEFAULT_N_BINS) -> VegasGrid:
-    """Uniform grid k / n_bins (vegas_grid.py:77-84)."""
+def check_grid_shape(d: int, n_bins: int):
+    """The argument checks of init_grid (vegas_grid.py:77-84) without building the table: the device-resident run
+    starts from its own uniform grid and a (d, 501) host table plus its validation cost ~100 us per call."""
     d = check_dimension(d)
     n_bins = int(n_bins)
     if n_bins < 2:
         raise ValueError("n_bins must be >= 2")
+    return d, n_bins
+
+
+def init_grid(d: int, n_bins: int = DEFAULT_N_BINS) -> VegasGrid:
+    """Uniform grid k / n_bins (vegas_grid.py:77-84)."""
+    d, n_bins = check_grid_shape(d, n_bins)
     return VegasGrid(d, n_bins, np.tile(np.arange(n_bins + 1) / n_bins, (d, 1)))
 
 

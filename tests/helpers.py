@@ -59,6 +59,56 @@ class ThreadComm:
     def barrier(self):
         self._s.barrier.wait()
 
+    # ---- tensor-level collectives on CUDA tensors of ONE device (every rank a thread with its own library context and
+    #      stream): the in-process stand-in for sharded.Comm's NCCL methods
+    @staticmethod
+    def _sync():
+        import torch
+        torch.cuda.current_stream().synchronize()
+
+    def all_gather_into(self, out, inp):
+        self._sync()                                   # my row is complete
+        self._s.slots[self.rank] = inp
+        self._s.barrier.wait()
+        n = inp.numel()
+        parts = [t.clone() for t in self._s.slots]     # read everyone (mine may alias `out`)
+        self._sync()
+        self._s.barrier.wait()                         # everyone has read: buffers may change again
+        for r, t in enumerate(parts):
+            out[r * n:(r + 1) * n].copy_(t)
+
+    def _all_reduce(self, t, op):
+        self._sync()
+        self._s.slots[self.rank] = t
+        self._s.barrier.wait()
+        total = self._s.slots[0].clone()
+        for other in self._s.slots[1:]:                # rank order on every rank: identical bits everywhere
+            total = op(total, other)
+        self._sync()
+        self._s.barrier.wait()
+        t.copy_(total)
+
+    def all_reduce_sum_(self, t):
+        import torch
+        self._all_reduce(t, torch.add)
+
+    def all_reduce_max_(self, t):
+        import torch
+        self._all_reduce(t, torch.maximum)
+
+    def exchange_tensors(self, sends, recvs):
+        self._sync()
+        for r, t in sends.items():
+            self._s.mail[(self.rank, r)] = t
+        self._s.barrier.wait()
+        for r, buf in recvs.items():
+            buf.copy_(self._s.mail[(r, self.rank)])
+        self._sync()
+        self._s.barrier.wait()
+        for r in sends:
+            self._s.mail.pop((self.rank, r), None)
+        self._s.barrier.wait()
+
     def exchange_rows(self, sends, recvs, d):
         for r, (lefts, lengths) in sends.items():
             self._s.mail[(self.rank, r)] = (np.array(lefts), np.array(lengths))
