@@ -653,9 +653,16 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
 
   int done = 0, enqueued = 0;
   std::vector<double> ivals, ivars;
+  // Speculation is withheld when the run is about to stop: the cumulative error of the next iteration is
+  // extrapolated geometrically from the last two (it falls several-fold per iteration while the grid adapts and by
+  // ~sqrt(k/(k+1)) afterwards); if that meets the target, the pass behind it would only be three no-op launches
+  // inside the timed run.  A wrong guess costs one host round trip, never a result: the decision is the device's.
+  const bool tol_mode = rel_tol > 0.0 || abs_tol > 0.0;
+  bool near_target = false;
+  double prev_err = 0.0;
   pcb_status st = enqueue(enqueued++);
   for (int it = 0; st == PCB_OK && it < iterations; ++it) {
-    if (enqueued < iterations) {
+    if (enqueued < iterations && enqueued <= it + 1 && !near_target) {
       st = enqueue(enqueued++);
       if (st != PCB_OK) break;
     }
@@ -674,6 +681,18 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
     done = it + 1;
     ivals.push_back(o.integral);
     ivars.push_back(o.variance);
+    if (tol_mode && !rec.stop) {
+      double wsum = 0.0, dot = 0.0;
+      for (int i = 0; i < done; ++i) {
+        const double w = 1.0 / std::fmax(ivars[i], 1e-30);
+        wsum += w;
+        dot += w * ivals[i];
+      }
+      const double target = std::fmax(abs_tol > 0 ? abs_tol : 0.0, rel_tol * std::fabs(dot / wsum));
+      const double err = std::pow(wsum, -0.5);
+      near_target = done >= 2 && prev_err > 0.0 && err * std::fmin(1.0, err / prev_err) <= target;
+      prev_err = err;
+    }
     if (progress) {
       // combine_iterations (mcubes.py:311-329): inverse-variance weights, variances floored at 1e-30
       double wsum = 0.0, dot = 0.0;
@@ -702,6 +721,10 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
       progress(user, &rec_out);
     }
     if (rec.stop) break;
+    if (enqueued <= it + 1 && enqueued < iterations) {   // speculation was withheld and the run goes on
+      st = enqueue(enqueued++);
+      if (st != PCB_OK) break;
+    }
   }
   // drain the (at most one) speculative no-op pass before anything is read back or reused
   if (!iteration_events && st == PCB_OK) st = cudaEventRecord(ctx->mc_events[1], ctx->stream) == cudaSuccess ? PCB_OK : fail(ctx, PCB_CUDA, "mcubes_run: event record failed");

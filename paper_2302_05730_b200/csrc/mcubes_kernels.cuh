@@ -109,8 +109,14 @@ __device__ __forceinline__ void draw_axis(const SampleArgs& a, const double* s_b
   int b = __double2loint(zi);
   b = b < nb ? b : nb - 1;
   const double frac = z - (zi - 4503599627370496.0);
+#ifdef PCB_EXP_NOCONFLICT_B   // experiment (wrong results): what would conflict-free boundary gathers buy?
+  const int bb = (b & ~15) | (int)(threadIdx.x & 15);
+  const double lo = s_b[j * nb1 + (bb < nb ? bb : b)];
+  const double wd = s_b[j * nb1 + (bb < nb ? bb : b) + 1] - lo;
+#else
   const double lo = s_b[j * nb1 + b];
   const double wd = s_b[j * nb1 + b + 1] - lo;
+#endif
   xj = lo + frac * wd;
   const double jw = nbd * wd;
   jac = (j == 0) ? jw : jac * jw;
@@ -130,32 +136,52 @@ __host__ __device__ inline size_t vsample_smem_bytes(int d, int nb) {
 
 // Add two staged records per lane into the warp's private row (see the header comment).  Straight-line code: the
 // caller interleaves it with the arithmetic of the round being drawn, which hides the shared-memory round trips.
+// One arbitration round per call: same-bin lanes are arbitrated by a tag store (exactly one lane reads its own id
+// back per bin), the winner does a plain read-modify-write whose LOAD is issued together with the tag load (the
+// row entry is fetched speculatively: one shared-memory round trip less on the dependent chain), and a lane that
+// lost keeps its record in a one-deep pending slot (`pend_b` < 0: empty) that flush_pending() applies at the end
+// of the round.  (Until round 2 of this build every call ran a second, mostly idle arbitration round plus a vote:
+// 43 % of the pass's stall samples sat on those dependent round trips, profiles/r2_ncu_vsample_config4_before.txt.)
+// A second loss of the same lane before the flush -- about one call in a thousand -- goes through the CAS atomic.
 __device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
-                                         double w1, int b1) {
+                                         double w1, int b1, int& pend_b, double& pend_w) {
+#ifdef PCB_EXP_NOCONFLICT_H   // experiment (wrong results): conflict-free table and tag accesses
+  b0 = (b0 & ~31) | lane; b1 = ((b1 & ~31) | lane) ^ 32;
+  if (b0 >= 480) b0 = lane; if (b1 >= 480) b1 = lane + 32;
+#endif
   // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
   // two records of one lane in the same bin become one update
   const bool same = b0 == b1;
   const double add0 = same ? w0 + w1 : w0, add1 = w1;
-  unsigned want = (add0 != 0.0 ? 1u : 0u) | ((!same && add1 != 0.0) ? 2u : 0u);
-  // Only lanes that still have an update pending touch shared memory: the table is bound by shared-memory
-  // wavefronts, so the second round -- a handful of collision losers -- must not replay the whole warp's loads.
-  // 64 records in ~500 bins collide somewhere in 98 % of the calls: the second round is unconditional.
-#pragma unroll
-  for (int round = 0; round < 2; ++round) {
-    if (want & 1u) tags[b0] = (unsigned char)lane;
-    if (want & 2u) tags[b1] = (unsigned char)lane;
-    __syncwarp();
-    bool win0 = false, win1 = false;
-    if (want & 1u) win0 = tags[b0] == lane;
-    if (want & 2u) win1 = tags[b1] == lane;
-    if (win0) hist[b0] = hist[b0] + add0;
-    if (win1) hist[b1] = hist[b1] + add1;
-    want &= ~((win0 ? 1u : 0u) | (win1 ? 2u : 0u));
-    __syncwarp();
+  const bool want0 = add0 != 0.0, want1 = !same && add1 != 0.0;
+  if (want0) tags[b0] = (unsigned char)lane;
+  if (want1) tags[b1] = (unsigned char)lane;
+  __syncwarp();
+  const double h0 = hist[b0], h1 = hist[b1];           // speculative: only a winner uses its value
+  const bool win0 = want0 && tags[b0] == lane, win1 = want1 && tags[b1] == lane;
+  if (win0) hist[b0] = h0 + add0;
+  if (win1) hist[b1] = h1 + add1;
+  __syncwarp();
+  if (want0 && !win0) {
+    if (pend_b < 0) { pend_b = b0; pend_w = add0; }
+    else atomicAdd(hist + b0, add0);
   }
-  if (__any_sync(PCB_FULL_MASK, want)) {  // triple collisions: shared-memory CAS atomic
-    if (want & 1u) atomicAdd(hist + b0, add0);
-    if (want & 2u) atomicAdd(hist + b1, add1);
+  if (want1 && !win1) {
+    if (pend_b < 0) { pend_b = b1; pend_w = add1; }
+    else atomicAdd(hist + b1, add1);
+  }
+}
+
+// apply the pending records of the warp's lanes to its row: tag-arbitrated rounds until none is left (usually one)
+__device__ __forceinline__ void flush_pending(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, int& pend_b,
+                                              double& pend_w) {
+  while (__any_sync(PCB_FULL_MASK, pend_b >= 0)) {
+    if (pend_b >= 0) tags[pend_b] = (unsigned char)lane;
+    __syncwarp();
+    if (pend_b >= 0 && tags[pend_b] == lane) {
+      hist[pend_b] = hist[pend_b] + pend_w;
+      pend_b = -1;
+    }
     __syncwarp();
   }
 }
@@ -230,6 +256,11 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   unsigned char* cur = s_stage;
   unsigned char* prev = s_stage + kStageBytes;
   const int my = wib * 32 + lane;
+  constexpr int kRows = (D + kSampleWarps - 1) / kSampleWarps;   // rows of the table this warp serves
+  int pend_b[kRows];
+  double pend_w[kRows];
+#pragma unroll
+  for (int q = 0; q < kRows; ++q) { pend_b[q] = -1; pend_w[q] = 0.0; }
   auto stage = [&](int slot, double w, const int (&bin)[D]) {
     reinterpret_cast<double*>(cur)[slot * kSlot + my] = w;
     unsigned short* rb = reinterpret_cast<unsigned short*>(cur + 2 * kSlot * 8);
@@ -243,12 +274,15 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
 #endif
     const double* rw = reinterpret_cast<const double*>(prev);
     const unsigned short* rb = reinterpret_cast<const unsigned short*>(prev + 2 * kSlot * 8);
-    for (int j = wib; j < D; j += kSampleWarps) {
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+      const int j = wib + q * kSampleWarps;
+      if (j >= D) break;
       double* hist = s_hist + (size_t)j * nb;
       unsigned char* tags = s_tag + (size_t)j * tag_bytes;
       auto one = [&](int w) {
         bin_pair(hist, tags, lane, rw[w * 32 + lane], rb[(j * 2) * kSlot + w * 32 + lane], rw[kSlot + w * 32 + lane],
-                 rb[(j * 2 + 1) * kSlot + w * 32 + lane]);
+                 rb[(j * 2 + 1) * kSlot + w * 32 + lane], pend_b[q], pend_w[q]);
       };
       if constexpr (decltype(unrolled)::value) {
 #pragma unroll
@@ -264,7 +298,16 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   // everything at once, compact code (single-sample rounds: odd p and the generic generators; the last round)
   auto bin_all = [&]() { bin_rows(0, kSampleWarps, std::false_type{}); };
   // the round is staged: publish it, and take the other buffer (whose records every warp has consumed) for the next
+  auto flush_rows = [&]() {
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+      const int j = wib + q * kSampleWarps;
+      if (j >= D) break;
+      flush_pending(s_hist + (size_t)j * nb, s_tag + (size_t)j * tag_bytes, lane, pend_b[q], pend_w[q]);
+    }
+  };
   auto end_round = [&]() {
+    flush_rows();
     __syncthreads();
     unsigned char* t = cur; cur = prev; prev = t;
   };
@@ -406,6 +449,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   }
   ph_stamp(1);
   bin_all();   // the last round's records
+  flush_rows();
   if (clamp_count) atomicAdd(a.clamps, clamp_count);
   __syncthreads();
   ph_stamp(2);
