@@ -202,6 +202,13 @@ pcb_status pcb_profile_end(pcb_ctx* ctx, int32_t kind, double* kernel_ms, int64_
 pcb_status pcb_eval_points(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, const double* points /* (n,d) */,
                            double* values /* (n) */);
 
+/* ---- independent QMC oracle: replaces the sampling loop of integrands.oracle_integral (integrands.py:223-260) -------
+ * sums[s] = sum over the first 2^log2_points points of the unscrambled Sobol' sequence (Joe-Kuo direction numbers, 30
+ * bits, Gray-code order: the generator behind scipy.stats.qmc.Sobol) of f(frac(point + shifts[s])).  The caller draws
+ * the shifts and forms mean / 3 standard errors from the per-shift averages like the reference.                    */
+pcb_status pcb_qmc_shift_sums(pcb_ctx* ctx, const pcb_integrand* f, int32_t log2_points, int32_t n_shifts,
+                              const double* shifts /* (n_shifts, d) */, double* sums /* (n_shifts) */);
+
 /* ---- serial integrand invocation micro-benchmark: replaces cli.cmd_bench_invoke's loop (cli.py:134-142;
  * PAPER.md:451-455): blocks*threads device threads each evaluate all n points serially, keeping a running
  * sum; ms_out[repetitions] are CUDA-event times, *accumulator is thread 0's sum (the reference's `acc`). */

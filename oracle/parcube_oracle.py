@@ -492,3 +492,30 @@ def mcubes_run(family, n, d, iterations, seed=0, workers=1, n_bins=500, adapt=Tr
     est, err, chi2 = combine([r["integral"] for r in its], [r["variance"] for r in its])
     return dict(estimate=est, errorest=err, chi2_per_dof=chi2, iterations=its, plan=plan,
                 progress=progress, boundaries=grid)
+
+
+# =========================================================================== QMC oracle
+def oracle_integral(family, d, n_points, n_shifts=16, seed=20260810, bounds=None):
+    """integrands.oracle_integral (integrands.py:223-260): randomly shifted Sobol' average; returns
+    (value, bound, per-shift estimates).  Third-party generator: scipy.stats.qmc.Sobol (unscrambled)."""
+    from scipy.stats import qmc
+
+    if n_points < 2**16:
+        raise ValueError("oracle needs n_points >= 2**16")
+    if n_shifts < 2:
+        raise ValueError("need at least two shifts for an error bound")
+    m = max(16, int(math.ceil(math.log2(n_points))))
+    shifts = np.random.default_rng(seed).random((n_shifts, d))
+    acc = np.zeros(n_shifts)
+    engine = qmc.Sobol(d=d, scramble=False)
+    remaining = 2**m
+    while remaining:
+        take = min(2**18, remaining)
+        base = engine.random(take)
+        for s in range(n_shifts):
+            pts = base + shifts[s]
+            pts -= np.floor(pts)
+            acc[s] += float(np.sum(genz_eval(family, d, pts, bounds)))
+        remaining -= take
+    estimates = acc / 2**m
+    return float(np.mean(estimates)), 3.0 * float(np.std(estimates, ddof=1)) / math.sqrt(n_shifts), estimates

@@ -115,6 +115,7 @@ SIGNATURES = {
     "pcb_profile_begin": (C.c_int, [C.c_void_p]),
     "pcb_profile_end": (C.c_int, [C.c_void_p, C.c_int32, _DP, C.POINTER(C.c_int64), _DP]),
     "pcb_eval_points": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_void_p]),
+    "pcb_qmc_shift_sums": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "pcb_bench_invoke": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.c_int64, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                    C.c_void_p, _DP]),
     "pcb_pagani_evaluate": (C.c_int, [C.c_void_p, C.POINTER(IntegrandC), C.POINTER(RuleC), C.POINTER(PaganiConfigC),
@@ -374,6 +375,16 @@ def eval_points(spec: DeviceSpec, points: np.ndarray, device=None) -> np.ndarray
     fc = spec.to_c()
     with ctx.call_lock:
         ctx.check(ctx.lib.pcb_eval_points(ctx.handle, C.byref(fc), pts.shape[0], _ptr(pts), _ptr(out)))
+    return out
+
+
+def qmc_shift_sums(spec: DeviceSpec, log2_points: int, shifts: np.ndarray, device=None) -> np.ndarray:
+    ctx = context(device)
+    sh = _f64(shifts)
+    out = np.empty(sh.shape[0])
+    fc = spec.to_c()
+    with ctx.call_lock:
+        ctx.check(ctx.lib.pcb_qmc_shift_sums(ctx.handle, C.byref(fc), int(log2_points), sh.shape[0], _ptr(sh), _ptr(out)))
     return out
 
 

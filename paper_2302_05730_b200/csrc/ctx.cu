@@ -13,6 +13,7 @@ namespace pcb {
   const void* eval_wide_kernel_fam##F(int d); \
   const void* points_kernel_fam##F(int d); \
   const void* invoke_kernel_fam##F(int d); \
+  const void* qmc_kernel_fam##F(int d); \
   const void* lanes_kernel_fam##F(int d, size_t* smem, int* threads); \
   const void* vsample_kernel_fam##F(int d, int rng);
 PCB_DECL(0, ) PCB_DECL(1, ) PCB_DECL(2, ) PCB_DECL(3, ) PCB_DECL(4, ) PCB_DECL(5, ) PCB_DECL(6, ) PCB_DECL(7, )
@@ -30,6 +31,8 @@ static const sample_getter kSample[PCB_N_FAMILIES] = {vsample_kernel_fam0, vsamp
 
 static const kernel_getter kInvoke[PCB_N_FAMILIES] = {invoke_kernel_fam0, invoke_kernel_fam1, invoke_kernel_fam2, invoke_kernel_fam3,
                                                       invoke_kernel_fam4, invoke_kernel_fam5, invoke_kernel_fam6, invoke_kernel_fam7};
+static const kernel_getter kQmc[PCB_N_FAMILIES] = {qmc_kernel_fam0, qmc_kernel_fam1, qmc_kernel_fam2, qmc_kernel_fam3,
+                                                   qmc_kernel_fam4, qmc_kernel_fam5, qmc_kernel_fam6, qmc_kernel_fam7};
 typedef const void* (*lanes_getter)(int d, size_t* smem, int* threads);
 static const lanes_getter kLanes[PCB_N_FAMILIES] = {lanes_kernel_fam0, lanes_kernel_fam1, lanes_kernel_fam2, lanes_kernel_fam3,
                                                     lanes_kernel_fam4, lanes_kernel_fam5, lanes_kernel_fam6, lanes_kernel_fam7};
@@ -269,6 +272,68 @@ pcb_status pcb_bench_invoke(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, con
   cudaEventDestroy(e1);
   if (st != PCB_OK) return st;
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(accumulator, out, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+// Sobol' direction numbers of the first 12 dimensions (Joe & Kuo, new-joe-kuo-6.21201: degree s, coefficient word a,
+// initial m_i), 30 bits -- the table behind scipy.stats.qmc.Sobol, which the reference's oracle uses
+// (integrands.py:247); tests/test_gpu_qmc.py checks the generated points against scipy bit for bit.
+static void sobol_directions(int d, unsigned* v /* [d][30] */) {
+  static const int kS[12] = {0, 1, 2, 3, 3, 4, 4, 5, 5, 5, 5, 5};
+  static const int kA[12] = {0, 0, 1, 1, 2, 1, 4, 2, 4, 7, 11, 13};
+  static const int kM[12][5] = {{0}, {1}, {1, 3}, {1, 3, 1}, {1, 1, 1}, {1, 1, 3, 3}, {1, 3, 5, 13}, {1, 1, 5, 5, 17},
+                                {1, 1, 5, 5, 5}, {1, 1, 7, 11, 19}, {1, 1, 5, 1, 1}, {1, 1, 1, 3, 11}};
+  const int bits = 30;
+  for (int j = 0; j < d; ++j) {
+    unsigned long long m[30];
+    if (j == 0) {
+      for (int i = 0; i < bits; ++i) m[i] = 1;
+    } else {
+      const int s = kS[j], a = kA[j];
+      for (int i = 0; i < s; ++i) m[i] = (unsigned long long)kM[j][i];
+      for (int i = s; i < bits; ++i) {
+        unsigned long long val = m[i - s] ^ (m[i - s] << s);
+        for (int k = 1; k < s; ++k) val ^= (unsigned long long)((a >> (s - 1 - k)) & 1) * (m[i - k] << k);
+        m[i] = val;
+      }
+    }
+    for (int i = 0; i < bits; ++i) v[j * bits + i] = (unsigned)(m[i] << (bits - 1 - i));
+  }
+}
+
+pcb_status pcb_qmc_shift_sums(pcb_ctx* ctx, const pcb_integrand* f, int32_t log2_points, int32_t n_shifts, const double* shifts,
+                              double* sums) {
+  if (!ctx) return PCB_INVALID;
+  PCB_TRY(validate_integrand(ctx, f));
+  if (log2_points < 10 || log2_points > 30 || n_shifts < 1 || n_shifts > 4096 || !shifts || !sums)
+    return fail(ctx, PCB_INVALID, "qmc_shift_sums: 2^10 <= points <= 2^30, 1 <= shifts <= 4096");
+  PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int d = f->d;
+  // 2^17 threads at most (512 CTAs of 256), at least 8 points per thread
+  int log2_threads = log2_points - 3;
+  if (log2_threads > 17) log2_threads = 17;
+  const unsigned blocks = 1u << (log2_threads - 8);
+  unsigned dirs[12 * 30];
+  sobol_directions(d, dirs);
+  const size_t dir_bytes = (size_t)d * 30 * sizeof(unsigned), shift_bytes = (size_t)n_shifts * d * sizeof(double);
+  PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure(dir_bytes + 64 + shift_bytes + ((size_t)n_shifts * blocks + n_shifts) * sizeof(double)));
+  unsigned* dirs_dev = ctx->mc_tmp.as<unsigned>();
+  double* shifts_dev = reinterpret_cast<double*>(ctx->mc_tmp.as<char>() + ((dir_bytes + 63) & ~(size_t)63));
+  double* partial = shifts_dev + (size_t)n_shifts * d;
+  double* sums_dev = partial + (size_t)n_shifts * blocks;
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(dirs_dev, dirs, dir_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(shifts_dev, shifts, shift_bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));   // `dirs` is a stack buffer
+  pcb_integrand fv = *f;
+  int lg = log2_points;
+  const unsigned* dirs_c = dirs_dev;
+  const double* shifts_c = shifts_dev;
+  void* args[] = {&fv, &lg, &dirs_c, &shifts_c, &partial};
+  PCB_CUDA_TRY(ctx, cudaLaunchKernel(kQmc[f->family](d), dim3(blocks, (unsigned)n_shifts), dim3(256), args, 0, ctx->stream));
+  ctx->launches++;
+  for (int s = 0; s < n_shifts; ++s) PCB_TRY(tree_sum_dev(ctx, partial + (size_t)s * blocks, blocks, sums_dev + s));
+  PCB_CUDA_TRY(ctx, cudaMemcpyAsync(sums, sums_dev, (size_t)n_shifts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return PCB_OK;
 }

@@ -437,4 +437,53 @@ __global__ void invoke_kernel(const __grid_constant__ pcb_integrand f, long long
   acc_out[blockIdx.x * (long long)blockDim.x + threadIdx.x] = acc;
 }
 
+// Randomly shifted Sobol' average (reference: integrands.py:223-260, the independent QMC oracle): shift s of the
+// launch's blockIdx.y, points [0, 2^log2n) in the Gray-code order of the generator (x_{i+1} = x_i ^ V[ctz(i+1)]);
+// a thread walks a contiguous run of points, point = frac(sobol + shift) as base + shift - floor(.), and the block's
+// sum goes to partial[shift][block] (the host-side driver finishes the per-shift sums with the pair tree).
+constexpr int kSobolBits = 30;   // scipy.stats.qmc.Sobol default: coordinates are multiples of 2^-30
+template <int FAM, int D>
+__global__ void __launch_bounds__(256) qmc_shift_kernel(const __grid_constant__ pcb_integrand f, int log2n,
+                                                        const unsigned* __restrict__ dirs /* [D][30] */,
+                                                        const double* __restrict__ shifts /* [n_shifts][D] */,
+                                                        double* __restrict__ partial /* [n_shifts][gridDim.x] */) {
+  using F = Family<FAM>;
+  __shared__ double s_warp[8];
+  const unsigned long long n = 1ULL << log2n, threads = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long per = n / threads, i0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * per;
+  unsigned x[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) x[j] = 0u;
+  for (unsigned long long gray = i0 ^ (i0 >> 1), b = 0; gray; gray >>= 1, ++b)
+    if (gray & 1ULL) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] ^= dirs[j * kSobolBits + b];
+    }
+  double sh[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) sh[j] = shifts[blockIdx.y * D + j];
+  double acc = 0.0;
+  for (unsigned long long i = i0; i < i0 + per; ++i) {
+    double pt[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double v = (double)x[j] * 9.313225746154785e-10 + sh[j];   // base * 2^-30 (exact) + shift
+      pt[j] = v - floor(v);
+    }
+    acc = acc + eval_at<F, D>(pt, f);
+    const int c = __ffsll((long long)~i) - 1;     // index of the lowest zero bit of i
+    if (c < kSobolBits) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) x[j] ^= dirs[j * kSobolBits + c];
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) acc = acc + __shfl_xor_sync(PCB_FULL_MASK, acc, m);
+  if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    partial[(size_t)blockIdx.y * gridDim.x + blockIdx.x] =
+        ((s_warp[0] + s_warp[1]) + (s_warp[2] + s_warp[3])) + ((s_warp[4] + s_warp[5]) + (s_warp[6] + s_warp[7]));
+}
+
 }  // namespace pcb

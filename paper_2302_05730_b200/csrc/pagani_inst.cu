@@ -78,6 +78,15 @@ const void* PCB_CAT(points_kernel_fam, PCB_FAM)(int d) {
   return nullptr;
 }
 
+const void* PCB_CAT(qmc_kernel_fam, PCB_FAM)(int d) {
+  switch (d) {
+#define X(D) case D: return (const void*)&qmc_shift_kernel<PCB_FAM, D>;
+    PCB_DIMS(X)
+#undef X
+  }
+  return nullptr;
+}
+
 const void* PCB_CAT(invoke_kernel_fam, PCB_FAM)(int d) {
   switch (d) {
 #define X(D) case D: return (const void*)&invoke_kernel<PCB_FAM, D>;
