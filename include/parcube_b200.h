@@ -26,7 +26,8 @@ typedef enum {
   PCB_NONFINITE = 1, /* integrand returned NaN/inf: see pcb_nonfinite (core.py:26-37)   */
   PCB_BUDGET = 2,    /* workload exceeds a cap (core.py:22-23, 262-263)                 */
   PCB_INVALID = 3,   /* bad argument (the reference's ValueError paths)                 */
-  PCB_CUDA = 4       /* CUDA runtime failure                                            */
+  PCB_CUDA = 4,      /* CUDA runtime failure                                            */
+  PCB_ABORTED = 5    /* pcb_ctx_abort() was called from a progress callback             */
 } pcb_status;
 
 /* Integrand families = the reference registry BENCHMARKS (integrands.py:131-139). */
@@ -178,6 +179,10 @@ typedef struct pcb_ctx pcb_ctx;
 pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out);
 void pcb_ctx_destroy(pcb_ctx* ctx);
 const char* pcb_last_error(const pcb_ctx* ctx);
+/* Ask the running refine / mcubes_run of this context to stop: callable from inside a progress callback (the
+ * reference's drivers propagate an exception raised by `progress` at once, pagani.py:341-349).  The driver returns
+ * PCB_ABORTED after the current iteration's record; nothing else of the context is affected.                       */
+void pcb_ctx_abort(pcb_ctx* ctx);
 /* Scratch memory of a context (region lists, estimates, contribution tables) lives in the device's stream-ordered
  * memory pool and is never handed back to the driver while the process lives; it grows on demand.  reserve() grows
  * the pool to at least `bytes` up front, so that the first large call pays no driver allocation in its loop
@@ -345,6 +350,8 @@ pcb_status pcb_grid_transform(pcb_ctx* ctx, int32_t d, int32_t n_bins, const dou
  * the first iteration with errorest <= max(abs_tol, rel_tol*|estimate|).  rel_tol > 0 adds the
  * time-to-epsrel stop of BASELINE.md section 3.  iterations_out: capacity `iterations`.
  * final_boundaries (optional): (d, n_bins+1).                                                 */
+/* Limits: the run's group-order tree covers at most 1024 work-groups (the reference's default plans have <= 256,
+ * mcubes.py:110-129: target_groups = 256); pcb_mcubes_sample has no such limit.                                     */
 pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes_plan* plan,
                           int32_t iterations, uint64_t seed, int32_t rng_kind, int32_t adapt, double alpha,
                           int32_t smoothing, double rel_tol, double abs_tol,

@@ -16,7 +16,7 @@ MAX_DIM = 12
 LIB_NAME = os.environ.get("PCB_LIB_NAME", "libparcube_b200.so")   # PCB_LIB_NAME: A/B builds in experiments
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
-PCB_OK, PCB_NONFINITE, PCB_BUDGET, PCB_INVALID, PCB_CUDA = range(5)
+PCB_OK, PCB_NONFINITE, PCB_BUDGET, PCB_INVALID, PCB_CUDA, PCB_ABORTED = range(6)
 RNG_REFERENCE_HASH, RNG_PHILOX, RNG_INJECTED = range(3)
 ERR_MODES = {"two-level": 0, "max-null": 1, "max-pairwise": 2}
 STOP_REASONS = ("tolerance met", "max iterations reached", "no active regions left", "region cap reached")
@@ -108,6 +108,7 @@ SIGNATURES = {
     "pcb_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "pcb_ctx_destroy": (None, [C.c_void_p]),
     "pcb_last_error": (C.c_char_p, [C.c_void_p]),
+    "pcb_ctx_abort": (None, [C.c_void_p]),
     "pcb_ctx_reserve": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
     "pcb_device_info": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "pcb_launch_count": (C.c_int64, [C.c_void_p]),
@@ -425,8 +426,9 @@ def pagani_refine(spec: DeviceSpec, orbit, cfg, progress=None, device=None):
             r = rec.contents
             progress({"iteration": r.iteration, "n_regions": int(r.n_regions), "active": int(r.active),
                       "estimate": r.estimate, "errorest": r.errorest})
-        except BaseException as exc:  # noqa: BLE001 - re-raised after the native call returns
+        except BaseException as exc:  # noqa: BLE001 - the driver stops at once; re-raised when the native call returns
             failure.append(exc)
+            ctx.lib.pcb_ctx_abort(ctx.handle)
 
     cb = PAGANI_PROGRESS_FN(_cb) if progress is not None else C.cast(None, PAGANI_PROGRESS_FN)
     with ctx.call_lock:
@@ -520,8 +522,9 @@ def mcubes_run(spec: DeviceSpec, plan, n_bins: int, iterations: int, seed: int, 
             progress({"iteration": r.iteration, "estimate": r.estimate, "errorest": r.errorest,
                       "chi2_per_dof": r.chi2_per_dof, "iter_integral": r.iter_integral,
                       "iter_sd": float(np.sqrt(r.iter_variance))})
-        except BaseException as exc:  # noqa: BLE001
+        except BaseException as exc:  # noqa: BLE001 - as in pagani_refine: stop the run, re-raise afterwards
             failure.append(exc)
+            ctx.lib.pcb_ctx_abort(ctx.handle)
 
     # no Python trampoline per iteration unless somebody listens (each call back into Python costs ~10 us)
     cb = MCUBES_PROGRESS_FN(_cb) if progress is not None else C.cast(None, MCUBES_PROGRESS_FN)

@@ -148,6 +148,10 @@ pcb_status pcb_ctx_reserve(pcb_ctx* ctx, uint64_t bytes, uint64_t* reserved_out)
   return PCB_OK;
 }
 
+void pcb_ctx_abort(pcb_ctx* ctx) {
+  if (ctx) ctx->abort_requested = 1;
+}
+
 const char* pcb_last_error(const pcb_ctx* ctx) { return ctx ? ctx->err.c_str() : "context is NULL"; }
 
 pcb_status pcb_device_info(pcb_ctx* ctx, char* name, int name_len, int32_t* sm_count, int32_t* clock_khz) {

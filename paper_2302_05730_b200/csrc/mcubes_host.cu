@@ -718,7 +718,15 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
       rec_out.chi2_per_dof = chi2;
       rec_out.iter_integral = o.integral;
       rec_out.iter_variance = o.variance;
+      ctx->abort_requested = 0;
       progress(user, &rec_out);
+      if (ctx->abort_requested) {   // the callback asked to stop: make the device stop too, drain, report
+        ctx->abort_requested = 0;
+        const int now = it;
+        cudaMemcpyAsync(stop_dev, &now, sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        return fail(ctx, PCB_ABORTED, "mcubes_run stopped by its progress callback at iteration %d", it);
+      }
     }
     if (rec.stop) break;
     if (enqueued <= it + 1 && enqueued < iterations) {   // speculation was withheld and the run goes on

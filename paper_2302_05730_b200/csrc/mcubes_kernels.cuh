@@ -139,18 +139,55 @@ __host__ __device__ inline size_t vsample_smem_bytes(int d, int nb) {
 // One arbitration round per call: same-bin lanes are arbitrated by a tag store (exactly one lane reads its own id
 // back per bin), the winner does a plain read-modify-write whose LOAD is issued together with the tag load (the
 // row entry is fetched speculatively: one shared-memory round trip less on the dependent chain), and a lane that
-// lost keeps its record in a one-deep pending slot (`pend_b` < 0: empty) that flush_pending() applies at the end
-// of the round.  (Until round 2 of this build every call ran a second, mostly idle arbitration round plus a vote:
-// 43 % of the pass's stall samples sat on those dependent round trips, profiles/r2_ncu_vsample_config4_before.txt.)
-// A second loss of the same lane before the flush -- about one call in a thousand -- goes through the CAS atomic.
-__device__ __forceinline__ void bin_pair(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
+// lost keeps its record in a one-deep pending slot (`pend_b` < 0: empty), which simply takes part in the lane's
+// next call as a third candidate -- no second arbitration round, no vote, no loop.  (Until round 2 of this build
+// every call ran a second, mostly idle arbitration round plus a vote: 43 % of the pass's stall samples sat on those
+// dependent round trips, profiles/r2_ncu_vsample_config4_before.txt.)  A lane that loses while its slot is still
+// occupied -- a few calls in a hundred warp-wide -- falls back to the CAS atomic.
+__device__ __forceinline__ void bin_pair_carry(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
                                          double w1, int b1, int& pend_b, double& pend_w) {
 #ifdef PCB_EXP_NOCONFLICT_H   // experiment (wrong results): conflict-free table and tag accesses
   b0 = (b0 & ~31) | lane; b1 = ((b1 & ~31) | lane) ^ 32;
   if (b0 >= 480) b0 = lane; if (b1 >= 480) b1 = lane + 32;
 #endif
   // a zero contribution leaves the table unchanged: skip it (empty records, f = 0 samples);
-  // two records of one lane in the same bin become one update
+  // records of one lane in the same bin become one update
+  const bool same = b0 == b1;
+  double add0 = same ? w0 + w1 : w0;
+  double add1 = w1;
+  const bool hit0 = pend_b == b0, hit1 = !same && pend_b == b1;   // the pending record meets a new one of its own lane
+  add0 = hit0 ? add0 + pend_w : add0;
+  add1 = hit1 ? add1 + pend_w : add1;
+  const bool wantp = pend_b >= 0 && !hit0 && !hit1;
+  const bool want0 = add0 != 0.0, want1 = !same && add1 != 0.0;
+  const int bp = wantp ? pend_b : b0;                  // always a valid bin: the loads below are unconditional
+  if (wantp) tags[bp] = (unsigned char)lane;
+  if (want0) tags[b0] = (unsigned char)lane;
+  if (want1) tags[b1] = (unsigned char)lane;
+  __syncwarp();
+  const double hp = hist[bp], h0 = hist[b0], h1 = hist[b1];   // speculative: only a winner uses its value
+  const unsigned char tp = tags[bp], t0 = tags[b0], t1 = tags[b1];
+  const bool winp = wantp && tp == lane, win0 = want0 && t0 == lane, win1 = want1 && t1 == lane;
+  if (winp) hist[bp] = hp + pend_w;
+  if (win0) hist[b0] = h0 + add0;
+  if (win1) hist[b1] = h1 + add1;
+  __syncwarp();
+  const bool lostp = wantp && !winp, lost0 = want0 && !win0, lost1 = want1 && !win1;
+  const bool ovf0 = lostp && lost0, ovf1 = lost1 && (lostp || lost0);
+  pend_w = lostp ? pend_w : (lost0 ? add0 : add1);
+  pend_b = lostp ? pend_b : (lost0 ? b0 : (lost1 ? b1 : -1));
+  if (ovf0 || ovf1) {
+    if (ovf0) atomicAdd(hist + b0, add0);
+    if (ovf1) atomicAdd(hist + b1, add1);
+  }
+}
+
+// The same with the pending slot emptied at the end of every round (flush_pending) instead of taking part in the next
+// call: two candidates per call, fewer live registers -- the form the 80-register kernels (D <= 6, three CTAs per
+// SM) take, where the third candidate spills (d = 6, 9.6e8 samples: 31.4 ms against 34.2 ms; d >= 7 at 128
+// registers prefers the carried form: d = 8 33.9 against 34.9 ms, d = 10 62.7 against 65.6 ms).
+__device__ __forceinline__ void bin_pair_flush(double* __restrict__ hist, unsigned char* __restrict__ tags, int lane, double w0, int b0,
+                                               double w1, int b1, int& pend_b, double& pend_w) {
   const bool same = b0 == b1;
   const double add0 = same ? w0 + w1 : w0, add1 = w1;
   const bool want0 = add0 != 0.0, want1 = !same && add1 != 0.0;
@@ -257,6 +294,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   unsigned char* prev = s_stage + kStageBytes;
   const int my = wib * 32 + lane;
   constexpr int kRows = (D + kSampleWarps - 1) / kSampleWarps;   // rows of the table this warp serves
+  constexpr bool kCarry = D >= 7;   // pending records take part in the next call (bin_pair_carry) or are flushed per round
   int pend_b[kRows];
   double pend_w[kRows];
 #pragma unroll
@@ -281,8 +319,12 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
       double* hist = s_hist + (size_t)j * nb;
       unsigned char* tags = s_tag + (size_t)j * tag_bytes;
       auto one = [&](int w) {
-        bin_pair(hist, tags, lane, rw[w * 32 + lane], rb[(j * 2) * kSlot + w * 32 + lane], rw[kSlot + w * 32 + lane],
-                 rb[(j * 2 + 1) * kSlot + w * 32 + lane], pend_b[q], pend_w[q]);
+        if constexpr (kCarry)
+          bin_pair_carry(hist, tags, lane, rw[w * 32 + lane], rb[(j * 2) * kSlot + w * 32 + lane], rw[kSlot + w * 32 + lane],
+                         rb[(j * 2 + 1) * kSlot + w * 32 + lane], pend_b[q], pend_w[q]);
+        else
+          bin_pair_flush(hist, tags, lane, rw[w * 32 + lane], rb[(j * 2) * kSlot + w * 32 + lane], rw[kSlot + w * 32 + lane],
+                         rb[(j * 2 + 1) * kSlot + w * 32 + lane], pend_b[q], pend_w[q]);
       };
       if constexpr (decltype(unrolled)::value) {
 #pragma unroll
@@ -306,8 +348,8 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
       flush_pending(s_hist + (size_t)j * nb, s_tag + (size_t)j * tag_bytes, lane, pend_b[q], pend_w[q]);
     }
   };
-  auto end_round = [&]() {
-    flush_rows();
+  auto end_round = [&]() {   // carried pending records stay in their lanes' slots across rounds (flushed once, at the end)
+    if constexpr (!kCarry) flush_rows();
     __syncthreads();
     unsigned char* t = cur; cur = prev; prev = t;
   };
@@ -390,7 +432,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
                          (inj_cube + k + 1) * D, active, x[1][j], jac[1], bin[1][j]);
           bin_from(j * kSampleWarps / D, (j + 1) * kSampleWarps / D);
         }
-        const double fx[2] = {eval_at<F, D>(x[0], a.f), eval_at<F, D>(x[1], a.f)};
+        const double fx[2] = {eval_at_sampler<F, D>(x[0], a.f), eval_at_sampler<F, D>(x[1], a.f)};
         const double v[2] = {fx[0] * jac[0], fx[1] * jac[1]};
         kc += 2ULL * D * kGolden;
         ctr += 2 * D;
@@ -413,7 +455,7 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
 #pragma unroll
         for (int j = 0; j < D; ++j)
           draw_axis<RNG>(a, s_b, j, coord[j], kc, (unsigned long long)T, ctr, (inj_cube + k) * D, active, x[j], jac, bin[j]);
-        const double fx = eval_at<F, D>(x, a.f);
+        const double fx = eval_at_sampler<F, D>(x, a.f);
         const double v = fx * jac;
         kc += (unsigned long long)D * kGolden;
         ctr += D;

@@ -379,7 +379,15 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       rec.errorest = errorest;
       if (records) records[n_rec] = rec;
       ++n_rec;
-      if (progress) progress(user, &rec);
+      if (progress) {
+        ctx->abort_requested = 0;
+        progress(user, &rec);
+        if (ctx->abort_requested) {
+          ctx->abort_requested = 0;
+          cudaStreamSynchronize(ctx->stream);
+          return fail(ctx, PCB_ABORTED, "refine stopped by its progress callback at iteration %d", it);
+        }
+      }
       if (srec->action == 1) { converged = true; reason = PCB_STOP_TOLERANCE; break; }
       if (srec->action == 2) { reason = PCB_STOP_MAX_ITER; break; }
       if (srec->action == 3) { reason = PCB_STOP_REGION_CAP; break; }
@@ -415,7 +423,15 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     rec.errorest = errorest;
     if (records) records[n_rec] = rec;
     ++n_rec;
-    if (progress) progress(user, &rec);
+    if (progress) {
+        ctx->abort_requested = 0;
+        progress(user, &rec);
+        if (ctx->abort_requested) {
+          ctx->abort_requested = 0;
+          cudaStreamSynchronize(ctx->stream);
+          return fail(ctx, PCB_ABORTED, "refine stopped by its progress callback at iteration %d", it);
+        }
+      }
     if (errorest <= tolerance_target(cfg->rel_tol, cfg->abs_tol, estimate)) {
       converged = true;
       reason = PCB_STOP_TOLERANCE;

@@ -67,6 +67,7 @@ struct pcb_ctx {
   std::map<const void*, size_t> smem_attr;  // dynamic shared memory already granted per kernel
   cudaStream_t stream = nullptr;
   std::string err;
+  volatile int abort_requested = 0;   // pcb_ctx_abort(), polled by the drivers after every progress callback
   long long launches = 0;
   char name[256] = {0};
   void* pinned = nullptr;  // 64 KiB staging for small device->host reads

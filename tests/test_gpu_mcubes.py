@@ -502,3 +502,21 @@ def test_segmented_thread_shards_reassemble_bit_for_bit():
         _it, _c, gp = _native.mcubes_sample(spec, plan, grid.boundaries, 11, thread_range=(t0, t1), want_group_partials=True)
         parts.append(gp)
     assert np.array_equal(np.concatenate(parts), gp_whole)
+
+
+def test_progress_exception_stops_the_run_at_once():
+    """mcubes.run calls `progress` inline (mcubes.py:364-366): an exception ends the run there; the device-resident loop
+    is told to stop and drained, and the next run on the context is unaffected."""
+    seen = []
+
+    def cb(rec):
+        seen.append(rec["iteration"])
+        if rec["iteration"] == 1:
+            raise KeyError("stop")
+
+    f = pb.get_integrand("f2", 6)
+    with pytest.raises(KeyError):
+        pb.mcubes_run(f, 10**6, 6, 15, seed=0, progress=cb)
+    assert seen == [0, 1]
+    again = pb.mcubes_run(f, 10**6, 6, 15, seed=0, rel_tol=1e-3)
+    assert len(again.iterations) == 4

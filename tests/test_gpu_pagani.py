@@ -435,3 +435,27 @@ def test_abs_tol_extension_matches_oracle(fam, d, rel, absv):
         assert abs(res.estimate - want["estimate"]) <= REL_EST * abs(want["estimate"])
     if res.converged:
         assert res.errorest <= max(absv, rel * abs(res.estimate))
+
+
+def test_progress_exception_stops_the_run_at_once():
+    """An exception raised by `progress` ends the refinement at that iteration and propagates (the reference calls
+    `progress` inline, pagani.py:341-349); the context stays usable."""
+    seen = []
+
+    class Stop(Exception):
+        pass
+
+    def cb(rec):
+        seen.append(rec["iteration"])
+        if rec["iteration"] == 2:
+            raise Stop("enough")
+
+    with pytest.raises(Stop):
+        pb.refine(pb.get_integrand("f1", 8), pb.PaganiConfig(rel_tol=1e-6, region_cap=1 << 22), progress=cb)
+    assert seen == [0, 1, 2]
+    seen.clear()
+    with pytest.raises(Stop):   # short-list path (<= 1024 regions per iteration)
+        pb.refine(pb.get_integrand("f4", 5), pb.PaganiConfig(rel_tol=1e-3), progress=cb)
+    assert seen == [0, 1, 2]
+    res = pb.refine(pb.get_integrand("f4", 5), pb.PaganiConfig(rel_tol=1e-3))
+    assert (res.iterations, res.regions_processed) == (10, 3328)
