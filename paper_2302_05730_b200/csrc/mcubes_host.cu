@@ -734,8 +734,19 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
       if (st != PCB_OK) break;
     }
   }
-  // drain the (at most one) speculative no-op pass before anything is read back or reused
+  // End of the run: the closing event and the two result copies (final boundaries, the tables of the iterations that
+  // ran) are enqueued behind the last kernel in one go and awaited once -- this also drains the at most one
+  // speculative no-op pass before anything is reused.
   if (!iteration_events && st == PCB_OK) st = cudaEventRecord(ctx->mc_events[1], ctx->stream) == cudaSuccess ? PCB_OK : fail(ctx, PCB_CUDA, "mcubes_run: event record failed");
+  if (st == PCB_OK && final_boundaries) {
+    const int cur = adapt ? (done & 1) : 0;
+    if (cudaMemcpyAsync(out_bounds_host, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+      st = fail(ctx, PCB_CUDA, "mcubes_run: copy of the final boundaries failed");
+  }
+  if (st == PCB_OK && contributions_out && done > 0) {
+    if (cudaMemcpyAsync(out_tables_host, ctx->mc_tables.p, (size_t)done * tbytes, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess)
+      st = fail(ctx, PCB_CUDA, "mcubes_run: copy of the contribution tables failed");
+  }
   cudaError_t drain = cudaStreamSynchronize(ctx->stream);
   if (st != PCB_OK) return st;
   PCB_CUDA_TRY(ctx, drain);
@@ -776,13 +787,6 @@ pcb_status pcb_mcubes_run(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcubes
   PCB_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->mc_events[0], ctx->mc_events[iteration_events ? done : 1]));
   if (seconds_device) *seconds_device = ms * 1e-3;
   *n_done = done;
-  if (final_boundaries) {
-    const int cur = adapt ? (done & 1) : 0;
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_bounds_host, ctx->mc_bounds[cur].p, bbytes, cudaMemcpyDeviceToHost, ctx->stream));
-  }
-  if (contributions_out)
-    PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out_tables_host, ctx->mc_tables.p, (size_t)done * tbytes, cudaMemcpyDeviceToHost, ctx->stream));
-  if (final_boundaries || contributions_out) PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   if (final_boundaries) std::memcpy(final_boundaries, out_bounds_host, bbytes);
   if (contributions_out) std::memcpy(contributions_out, out_tables_host, (size_t)done * tbytes);
   return PCB_OK;

@@ -294,7 +294,10 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
   unsigned char* prev = s_stage + kStageBytes;
   const int my = wib * 32 + lane;
   constexpr int kRows = (D + kSampleWarps - 1) / kSampleWarps;   // rows of the table this warp serves
-  constexpr bool kCarry = D >= 7;   // pending records take part in the next call (bin_pair_carry) or are flushed per round
+#ifndef PCB_VS_CARRY_MIN_D
+#define PCB_VS_CARRY_MIN_D 7
+#endif
+  constexpr bool kCarry = D >= PCB_VS_CARRY_MIN_D;   // pending records take part in the next call (bin_pair_carry) or are flushed per round
   int pend_b[kRows];
   double pend_w[kRows];
 #pragma unroll

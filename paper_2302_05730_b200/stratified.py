@@ -86,7 +86,20 @@ class McubesPlan(_Frozen):
 
 def make_plan(n, d: int, group_size: int = 128, target_groups: int = 256) -> McubesPlan:
     """g = largest integer with g^d <= n//2; p = max(2, round(n/g^d)); s batches the sub-cubes
-    into ~target_groups work-groups (mcubes.py:110-129)."""
+    into ~target_groups work-groups (mcubes.py:110-129).  Plans are immutable: one instance per argument set."""
+    key = (int(n), int(d), int(group_size), int(target_groups))
+    hit = _PLAN_CACHE.get(key)
+    if hit is None:
+        if len(_PLAN_CACHE) > 256:
+            _PLAN_CACHE.clear()
+        hit = _PLAN_CACHE[key] = _make_plan(*key)
+    return hit
+
+
+_PLAN_CACHE: dict = {}
+
+
+def _make_plan(n: int, d: int, group_size: int, target_groups: int) -> McubesPlan:
     d = check_dimension(d)
     n = int(n)
     if n < 2 ** (d + 1):
@@ -179,8 +192,14 @@ def _raise_nonfinite(exc: _native.NonFiniteStatus, plan: McubesPlan):
 
 
 def _table(d, n_bins, c) -> BinContributions:
-    out = BinContributions(d, n_bins)
-    out.c[:] = c
+    """A BinContributions over `c` itself when it is a float64 (d, n_bins) array the caller hands over (the per-iteration
+    slices of a run's table block), else over a copy."""
+    out = BinContributions.__new__(BinContributions)
+    out.d, out.n_bins = int(d), int(n_bins)
+    if isinstance(c, np.ndarray) and c.dtype == np.float64 and c.shape == (d, n_bins) and c.flags.writeable:
+        out.c = c
+    else:
+        out.c = np.array(c, dtype=np.float64).reshape(d, n_bins)
     return out
 
 
