@@ -183,10 +183,12 @@ const char* pcb_last_error(const pcb_ctx* ctx);
  * reference's drivers propagate an exception raised by `progress` at once, pagani.py:341-349).  The driver returns
  * PCB_ABORTED after the current iteration's record; nothing else of the context is affected.                       */
 void pcb_ctx_abort(pcb_ctx* ctx);
-/* Scratch memory of a context (region lists, estimates, contribution tables) lives in the device's stream-ordered
- * memory pool and is never handed back to the driver while the process lives; it grows on demand.  reserve() grows
- * the pool to at least `bytes` up front, so that the first large call pays no driver allocation in its loop
- * (a refine() to the default region cap 2^26 at d = 8 peaks at ~11 GB).  *reserved_out = pool size afterwards.   */
+/* Scratch memory of a context (region lists, estimates, contribution tables): every buffer is a reserved virtual
+ * address range backed by physical chunks on demand (CUDA virtual memory management); growing maps more chunks, the
+ * base never moves, nothing is freed or copied, and the context keeps what it has until it is destroyed.  reserve()
+ * creates `bytes` of physical chunks up front, so that the first large call maps them instead of asking the driver for
+ * memory inside its loop (a refine() to the default region cap 2^26 at d = 8 peaks at ~11 GB).
+ * *reserved_out = bytes held in reserve afterwards.                                                                */
 pcb_status pcb_ctx_reserve(pcb_ctx* ctx, uint64_t bytes, uint64_t* reserved_out);
 /* name and SM count of the context's device, multiprocessor clock in kHz */
 pcb_status pcb_device_info(pcb_ctx* ctx, char* name, int name_len, int32_t* sm_count, int32_t* clock_khz);

@@ -94,12 +94,7 @@ pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out) {
   ctx->clock_khz = khz;
   std::strncpy(ctx->name, prop.name, sizeof(ctx->name) - 1);
   PCB_CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-  {  // scratch memory: the device's stream-ordered pool, never trimmed (DevBuf in pcb_host.h)
-    cudaMemPool_t pool;
-    PCB_CUDA_TRY(ctx, cudaDeviceGetDefaultMemPool(&pool, device_ordinal));
-    unsigned long long keep = ~0ULL;
-    PCB_CUDA_TRY(ctx, cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  }
+  if (!Vmm::get().ok) return fail(ctx, PCB_CUDA, "the driver does not offer the virtual memory management API the scratch buffers are built on");
   PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pinned, 1 << 16));
   PCB_CUDA_TRY(ctx, ctx->scalars.ensure(64 * sizeof(double)));
   return PCB_OK;
@@ -109,11 +104,13 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) {
-    ctx->release_buffers();          // stream-ordered frees need the stream
     cudaStreamSynchronize(ctx->stream);
+    ctx->release_buffers();
     cudaStreamDestroy(ctx->stream);
     ctx->stream = nullptr;
   }
+  for (auto h : ctx->chunk_cache.free_chunks) Vmm::get().release(h);
+  ctx->chunk_cache.free_chunks.clear();
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   if (ctx->mc_records) cudaFreeHost(ctx->mc_records);
   if (ctx->pg_record) cudaFreeHost(ctx->pg_record);
@@ -131,20 +128,20 @@ void pcb_ctx_destroy(pcb_ctx* ctx) {
 pcb_status pcb_ctx_reserve(pcb_ctx* ctx, uint64_t bytes, uint64_t* reserved_out) {
   if (!ctx) return PCB_INVALID;
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  cudaMemPool_t pool;
-  PCB_CUDA_TRY(ctx, cudaDeviceGetDefaultMemPool(&pool, ctx->device));
-  unsigned long long have = 0;
-  PCB_CUDA_TRY(ctx, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
-  if (bytes > have) {
-    // one block of the missing size, released at once: the pool keeps the backing (release threshold = never) and
-    // serves the context's later requests from it without going to the driver
-    void* p = nullptr;
-    PCB_CUDA_TRY(ctx, cudaMallocAsync(&p, (size_t)(bytes - have), ctx->stream));
-    PCB_CUDA_TRY(ctx, cudaFreeAsync(p, ctx->stream));
-    PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    PCB_CUDA_TRY(ctx, cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have));
+  const Vmm& v = Vmm::get();
+  auto& cache = ctx->chunk_cache;
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = ctx->device;
+  // physical chunks created now, mapped into whichever buffer grows later (DevBuf::ensure)
+  while ((uint64_t)cache.free_chunks.size() * ChunkCache::kChunk < bytes) {
+    CUmemGenericAllocationHandle h;
+    if (v.create(&h, ChunkCache::kChunk, &prop, 0) != CUDA_SUCCESS)
+      return fail(ctx, PCB_CUDA, "pcb_ctx_reserve: the device has no room for %llu bytes", (unsigned long long)bytes);
+    cache.free_chunks.push_back(h);
   }
-  if (reserved_out) *reserved_out = have;
+  if (reserved_out) *reserved_out = (uint64_t)cache.free_chunks.size() * ChunkCache::kChunk;
   return PCB_OK;
 }
 

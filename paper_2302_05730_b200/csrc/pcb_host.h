@@ -1,9 +1,11 @@
 // Host-side runtime shared by the C-ABI translation units: context, device buffers, launch helpers.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <array>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -16,40 +18,138 @@
 
 namespace pcb {
 
-// Device scratch buffer of a context.  Memory comes from the device's stream-ordered pool on the context's stream
-// (cudaMallocAsync / cudaFreeAsync; the pool's release threshold is raised to "never" at context creation), so
-// growing a buffer in the middle of a refinement neither synchronises the device nor returns memory to the
-// driver: a released block is reused by the next request of the same stream -- in this call or in the next one.
-// (Round 1 used cudaFree + cudaMalloc here: a device-wide synchronisation and a driver allocation per growth step,
-// up to 17x on a cold refine().)
+// ------------------------------------------------------------------------------------------------------------
+// Device scratch memory of a context: growable buffers on CUDA's virtual memory management API.
+// A DevBuf reserves a (large) virtual address range once and backs it with physical chunks on demand: growing a
+// buffer maps more chunks BEHIND the ones in use -- the base pointer never changes, nothing is freed or copied,
+// nothing depends on an allocator's free-list state -- and a context never hands memory back before it is
+// destroyed.  The region lists of a refinement double every iteration; with this layout the growth of a list to
+// 3.4 GB costs ~50 map calls in total, whatever ran before.
+// (Round 1 grew buffers with cudaFree + cudaMalloc: a device-wide synchronisation and a driver allocation per step,
+// up to 17x on a refine() that outgrew its buffers.  The stream-ordered pool tried first in round 2 removed that but
+// showed rare 0.2-1.5 s stalls when a request of several GB met a fragmented pool: profiles/r2_cold_call.txt history.)
+// The driver entry points are taken through cudaGetDriverEntryPoint: the library does not link libcuda, so it still
+// loads on a machine without a driver (the CPU test-suite checks the exported symbols there).
+// ------------------------------------------------------------------------------------------------------------
+struct Vmm {
+  CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*address_free)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  bool ok = false;
+  static const Vmm& get() {
+    static const Vmm v = [] {
+      Vmm x;
+      auto load = [](const char* name, void** fn) {
+        cudaDriverEntryPointQueryResult q;
+        return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess && *fn;
+      };
+      x.ok = load("cuMemAddressReserve", (void**)&x.reserve) && load("cuMemAddressFree", (void**)&x.address_free) &&
+             load("cuMemCreate", (void**)&x.create) && load("cuMemRelease", (void**)&x.release) && load("cuMemMap", (void**)&x.map) &&
+             load("cuMemUnmap", (void**)&x.unmap) && load("cuMemSetAccess", (void**)&x.set_access) &&
+             load("cuMemGetAllocationGranularity", (void**)&x.granularity);
+      (void)cudaGetLastError();
+      return x;
+    }();
+    return v;
+  }
+};
+
+// physical chunks created ahead of time (pcb_ctx_reserve) and handed to the buffers that grow
+struct ChunkCache {
+  static constexpr size_t kChunk = (size_t)64 << 20;
+  std::vector<CUmemGenericAllocationHandle> free_chunks;   // each kChunk bytes
+};
+
 struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  const cudaStream_t* stream = nullptr;   // the owning context's stream (set by pcb_ctx's constructor)
+  void* p = nullptr;      // base of the reserved range; stable once set
+  size_t cap = 0;         // bytes backed by physical memory
+  const int* device = nullptr;        // the owning context's device ordinal
+  ChunkCache* cache = nullptr;        // the owning context's pre-created chunks
+  size_t va = 0;
+  struct Mapped { CUmemGenericAllocationHandle h; size_t bytes; };
+  std::vector<Mapped> chunks;
+  static constexpr size_t kVirtual = (size_t)1 << 37;   // 128 GiB of address space per buffer
   ~DevBuf() { release(); }
   void release() {
-    if (p) {
-      if (stream && *stream) cudaFreeAsync(p, *stream);
-      else cudaFree(p);
+    const Vmm& v = Vmm::get();
+    if (p && v.ok) {
+      if (cap) v.unmap((CUdeviceptr)p, cap);
+      for (auto& c : chunks) v.release(c.h);
+      v.address_free((CUdeviceptr)p, va);
     }
+    chunks.clear();
     p = nullptr;
     cap = 0;
+    va = 0;
   }
-  // grow-only; contents are NOT preserved
+  // grow-only; the base pointer and the contents are preserved
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
-    release();
-    size_t want = bytes + bytes / 8 + 256;
-    auto get = [&](size_t n) { return (stream && *stream) ? cudaMallocAsync(&p, n, *stream) : cudaMalloc(&p, n); };
-    cudaError_t e = get(want);
-    if (e != cudaSuccess) {
-      (void)cudaGetLastError();
-      e = get(bytes);
-      want = bytes;
-    }
-    if (e == cudaSuccess) cap = want;
-    else p = nullptr;
+    static const bool debug = std::getenv("PCB_DEBUG_MEM") != nullptr;
+    if (!debug) return grow(bytes);
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t before = cap, cached = cache ? cache->free_chunks.size() : 0;
+    const cudaError_t e = grow(bytes);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "DevBuf %p: %zu -> %zu MiB (asked %zu MiB, %zu cached chunks used) in %.3f ms\n", p, before >> 20, cap >> 20,
+                 bytes >> 20, cached - (cache ? cache->free_chunks.size() : 0), ms);
     return e;
+  }
+  cudaError_t grow(size_t bytes) {
+    const Vmm& v = Vmm::get();
+    if (!v.ok || !device) return cudaErrorNotSupported;
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = *device;
+    size_t gran = (size_t)2 << 20;
+    if (v.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || gran == 0) gran = (size_t)2 << 20;
+    if (!p) {
+      CUdeviceptr base = 0;
+      if (v.reserve(&base, kVirtual, 0, 0, 0) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+      p = (void*)base;
+      va = kVirtual;
+    }
+    if (bytes > va) return cudaErrorMemoryAllocation;
+    CUmemAccessDesc acc = {};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    auto map_one = [&](CUmemGenericAllocationHandle h, size_t n) -> bool {
+      if (v.map((CUdeviceptr)p + cap, n, 0, h, 0) != CUDA_SUCCESS) return false;
+      if (v.set_access((CUdeviceptr)p + cap, n, &acc, 1) != CUDA_SUCCESS) { v.unmap((CUdeviceptr)p + cap, n); return false; }
+      chunks.push_back({h, n});
+      cap += n;
+      return true;
+    };
+    // geometric growth (a list that doubles per iteration maps ~2 new ranges per step); big steps take the
+    // context's pre-created 64-MiB chunks first
+    size_t want = bytes - cap;
+    if (want < cap / 2) want = cap / 2;
+    want = (want + gran - 1) / gran * gran;
+    while (cache && want >= ChunkCache::kChunk && !cache->free_chunks.empty() && cap < bytes + ChunkCache::kChunk) {
+      CUmemGenericAllocationHandle h = cache->free_chunks.back();
+      if (!map_one(h, ChunkCache::kChunk)) break;
+      cache->free_chunks.pop_back();
+      want = want > ChunkCache::kChunk ? want - ChunkCache::kChunk : 0;
+      if (cap >= bytes && want < ChunkCache::kChunk) break;
+    }
+    while (cap < bytes || want >= gran) {
+      size_t n = want >= gran ? want : (bytes - cap + gran - 1) / gran * gran;
+      CUmemGenericAllocationHandle h;
+      if (v.create(&h, n, &prop, 0) != CUDA_SUCCESS) {
+        if (cap >= bytes) break;                        // the geometric extra is optional
+        n = (bytes - cap + gran - 1) / gran * gran;     // exact need only
+        if (v.create(&h, n, &prop, 0) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+      }
+      if (!map_one(h, n)) { v.release(h); return cudaErrorMemoryAllocation; }
+      want = 0;
+    }
+    return cap >= bytes ? cudaSuccess : cudaErrorMemoryAllocation;
   }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
@@ -123,8 +223,9 @@ struct pcb_ctx {
             &mc_hist, &mc_contrib, &mc_seg, &mc_group, &mc_tmp, &mc_inject, &mc_state, &mc_tables, &mc_timeline, &mc_row,
             &mc_gathered, &pg_row, &pg_gathered, &pg_lists, &pg_rowb};
   }
+  pcb::ChunkCache chunk_cache;
   pcb_ctx() {
-    for (pcb::DevBuf* b : buffers()) b->stream = &stream;
+    for (pcb::DevBuf* b : buffers()) { b->device = &device; b->cache = &chunk_cache; }
   }
   void release_buffers() {
     for (pcb::DevBuf* b : buffers()) b->release();
