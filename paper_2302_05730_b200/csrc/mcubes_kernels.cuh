@@ -123,7 +123,10 @@ __device__ __forceinline__ void draw_axis(const SampleArgs& a, const double* s_b
   bin_j = b;
 }
 
-constexpr int kSampleWarps = 8;  // warps per CTA; two CTAs per SM at 128 registers
+#ifndef PCB_SAMPLE_WARPS
+#define PCB_SAMPLE_WARPS 8
+#endif
+constexpr int kSampleWarps = PCB_SAMPLE_WARPS;  // warps per CTA; two CTAs per SM at 128 registers
 constexpr int kSlot = kSampleWarps * 32;   // records per staged sample slot
 
 // shared memory of one CTA: boundaries, one table row + tag bytes per axis, the staged records of TWO rounds

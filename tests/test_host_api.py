@@ -167,3 +167,21 @@ def test_abs_tol_is_an_extension_with_reference_default():
         pb.PaganiConfig(abs_tol=-1.0)
     c = _native.pagani_config_to_c(pb.PaganiConfig(rel_tol=1e-4, abs_tol=2e-9))
     assert (c.rel_tol, c.abs_tol) == (1e-4, 2e-9)
+
+
+def test_bench_refuses_to_claim_gpus_it_does_not_have():
+    """`bench.py --gpus N` launched without torchrun spawns N ranks itself -- and says so instead of printing n_gpus = N
+    from one process when the node has fewer devices (missing #2)."""
+    import json
+    import subprocess
+    import sys
+    proc = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"], capture_output=True,
+                          text=True, timeout=300, env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK")})
+    assert proc.returncode == 2, (proc.stdout, proc.stderr[-500:])
+    line = json.loads(proc.stdout.strip().splitlines()[-1])
+    assert "error" in line and "n_gpus" not in line
+    # under a launcher whose world size disagrees with --gpus it refuses as well
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    proc = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"], capture_output=True,
+                          text=True, timeout=300, env=env)
+    assert proc.returncode != 0 and "refusing to report n_gpus=4" in proc.stderr

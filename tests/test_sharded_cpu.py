@@ -202,3 +202,50 @@ def test_sharded_pagani_is_bit_identical_to_single_process(tmp_path, family, d, 
     # the final lists are balanced to within one region
     sizes = [int(r["final_local"]) for r in ranks]
     assert max(sizes) - min(sizes) <= 1
+
+
+# ================================================================================ tensor-level collectives
+def _tensor_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_05730_b200 import sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = sharded.Comm()
+        # in-place all-gather: the rank's row sits at its own slot of the target, like the library's packed rows
+        n = 7
+        gathered = torch.zeros(world * n, dtype=torch.float64)
+        row = torch.arange(n, dtype=torch.float64) + 100.0 * rank
+        comm.all_gather_into(gathered, row)
+        table = torch.full((5,), float(rank + 1), dtype=torch.float64)
+        comm.all_reduce_sum_(table)
+        peak = torch.tensor([float(rank), -float(rank)], dtype=torch.float64)
+        comm.all_reduce_max_(peak)
+        # ring exchange of [2][d][n] row blocks of different sizes
+        d = 3
+        right, left = (rank + 1) % world, (rank - 1) % world
+        send = torch.full((2, d, rank + 1), float(rank), dtype=torch.float64)
+        recv = torch.empty((2, d, left + 1), dtype=torch.float64)
+        comm.exchange_tensors({right: send}, {left: recv})
+        np.savez(os.path.join(out_dir, f"t{rank}.npz"), gathered=gathered.numpy(), table=table.numpy(), peak=peak.numpy(),
+                 recv=recv.numpy(), left=left)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_comm_tensor_collectives_under_gloo(tmp_path, world):
+    """The tensor-level surface the device drivers use (all_gather_into, all_reduce_sum_/max_, exchange_tensors), on CPU
+    tensors under gloo: same calls, same semantics as under NCCL on the library's device buffers."""
+    mp.spawn(_tensor_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for rank in range(world):
+        z = np.load(tmp_path / f"t{rank}.npz")
+        want = np.concatenate([np.arange(7) + 100.0 * r for r in range(world)])
+        assert np.array_equal(z["gathered"], want)
+        assert np.array_equal(z["table"], np.full(5, world * (world + 1) / 2))
+        assert np.array_equal(z["peak"], [world - 1.0, 0.0])
+        left = int(z["left"])
+        assert z["recv"].shape == (2, 3, left + 1) and np.all(z["recv"] == left)
