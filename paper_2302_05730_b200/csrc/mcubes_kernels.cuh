@@ -14,12 +14,17 @@
 //   bin       warp w serves axis w (w + 8 for D > 8): it adds the records the CTA staged in the PREVIOUS round to
 //             ITS private row of the contribution table (n_bins doubles in shared memory).  Shared-memory FP64
 //             atomicAdd is a CAS loop on sm_100 (ATOMS.CAST.SPIN), so same-bin lanes are arbitrated by a tag round
-//             (winner does a plain read-modify-write), losers take a second round, triple collisions use the CAS
-//             atomic.
+//             (the winner does a plain read-modify-write); a loser keeps its record in a one-deep pending slot that
+//             takes part in its next call (d >= 7) or is flushed at the end of the round (d <= 6); a second loss
+//             before the slot is free uses the CAS atomic (bin_pair_carry / bin_pair_flush below).
 // The staging is double-buffered and the accumulation is dealt over the axis steps of the draw as straight-line
 // code, so the shared-memory round trips of `bin` hide behind the integer / FP64 arithmetic of `draw` inside every
 // warp; one barrier per round.  No sample record ever travels to HBM.  Rows are merged CTA -> grid in a fixed
-// order (reduce_kernel), so the table is deterministic.
+// order (reduce_kernel).  The ORDER in which same-bin contributions of one warp are added is decided by which
+// lane's tag store lands last (and, for the rare CAS path, by the order of the compare-and-swaps): fixed by the
+// hardware for a given launch configuration -- the tests find the table bit-reproducible run to run on the B200 --
+// but not by the CUDA memory model.  The contract is therefore "contribution table to summation order" (1e-12
+// against the reference); (integral, variance), which never pass through this path, are bit-reproducible by design.
 #pragma once
 
 #include <type_traits>
