@@ -32,7 +32,7 @@
 #include "pagani_eval_mult.cuh"
 
 #ifndef PCB_LANES_GENERIC_W
-#define PCB_LANES_GENERIC_W 4
+#define PCB_LANES_GENERIC_W 0   // 4 or 8: force the chains per lane of the generic lane kernel (experiments); 0: measured choice
 #endif
 #ifndef PCB_LANES_HALVES_REAL
 #define PCB_LANES_HALVES_REAL 1   // 2: real families also split the virtual threads over two warps (measured slower: f4 d=8 0.57 vs 0.41 ms)
@@ -54,7 +54,6 @@ struct LaneLayout {
   static constexpr int kTerm = 5 * D;                             // doubles per lane: term[j][c], c = 0..4
   // term[j][c], c = 1..4, is replaced in place by the VALUE of the axial point (j, c) once the tables are complete
   // (every slot has exactly one reader, the warp that evaluates that point; the centre terms stay)
-  static constexpr int kDesc = 4 * (kPairs > 0 ? kPairs : 1);     // unsigned per CTA
   // the two warps of a CTA share the tables of 32 regions and take virtual threads 0..31 and 32..63; the second
   // warp hands over its five sums.  Scratch per lane: the D centre factors while the tables are built, afterwards
   // the hand-over slots
@@ -63,10 +62,33 @@ struct LaneLayout {
     return a > b ? a : b;
   }
   static constexpr size_t smem_bytes(size_t vsize) {
-    return 32 * (kTab * vsize + (size_t)kTerm * 8 + scratch_doubles(vsize) * 8) + 6 * 8 * 8 + (size_t)kDesc * 4;
+    return 32 * (kTab * vsize + (size_t)kTerm * 8 + scratch_doubles(vsize) * 8) + 6 * 8 * 8;
   }
 };
 
+// Pair point q = 4 * pair + signs of the rule (quadrature.py:186-197) as data: the byte offsets, inside a lane's
+// tables, of its three factors -- Rab[pair], phi[a][3 + (q & 1)], phi[b][3 + (q >> 1 & 1)].  Constant memory, indexed by
+// loop counters only: the loads and the offsets stay on the uniform datapath and a gather is one shared-memory
+// load with a uniform offset (the descriptors used to sit in shared memory: a mask / shift and a multiply-add per gather).
+template <int D, bool UNIT, bool HALVES, int VSIZE>
+struct PairPointTable {
+  using L = LaneLayout<D, UNIT, HALVES>;
+  unsigned w[4 * (L::kPairs > 0 ? L::kPairs : 1)][4];
+  constexpr PairPointTable() : w{} {
+    int e = 0;
+    for (int a = 0; a < D; ++a)
+      for (int b = a + 1; b < D; ++b, ++e)
+        for (int sg = 0; sg < 4; ++sg) {
+          unsigned* d = w[4 * e + sg];
+          d[0] = (unsigned)(L::kRab + e) * 32u * VSIZE;
+          d[1] = (unsigned)(L::kP34 + 2 * a + (sg & 1)) * 32u * VSIZE;
+          d[2] = (unsigned)(L::kP34 + 2 * b + ((sg >> 1) & 1)) * 32u * VSIZE;
+          d[3] = 0u;
+        }
+  }
+};
+template <int D, bool UNIT, bool HALVES, int VSIZE>
+__constant__ PairPointTable<D, UNIT, HALVES, VSIZE> kPairPoints = PairPointTable<D, UNIT, HALVES, VSIZE>();
 
 // level LEV of a binary counter over blocks: an odd index closes the pair (left + right) and carries upward
 template <int LEV, int NLEV>
@@ -118,19 +140,8 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
   V* cen_s = reinterpret_cast<V*>(smem_raw + sizeof(V) * 32 * L::kTab + 8 * 32 * L::kTerm) + lane;   // cen_s[j * 32] (table phase)
   double* xfer = scratch;                                                                           // xfer[k * 32]: the second half's sums
   double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (sizeof(V) * L::kTab + 8 * L::kTerm + 8 * kScratchD));   // [6][8]
-  unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                                          // [4 * kPairs]
 
   const pcb_rule& rule = args.rule;
-  // pair point q = 4 * pair + signs -> entry indices of its three factors
-  for (int q = threadIdx.x; q < 4 * L::kPairs; q += 32 * kHalves) {
-    const int e = q >> 2;
-    int a = 0, b = 0, idx = 0;
-    for (int j = 0; j < D; ++j)
-      for (int k = j + 1; k < D; ++k, ++idx)
-        if (idx == e) { a = j; b = k; }
-    desc[q] = (unsigned)(L::kRab + e) | ((unsigned)(L::kP34 + 2 * a + (q & 1)) << 10) | ((unsigned)(L::kP34 + 2 * b + ((q >> 1) & 1)) << 20);
-    (void)e;
-  }
   if (threadIdx.x < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
     const int o = threadIdx.x / 5, k = threadIdx.x % 5;
     double w = rule.weights[k][o < 5 ? o : 4];
@@ -144,10 +155,13 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
 
   // value of pair / corner points from the lane's tables
   V full = one;   // unit-modulus families: product of the centre factors of the current region
+  auto tab_at = [&](unsigned byte_off) -> V {
+    return *reinterpret_cast<const V*>(reinterpret_cast<const unsigned char*>(tab) + byte_off);
+  };
   auto pair_value = [&](int i) -> double {
-    const unsigned dsc = desc[i - 1 - 4 * D];
-    const V lead = MF::unit ? full : tab[(dsc & 1023u) * 32];
-    const V v = mmul(mmul(lead, tab[((dsc >> 10) & 1023u) * 32]), tab[(dsc >> 20) * 32]);
+    const unsigned* dsc = kPairPoints<D, MF::unit, (PCB_LANES_HALVES_REAL > 1 || MF::cplx), (int)sizeof(V)>.w[i - 1 - 4 * D];
+    const V lead = MF::unit ? full : tab_at(dsc[0]);
+    const V v = mmul(mmul(lead, tab_at(dsc[1])), tab_at(dsc[2]));
     return v.re * jac;
   };
   auto corner_head = [&](unsigned bits) -> V {   // groups 0 and 1 (all groups when D < 6)
@@ -496,8 +510,45 @@ struct GenericLaneLayout {
   static constexpr int kCorner0 = 2 * D * D + 2 * D + 1;
   static constexpr int kSteps = (kFe + 63) / 64;
   static constexpr int kTerm = 7 * D;   // doubles per lane
-  static constexpr size_t smem_bytes() { return 32 * (size_t)(kTerm + D) * 8 + 6 * 8 * 8 + (size_t)kCorner0 * 4; }
+  static constexpr size_t smem_bytes() { return 32 * (size_t)(kTerm + D) * 8 + 6 * 8 * 8; }
 };
+
+// Centre / axial / pair point i of the rule (quadrature.py:168-197), as data: which abscissa c_j in 0..4 every axis
+// takes (one byte per axis: `__byte_perm` turns byte j into the byte offset c_j * 256 of the lane's term table in ONE
+// instruction) and the row of its orbit weights.  The table lives in constant memory and is indexed by loop
+// counters only, so the loads, the extraction and the resulting offsets stay on the uniform datapath and the
+// D gathers of a point are D shared-memory loads with a uniform offset -- until round 2 of this build the
+// descriptor sat in shared memory and every gather paid two compares, two selects and a multiply-add per axis
+// (18 % of the kernel's instructions, profiles/r2_ncu_pagani_lanes_f3_d8_before.txt).
+template <int D>
+struct PlainPointTable {
+  unsigned w[2 * D * D + 2 * D + 1][4];   // [i][0..2]: bytes c_0..c_11, [i][3]: orbit row
+  constexpr PlainPointTable() : w{} {
+    const int n = 2 * D * D + 2 * D + 1;
+    for (int i = 0; i < n; ++i) {
+      int a = -1, b = -1, ca = 0, cb = 0, orbit = 0;
+      if (i == 0) {
+      } else if (i <= 2 * D) {
+        const int q = i - 1; a = q >> 1; ca = 1 + (q & 1); orbit = 1;
+      } else if (i <= 4 * D) {
+        const int q = i - 1 - 2 * D; a = q >> 1; ca = 3 + (q & 1); orbit = 2;
+      } else {
+        const int q = i - 1 - 4 * D, pr = q >> 2, sg = q & 3;
+        int idx = 0;
+        for (int j = 0; j < D; ++j)
+          for (int k = j + 1; k < D; ++k, ++idx)
+            if (idx == pr) { a = j; b = k; }
+        ca = 3 + (sg & 1); cb = 3 + (sg >> 1); orbit = 3;
+      }
+      for (int k = 0; k < 4; ++k) w[i][k] = 0u;
+      if (a >= 0) w[i][a >> 2] |= (unsigned)ca << (8 * (a & 3));
+      if (b >= 0) w[i][b >> 2] |= (unsigned)cb << (8 * (b & 3));
+      w[i][3] = (unsigned)orbit;
+    }
+  }
+};
+template <int D>
+__constant__ PlainPointTable<D> kPlainPoints = PlainPointTable<D>();
 
 // corner combine over the lane's table, same association as CornerCombine (pagani_eval.cuh)
 template <class F, int D>
@@ -545,8 +596,22 @@ struct LaneCorner {
   }
 };
 
+#ifndef PCB_LANES_GENERIC_MINB
+#define PCB_LANES_GENERIC_MINB 12
+#endif
+// Independent dependency chains per lane.  Eight chains at 255 registers (8 resident warps per SM) against four at
+// 168 (12 warps), measured on lists of 2.5e5 .. 1.7e6 regions after the point descriptors moved to constant memory
+// [r2]: f3 gains at every d (its final map is a 19-operation FP64 chain per point: d=8 2.16 -> 2.48e11 evaluations/s,
+// d=6 1.45 -> 2.19e11); f2 gains for d = 6..9 (d=8 3.74 -> 4.13e11, d=6 2.72 -> 3.06e11) and loses outside
+// (d=5 2.36 -> 2.09e11, d=10 5.68 -> 5.17e11).
 template <int FAM, int D>
-__global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
+__host__ __device__ constexpr int generic_lane_chains() {
+  if (PCB_LANES_GENERIC_W != 0) return PCB_LANES_GENERIC_W;
+  if (FAM == PCB_F3_CORNER_PEAK) return 8;
+  return (D >= 6 && D <= 9) ? 8 : 4;
+}
+template <int FAM, int D>
+__global__ void __launch_bounds__(32, generic_lane_chains<FAM, D>() == 8 ? 1 : PCB_LANES_GENERIC_MINB) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
   using F = Family<FAM>;
   using L = GenericLaneLayout<D>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -554,25 +619,8 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
   double* term = reinterpret_cast<double*>(smem_raw) + lane;               // term[(7j + c) * 32]
   double* stash = term + 32 * L::kTerm;                                    // stash[j * 32]
   double* s_w = reinterpret_cast<double*>(smem_raw + 32 * (size_t)(L::kTerm + D) * 8);   // [6][8]
-  unsigned* desc = reinterpret_cast<unsigned*>(s_w + 48);                  // [kCorner0]: a | ca << 4 | b << 8 | cb << 12 | orbit << 16
 
   const pcb_rule& rule = args.rule;
-  for (int i = lane; i < L::kCorner0; i += 32) {
-    int a = 15, b = 15, ca = 0, cb = 0, orbit = 0;
-    if (i == 0) {
-    } else if (i <= 2 * D) {
-      int q = i - 1; a = q >> 1; ca = 1 + (q & 1); orbit = 1;
-    } else if (i <= 4 * D) {
-      int q = i - 1 - 2 * D; a = q >> 1; ca = 3 + (q & 1); orbit = 2;
-    } else {
-      int q = i - 1 - 4 * D, pr = q >> 2, sg = q & 3, idx = 0;
-      for (int j = 0; j < D; ++j)
-        for (int k = j + 1; k < D; ++k, ++idx)
-          if (idx == pr) { a = j; b = k; }
-      ca = 3 + (sg & 1); cb = 3 + (sg >> 1); orbit = 3;
-    }
-    desc[i] = (unsigned)a | ((unsigned)ca << 4) | ((unsigned)b << 8) | ((unsigned)cb << 12) | ((unsigned)orbit << 16);
-  }
   if (lane < 30) {  // orbit weights; rows 4 / 5: corners with even / odd bit count (quadrature.py:199-203)
     const int o = lane / 5, k = lane % 5;
     double w = rule.weights[k][o < 5 ? o : 4];
@@ -582,15 +630,43 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
   __syncwarp();
   const double jac = args.f.bounded ? args.f.jac : 1.0;   // x * 1.0 == x
 
-  // centre / axial / pair point i: its D terms in numpy's order
-  auto plain_value = [&](int i, int& row) -> double {
-    const unsigned dsc = desc[i];
-    const int a = dsc & 15u, ca = (dsc >> 4) & 15u, b = (dsc >> 8) & 15u, cb = (dsc >> 12) & 15u;
-    row = (int)(dsc >> 16);
+  // centre / axial / pair point i: its D terms combined in numpy's order (the final map is applied W points at a time)
+  auto plain_sum = [&](int i, int& row) -> double {
+    const unsigned* dsc = kPlainPoints<D>.w[i];
+    row = (int)dsc[3];
     double t[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) t[j] = term[(7 * j + (j == a ? ca : (j == b ? cb : 0))) * 32];
-    return F::template finish<D>(combine_terms<F, D>(t), args.f) * jac;
+    for (int j = 0; j < D; ++j) {
+      const unsigned off = __byte_perm(dsc[j >> 2], 0u, 0x4404u | ((unsigned)(j & 3) << 4));   // c_j * 256 bytes
+      t[j] = *reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(term) + 7 * j * 256 + off);
+    }
+    return combine_terms<F, D>(t);
+  };
+  // The final map of W independent points.  A family whose map has an off-domain branch (f3: libm semantics for
+  // 1 + s <= 0 and the extremes) offers a branch-free form for arguments known to be in the domain; `fast` (warp-
+  // uniform: every lane's region keeps all its sums inside the domain) selects it, and the W dependency chains
+  // become one straight-line block the compiler interleaves.  With the branch inside every evaluation the chains ran
+  // one after the other and the kernel waited on the FP64 latency (f3 d=8: 0.70 -> see DESIGN 4.1).
+  bool fast = true;
+  auto finish_block = [&](auto& sums) {
+    constexpr int N = (int)(sizeof(sums) / sizeof(double));
+    if constexpr (HasIndomainFinish<F>::value) {
+      if (fast) {
+        F::template finish_indomain_many<D, N>(sums, args.f);
+#pragma unroll
+        for (int v = 0; v < N; ++v) sums[v] = sums[v] * jac;
+      } else {
+#pragma unroll
+        for (int v = 0; v < N; ++v) sums[v] = finish_out_of_line<F, D>(sums[v], args.f) * jac;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < N; ++v) sums[v] = F::template finish<D>(sums[v], args.f) * jac;
+    }
+  };
+  auto finish_one = [&](double sum) -> double {
+    if constexpr (HasIndomainFinish<F>::value) return finish_out_of_line<F, D>(sum, args.f) * jac;
+    else return F::template finish<D>(sum, args.f) * jac;
   };
 
   for (long long batch = blockIdx.x; batch * 32 < args.n; batch += gridDim.x) {
@@ -599,6 +675,7 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
     const long long rc = live ? r : args.n - 1;
     double vol = 1.0;
     double next_left = args.lefts[rc], next_len = args.lengths[rc];
+    double sum_min = 0.0, sum_abs = 0.0;   // bounds of the combined sums of this region (families with a domain)
 #pragma unroll 1
     for (int j = 0; j < D; ++j) {
       const double left = next_left, len = next_len;
@@ -607,14 +684,23 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
         next_len = args.lengths[(j + 1) * args.ld + rc];
       }
       vol = (j == 0) ? len : vol * len;   // np.prod, left to right
+      double t_min = 0.0, t_abs = 0.0;
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
         const double x = left + len * rule.offsets[c];   // quadrature.py:301-302: mul, then add
-        term[(7 * j + c) * 32] = axis_term<F>(j, x, args.f);
+        const double t = axis_term<F>(j, x, args.f);
+        term[(7 * j + c) * 32] = t;
+        if constexpr (HasIndomainFinish<F>::value) {
+          t_min = c == 0 ? t : fmin(t_min, t);
+          t_abs = c == 0 ? fabs(t) : fmax(t_abs, fabs(t));
+        }
       }
+      sum_min += t_min;
+      sum_abs += t_abs;
     }
+    if constexpr (HasIndomainFinish<F>::value) fast = __all_sync(PCB_FULL_MASK, F::sums_indomain(sum_min, sum_abs));
 
-    constexpr int W = PCB_LANES_GENERIC_W;
+    constexpr int W = generic_lane_chains<FAM, D>();
     constexpr int kLevels = W == 8 ? 3 : 4;   // log2(64 / W)
     double two_f0 = 0.0, first_of_pair = 0.0, best = -1.0;
     int axis = 0;
@@ -680,7 +766,8 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
         }
         double fx[W];
 #pragma unroll
-        for (int v = 0; v < W; ++v) fx[v] = F::template finish<D>(head[v].tail_up(up[v < kSplit ? 0 : 1]), args.f) * jac;
+        for (int v = 0; v < W; ++v) fx[v] = head[v].tail_up(up[v < kSplit ? 0 : 1]);
+        finish_block(fx);
 #pragma unroll
         for (int v = 0; v < W; ++v)
 #pragma unroll
@@ -705,7 +792,8 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
           double fx[W];
           int row[W];
 #pragma unroll
-          for (int v = 0; v < W; ++v) fx[v] = plain_value(lo + v, row[v]);
+          for (int v = 0; v < W; ++v) fx[v] = plain_sum(lo + v, row[v]);
+          finish_block(fx);
 #pragma unroll
           for (int v = 0; v < W; ++v) {
             split_note(lo + v, fx[v]);
@@ -716,8 +804,8 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
         } else if (!kSharedCorners && lo >= L::kCorner0 && hi < L::kFe) {   // W corner points, each with its own weights
           double fx[W];
 #pragma unroll
-          for (int v = 0; v < W; ++v)
-            fx[v] = F::template finish<D>(head[v].tail(term, (unsigned)(lo + v - L::kCorner0)), args.f) * jac;
+          for (int v = 0; v < W; ++v) fx[v] = head[v].tail(term, (unsigned)(lo + v - L::kCorner0));
+          finish_block(fx);
 #pragma unroll
           for (int v = 0; v < W; ++v) {
             const double* w = s_w + 8 * (4 + (__popc((unsigned)(lo + v - L::kCorner0)) & 1));
@@ -731,11 +819,11 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
             double fx;
             int row;
             if (i < L::kCorner0) {
-              fx = plain_value(i, row);
+              fx = finish_one(plain_sum(i, row));
               split_note(i, fx);
             } else if (i < L::kFe) {
               const unsigned bits = (unsigned)(i - L::kCorner0);
-              fx = F::template finish<D>(head[v].tail(term, bits), args.f) * jac;
+              fx = finish_one(head[v].tail(term, bits));
               row = 4 + (__popc(bits) & 1);
             } else {
               continue;
@@ -767,12 +855,12 @@ __global__ void __launch_bounds__(32, PCB_LANES_GENERIC_W == 8 ? 1 : 12) pagani_
         for (int i = 0; i < L::kFe; ++i) {
           double fx;
           int row;
-          if (i < L::kCorner0) fx = plain_value(i, row);
+          if (i < L::kCorner0) fx = finish_one(plain_sum(i, row));
           else {
             LaneCorner<F, D> cc;
             const unsigned bits = (unsigned)(i - L::kCorner0);
             cc.head(term, bits & 63u);
-            fx = F::template finish<D>(cc.tail(term, bits), args.f) * jac;
+            fx = finish_one(cc.tail(term, bits));
           }
           if (!isfinite(fx)) {
             atomicMin(args.bad, (unsigned long long)r * (unsigned long long)L::kFe + (unsigned long long)i);

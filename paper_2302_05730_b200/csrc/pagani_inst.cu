@@ -47,11 +47,6 @@ static const void* lanes_kernel_for(size_t* smem, int* threads) {
     *smem = LaneLayout<D, MultFamily<PCB_FAM>::unit, (MultFamily<PCB_FAM>::cplx || PCB_LANES_HALVES_REAL > 1)>::smem_bytes(sizeof(MVal<MultFamily<PCB_FAM>::cplx>));
     *threads = (MultFamily<PCB_FAM>::cplx || PCB_LANES_HALVES_REAL > 1) ? 64 : 32;   // complex factors: two warps share the tables of 32 regions
     return (const void*)&pagani_eval_lanes_kernel<PCB_FAM, D>;
-  } else if constexpr (PCB_FAM == PCB_F3_CORNER_PEAK && D > 6) {
-    // the double-double power dominates f3; from d = 7 on the warp-per-region kernel hides its latency better
-    // (390625 regions at d = 8: 1.07 ms vs 1.59 ms; d = 6: 0.39 vs 0.32 ms, d = 5: 1.26 vs 1.15 ms)
-    *smem = 0;
-    return nullptr;
   } else {
     *smem = GenericLaneLayout<D>::smem_bytes();
     *threads = 32;
