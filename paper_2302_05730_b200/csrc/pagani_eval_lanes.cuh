@@ -34,6 +34,9 @@
 #ifndef PCB_LANES_GENERIC_W
 #define PCB_LANES_GENERIC_W 0   // 4 or 8: force the chains per lane of the generic lane kernel (experiments); 0: measured choice
 #endif
+#ifndef PCB_LANES_AXIAL_UNROLL
+#define PCB_LANES_AXIAL_UNROLL 2   // centre / axial evaluations in flight per warp (a full transcendental each)
+#endif
 #ifndef PCB_LANES_HALVES_REAL
 #define PCB_LANES_HALVES_REAL 1   // 2: real families also split the virtual threads over two warps (measured slower: f4 d=8 0.57 vs 0.41 ms)
 #endif
@@ -112,7 +115,13 @@ constexpr int lanes_min_blocks() {
   constexpr bool cplx = MultFamily<FAM>::cplx || PCB_LANES_HALVES_REAL > 1;   // two warps per CTA
   constexpr size_t smem = LaneLayout<D, MultFamily<FAM>::unit, cplx>::smem_bytes(MultFamily<FAM>::cplx ? 16 : 8) + 1024;
   constexpr int by_smem = (int)((227u << 10) / smem);
-  constexpr int cap = cplx ? 6 : 10;
+#ifndef PCB_LANES_CPLX_CAP
+#define PCB_LANES_CPLX_CAP 6
+#endif
+#ifndef PCB_LANES_CPLX_W
+#define PCB_LANES_CPLX_W 4
+#endif
+  constexpr int cap = cplx ? PCB_LANES_CPLX_CAP : 10;
   return by_smem < 1 ? 1 : (by_smem < cap ? by_smem : cap);
 }
 
@@ -250,7 +259,8 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     cta_sync();
     // the 4D + 1 centre / axial evaluations, dealt to the halves point by point; each value replaces the one term
     // that only its own evaluation reads
-#pragma unroll 2
+    constexpr int kAxialUnroll = PCB_LANES_AXIAL_UNROLL;
+#pragma unroll kAxialUnroll
     for (int q = half; q < 4 * D; q += kHalves) {
       const double fx = axial_eval(q);
       term[axial_slot(q) * 32] = fx;
@@ -298,7 +308,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
     //      levels of the pair tree are fixed-register adds, the remaining ones a binary counter over the blocks.
     // chains per lane: where the tables leave room for >= 10 warps per SM (d <= 6) four chains and more warps win, above
     // that the eight-chain version hides the latency better (measured: f4 d=5 0.50 -> 0.42 ms, d=6 0.185 -> 0.161, d=8 0.41 vs 0.45)
-    constexpr int W = kHalves > 1 ? 4 : (D <= 6 ? 4 : 8);
+    constexpr int W = kHalves > 1 ? PCB_LANES_CPLX_W : (D <= 6 ? 4 : 8);
     constexpr int kCounterLevels = (kVt / W) == 8 ? 3 : 4;   // log2(kVt / W)
     // split axis (pagani.py:215-223): first maximum over the axes of the fourth-difference indicator
     int axis = 0;
@@ -458,7 +468,21 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
 #pragma unroll
       for (int k = 0; k < 5; ++k) cur[k] = acc[0][k];
       // remaining levels: binary counter over the blocks
+#ifdef PCB_EXP_COUNTER_LOCAL
+      {
+        int lev = 0;
+#pragma unroll 1
+        while ((blk >> lev) & 1) {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) cur[k] = hold[lev][k] + cur[k];
+          ++lev;
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) hold[lev < kCounterLevels ? lev : 0][k] = cur[k];
+      }
+#else
       counter_merge<0, kCounterLevels>(blk, cur, hold);
+#endif
     }
     // top level of the pair tree: virtual threads 0..31 (half 0) + 32..63 (half 1)
     if constexpr (kHalves > 1) {
