@@ -400,8 +400,9 @@ pcb_status pcb_mcubes_shard_end(pcb_ctx* ctx, int32_t n_done, double* contributi
 pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,
                         const uint64_t* counters, double* out);
 
-/* ---- self-test hook: the sampler's division-by-constant sequence, out[i] = x[i] / g ----------
- * (tests compare it bit-for-bit with IEEE division; not part of the reference surface)          */
+/* ---- self-test hook: the sampler's division-by-constant sequence, out[i] = x[i] / g (g >= 1), and its
+ * branch-free reciprocal, out[i] = 1 / x[i] for normal x (g == 0)
+ * (tests compare both bit-for-bit with IEEE division; not part of the reference surface)          */
 pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g, double* out);
 
 #ifdef __cplusplus

@@ -310,7 +310,7 @@ __global__ void cube_values_kernel(int p, const double* __restrict__ fx, const d
 
 __global__ void debug_divide_kernel(long long n, const double* __restrict__ x, double g, double rg, double* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = div_by_const(x[i], g, rg);
+    out[i] = g > 0.0 ? div_by_const(x[i], g, rg) : rcp_normal(x[i]);
 }
 
 __global__ void deinterleave2_kernel(const double* __restrict__ in, int n, double* __restrict__ a, double* __restrict__ b) {

@@ -155,6 +155,7 @@ struct PassTail {
   double* row = nullptr;               // device: [2 * width] group pairs, then bad, clamps
   long long row_doubles = 0;
   bool defer_finish = false;
+  bool grid_in_unit = true;     // every boundary lies in [0, 1] (always true for grids refined on the device)
   const double* gathered = nullptr;    // device: world rows
   int world = 0;
   long long total_groups = 0;
@@ -212,6 +213,35 @@ static pcb_status enqueue_finish(pcb_ctx* ctx, const pcb_mcubes_plan* plan, cons
   return PCB_OK;
 }
 
+// PCB_FAST_DOMAIN (pcb_device.cuh): can the sampler evaluate the family's inner operations without their range tests?
+// Samples are grid points in [0, 1]^d pushed through the optional affine map of scale_to_bounds.
+static int sampler_fast_domain(const pcb_integrand* f, bool grid_in_unit) {
+  if (!grid_in_unit) return 0;
+  double lo[PCB_MAX_DIM], hi[PCB_MAX_DIM];
+  for (int j = 0; j < f->d; ++j) {
+    lo[j] = f->bounded ? f->low[j] : 0.0;
+    hi[j] = f->bounded ? f->low[j] + f->width[j] : 1.0;
+    if (!(std::isfinite(lo[j]) && std::isfinite(hi[j]))) return 0;
+    if (lo[j] > hi[j]) std::swap(lo[j], hi[j]);
+  }
+  if (f->family == PCB_F2_PRODUCT_PEAK) {          // a2 + u*u normal with a normal reciprocal
+    if (!(f->param[0] >= 0x1p-900 && f->param[0] <= 0x1p900)) return 0;
+    for (int j = 0; j < f->d; ++j)
+      if (!(std::fmax(std::fabs(lo[j] - 0.5), std::fabs(hi[j] - 0.5)) <= 0x1p400)) return 0;
+    return PCB_FAST_DOMAIN;
+  }
+  if (f->family == PCB_F3_CORNER_PEAK) {           // 1 + sum (j+1) x_j in [2^-20, 2^21], rounding of the sum below 2^-29
+    double sum_min = 0.0, sum_abs = 0.0;
+    for (int j = 0; j < f->d; ++j) {
+      const double a = (double)(j + 1) * lo[j], b = (double)(j + 1) * hi[j];
+      sum_min += std::fmin(a, b);
+      sum_abs += std::fmax(std::fabs(a), std::fabs(b));
+    }
+    return (sum_min >= -1.0 + 0x1p-20 && sum_abs <= 0x1p20) ? PCB_FAST_DOMAIN : 0;
+  }
+  return 0;
+}
+
 // Enqueue one V-Sample pass over logical threads [t_begin, t_end) with device-resident boundaries; nothing
 // here waits for the device.  Leaves: contributions in ctx->mc_contrib (d*nb), per-group (I, Var) in
 // ctx->mc_group, scalars (bad, clamps, integral, variance) in ctx->scalars[kMcSlot..]; with tail.hist_i set
@@ -243,6 +273,7 @@ static pcb_status enqueue_pass(pcb_ctx* ctx, const pcb_integrand* f, const pcb_m
 
   SampleArgs a;
   a.f = *f;
+  a.f.reserved = sampler_fast_domain(f, tail.grid_in_unit);
   a.g = plan->g; a.p = plan->p; a.nb = nb; a.squared_weighted = squared_weighted;
   a.m = plan->m; a.s = plan->s;
   a.n_threads = n_threads;
@@ -385,8 +416,10 @@ pcb_status pcb_mcubes_sample(pcb_ctx* ctx, const pcb_integrand* f, const pcb_mcu
   }
   long long n_groups = 0;
   PCB_TRY(arm_pass_scalars(ctx));
+  PassTail plain;
+  for (size_t i = 0; i < (size_t)d * (nb + 1) && plain.grid_in_unit; ++i) plain.grid_in_unit = boundaries[i] >= 0.0 && boundaries[i] <= 1.0;
   PCB_TRY(enqueue_pass(ctx, f, plan, ctx->mc_bounds[0].as<double>(), seed, rng_kind, inj, squared_weighted, thread_begin,
-                       thread_end, PassTail{}, &n_groups));
+                       thread_end, plain, &n_groups));
   PCB_TRY(read_mc_scalars(ctx));
   const unsigned long long* hu = (const unsigned long long*)ctx->pinned + kMcSlot;
   const double* hd = (const double*)ctx->pinned + kMcSlot;
@@ -522,13 +555,13 @@ pcb_status pcb_mcubes_sample_cube(pcb_ctx* ctx, const pcb_integrand* f, const pc
 }
 
 pcb_status pcb_debug_divide(pcb_ctx* ctx, int64_t n, const double* x, int32_t g, double* out) {
-  if (!ctx || n < 0 || g < 1 || (n > 0 && (!x || !out))) return fail(ctx, PCB_INVALID, "debug_divide: bad arguments");
+  if (!ctx || n < 0 || g < 0 || (n > 0 && (!x || !out))) return fail(ctx, PCB_INVALID, "debug_divide: bad arguments");
   if (n == 0) return PCB_OK;
   PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   PCB_CUDA_TRY(ctx, ctx->mc_tmp.ensure((size_t)n * 16));
   double* x_dev = ctx->mc_tmp.as<double>();
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(x_dev, x, (size_t)n * 8, cudaMemcpyHostToDevice, ctx->stream));
-  debug_divide_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(n, x_dev, (double)g, 1.0 / (double)g, x_dev + n);
+  debug_divide_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(n, x_dev, (double)g, g ? 1.0 / (double)g : 0.0, x_dev + n);
   ctx->launches++;
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(out, x_dev + n, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));

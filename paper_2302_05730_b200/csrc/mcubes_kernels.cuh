@@ -443,7 +443,19 @@ __global__ void __launch_bounds__(kSampleWarps * 32, vsample_ctas_per_sm(D)) vsa
                          (inj_cube + k + 1) * D, active, x[1][j], jac[1], bin[1][j]);
           bin_from(j * kSampleWarps / D, (j + 1) * kSampleWarps / D);
         }
-        const double fx[2] = {eval_at_sampler<F, D>(x[0], a.f), eval_at_sampler<F, D>(x[1], a.f)};
+        double fx[2];
+        if constexpr (kHasFastSampler<F>) {   // branch-free evaluation where the host established the domain (pcb_device.cuh)
+          if (a.f.reserved & PCB_FAST_DOMAIN) {
+            fx[0] = eval_at_sampler<F, D, true>(x[0], a.f);
+            fx[1] = eval_at_sampler<F, D, true>(x[1], a.f);
+          } else {
+            fx[0] = eval_at_sampler<F, D>(x[0], a.f);
+            fx[1] = eval_at_sampler<F, D>(x[1], a.f);
+          }
+        } else {
+          fx[0] = eval_at_sampler<F, D>(x[0], a.f);
+          fx[1] = eval_at_sampler<F, D>(x[1], a.f);
+        }
         const double v[2] = {fx[0] * jac[0], fx[1] * jac[1]};
         kc += 2ULL * D * kGolden;
         ctr += 2 * D;

@@ -66,6 +66,18 @@ def test_division_by_constant_is_ieee_exact():
         assert np.array_equal(_native.debug_divide(x, g), x / g), g
 
 
+def test_reciprocal_is_ieee_exact():
+    """rcp_normal (pcb_device.cuh): the branch-free reciprocal of the sampler's product-peak / corner-peak forms."""
+    rng = np.random.default_rng(11)
+    x = np.concatenate([
+        rng.random(2_000_000) + 1e-4, 0.0004 + 0.25 * rng.random(1_000_000),          # the range of a2 + u*u
+        np.ldexp(1.0 + rng.random(1_000_000), rng.integers(-900, 900, 1_000_000)),     # any normal exponent
+        np.nextafter(np.ldexp(1.0, np.arange(-100, 100)), 0), np.nextafter(np.ldexp(1.0, np.arange(-100, 100)), 4),
+        np.ldexp(1.0, np.arange(-100, 100)), 1.0 + np.ldexp(1.0, -np.arange(1, 53)), 2.0 - np.ldexp(1.0, -np.arange(1, 53)),
+        -(rng.random(1000) + 0.5)])
+    assert np.array_equal(_native.debug_divide(x, 0), 1.0 / x)
+
+
 def test_transform_matches_reference_example():
     x, jac, b = pb.transform(0.75, vegas.VegasGrid(1, 2, [[0.0, 0.8, 1.0]]))     # SPEC.md:294
     assert abs(x[0] - 0.9) < 1e-15 and abs(jac - 0.4) < 1e-15 and b[0] == 1
