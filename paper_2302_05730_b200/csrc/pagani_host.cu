@@ -91,6 +91,34 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   return PCB_OK;
 }
 
+// CUDA loads a kernel's code when it is first launched (lazy module loading): tens of milliseconds for the large
+// evaluate kernels, in the middle of whichever run happens to need the kernel first -- the config-5 sweep showed
+// it as runs 45x slower than a neighbour with more regions (the lane kernel is first used when a list passes 12288
+// regions).  A refinement therefore touches every kernel it may launch before its clock starts; once per kernel
+// and context.
+static pcb_status preload_refine_kernels(pcb_ctx* ctx, const pcb_integrand* f, const pcb_pagani_config* cfg) {
+  size_t lanes_smem = 0;
+  int lanes_threads = 32;
+  const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem, &lanes_threads) : nullptr;
+  const void* fns[] = {cfg->group_size > 64 ? eval_wide_kernel(f->family, f->d) : eval_kernel(f->family, f->d), lanes_fn,
+                       (const void*)&tiling_kernel, (const void*)&tree_level_kernel, (const void*)&short_iteration_kernel,
+                       (const void*)&classify_kernel, (const void*)&scan_counts_kernel, (const void*)&max_kernel,
+                       (const void*)&split_kernel};
+  for (const void* fn : fns) {
+    if (!fn || !ctx->preloaded.insert(fn).second) continue;
+    cudaFuncAttributes attr;
+    PCB_CUDA_TRY(ctx, cudaFuncGetAttributes(&attr, fn));
+  }
+  if (lanes_fn && lanes_smem <= ctx->smem_optin) {
+    size_t& have = ctx->smem_attr[lanes_fn];
+    if (have < lanes_smem) {
+      PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(lanes_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lanes_smem));
+      have = lanes_smem;
+    }
+  }
+  return PCB_OK;
+}
+
 pcb_status tree_sum_dev(pcb_ctx* ctx, const double* in, long long n, double* out) {
   if (n <= 0) {
     PCB_CUDA_TRY(ctx, cudaMemsetAsync(out, 0, sizeof(double), ctx->stream));
@@ -274,6 +302,7 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     return fail(ctx, PCB_BUDGET, "uniform split needs %.0Lf regions, cap is %lld", exact, (long long)cfg->region_cap);
   n = (long long)exact;
 
+  PCB_TRY(preload_refine_kernels(ctx, f, cfg));
   cudaEvent_t ev0, ev1;
   PCB_CUDA_TRY(ctx, cudaEventCreate(&ev0));
   PCB_CUDA_TRY(ctx, cudaEventCreate(&ev1));

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <set>
 #include <string>
 #include <utility>
 #include <vector>
@@ -165,6 +166,7 @@ struct pcb_ctx {
   size_t smem_per_sm = 0;
   size_t total_mem = 0;
   std::map<const void*, size_t> smem_attr;  // dynamic shared memory already granted per kernel
+  std::set<const void*> preloaded;          // kernels whose code is known to be loaded (lazy module loading)
   cudaStream_t stream = nullptr;
   std::string err;
   volatile int abort_requested = 0;   // pcb_ctx_abort(), polled by the drivers after every progress callback
