@@ -40,8 +40,25 @@ typedef enum {
   PCB_F6_DISCONTINUOUS = 5, /* exp(sum (i+4)x_i) below thresholds  integrands.py:95-118  */
   PCB_SUM = 6,              /* sum x_i                             integrands.py:121-128 */
   PCB_ONE = 7,              /* constant 1 (SPEC.md known answers)                        */
-  PCB_N_FAMILIES = 8
+  PCB_N_FAMILIES = 8         /* built-in families; ids PCB_USER_FAMILY_BASE .. +PCB_MAX_USER_FAMILIES-1 are run-time families */
 } pcb_family;
+
+/* Run-time families: a device functor compiled from user source against this library's own kernel templates
+ * (paper_2302_05730_b200/userfn.py writes the translation unit and runs nvcc), loaded as a cubin and bound to one
+ * dimension.  The reference integrates any Python callable (core.py:72-93); a callable cannot run on the device, its
+ * CUDA source can.  The kernels, launch paths and results contracts are the built-in families' own. */
+#define PCB_USER_FAMILY_BASE 8
+#define PCB_MAX_USER_FAMILIES 8
+typedef struct {
+  const char* eval;           /* pagani_eval_kernel<family, d>                 */
+  const char* eval_wide;      /* pagani_eval_kernel<family, d, true>           */
+  const char* lanes;          /* pagani_eval_lanes_generic_kernel<family, d>   */
+  const char* points;         /* eval_points_kernel<family, d>                 */
+  const char* invoke;         /* invoke_kernel<family, d>                      */
+  const char* qmc;            /* qmc_shift_kernel<family, d>                   */
+  const char* sample_hash;    /* vsample_kernel<family, d, PCB_RNG_REFERENCE_HASH> */
+  const char* sample_generic; /* vsample_kernel<family, d, PCB_RNG_PHILOX>     */
+} pcb_user_kernel_names;
 
 /* A compiled device functor is selected by (family, d); `param` carries the family's
  * constants as computed by the host in the reference's own expressions:
@@ -395,6 +412,14 @@ pcb_status pcb_mcubes_shard_wait(pcb_ctx* ctx, int32_t iteration, pcb_mcubes_ite
 /* drains the stream; contributions_out (n_done, d, n_bins) needs keep_tables; final_boundaries (d, n_bins+1) */
 pcb_status pcb_mcubes_shard_end(pcb_ctx* ctx, int32_t n_done, double* contributions_out, double* final_boundaries,
                                 double* seconds_device);
+
+/* ---- run-time families ------------------------------------------------------------------------
+ * Load `cubin` (compiled for sm_100a from this library's kernel templates) as family `family` in
+ * [PCB_USER_FAMILY_BASE, PCB_USER_FAMILY_BASE + PCB_MAX_USER_FAMILIES) for dimension d; every kernel named in
+ * `names` must exist in the image.  Process-wide; reloading a slot replaces it.                              */
+pcb_status pcb_user_family_load(pcb_ctx* ctx, int32_t family, int32_t d, const void* cubin, uint64_t bytes,
+                                const pcb_user_kernel_names* names);
+pcb_status pcb_user_family_unload(pcb_ctx* ctx, int32_t family);
 
 /* ---- RNG mirror: replaces mcubes._uniform / derive_seed (mcubes.py:51-60) -------------- */
 pcb_status pcb_uniforms(pcb_ctx* ctx, uint64_t seed, int32_t rng_kind, int64_t n, const uint64_t* streams,

@@ -67,6 +67,8 @@ def genz_eval(family: str, d: int, points: np.ndarray, bounds=None) -> np.ndarra
     if bounds is not None:
         low, width, jac = bounds
         return genz_eval(family, d, low + width * pts) * jac
+    if callable(family):  # a vectorised user function, FunctionIntegrand(vectorized=True) (core.py:72-93)
+        return np.asarray(family(pts), dtype=np.float64)
     idx = np.arange(1, d + 1, dtype=float)
     if family == "f1":
         return np.cos(pts @ idx)

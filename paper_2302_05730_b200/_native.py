@@ -176,6 +176,8 @@ SIGNATURES = {
     "pcb_grid_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
     "pcb_debug_divide": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p]),
+    "pcb_user_family_load": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64, C.c_void_p]),
+    "pcb_user_family_unload": (C.c_int, [C.c_void_p, C.c_int32]),
     "pcb_uniforms": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 

@@ -36,16 +36,66 @@ static const kernel_getter kQmc[PCB_N_FAMILIES] = {qmc_kernel_fam0, qmc_kernel_f
 typedef const void* (*lanes_getter)(int d, size_t* smem, int* threads);
 static const lanes_getter kLanes[PCB_N_FAMILIES] = {lanes_kernel_fam0, lanes_kernel_fam1, lanes_kernel_fam2, lanes_kernel_fam3,
                                                     lanes_kernel_fam4, lanes_kernel_fam5, lanes_kernel_fam6, lanes_kernel_fam7};
-const void* eval_lanes_kernel(int family, int d, size_t* smem, int* threads) { return kLanes[family](d, smem, threads); }
-const void* eval_kernel(int family, int d) { return kEval[family](d); }
-const void* eval_wide_kernel(int family, int d) { return kEvalWide[family](d); }
-const void* points_kernel(int family, int d) { return kPoints[family](d); }
-const void* vsample_kernel_ptr(int family, int d, int rng) { return kSample[family](d, rng); }
+// run-time families (pcb_user_family_load): kernels fetched from a loaded cubin, bound to one dimension
+struct UserFamily {
+  int d = 0;
+  cudaLibrary_t lib = nullptr;
+  const void* fn[8] = {};   // order of pcb_user_kernel_names
+};
+static UserFamily g_user[PCB_MAX_USER_FAMILIES];
+static const UserFamily* user_family(int family, int d) {
+  const int slot = family - PCB_USER_FAMILY_BASE;
+  if (slot < 0 || slot >= PCB_MAX_USER_FAMILIES || !g_user[slot].lib || g_user[slot].d != d) return nullptr;
+  return &g_user[slot];
+}
+size_t generic_lanes_smem(int d);   // pagani_inst.cu: GenericLaneLayout<d>::smem_bytes()
+
+const void* eval_lanes_kernel(int family, int d, size_t* smem, int* threads) {
+  if (family >= PCB_N_FAMILIES) {
+    const UserFamily* u = user_family(family, d);
+    *smem = u ? generic_lanes_smem(d) : 0;
+    *threads = 32;
+    return u ? u->fn[2] : nullptr;
+  }
+  return kLanes[family](d, smem, threads);
+}
+const void* eval_kernel(int family, int d) {
+  if (family >= PCB_N_FAMILIES) { const UserFamily* u = user_family(family, d); return u ? u->fn[0] : nullptr; }
+  return kEval[family](d);
+}
+const void* eval_wide_kernel(int family, int d) {
+  if (family >= PCB_N_FAMILIES) { const UserFamily* u = user_family(family, d); return u ? u->fn[1] : nullptr; }
+  return kEvalWide[family](d);
+}
+const void* points_kernel(int family, int d) {
+  if (family >= PCB_N_FAMILIES) { const UserFamily* u = user_family(family, d); return u ? u->fn[3] : nullptr; }
+  return kPoints[family](d);
+}
+const void* vsample_kernel_ptr(int family, int d, int rng) {
+  if (family >= PCB_N_FAMILIES) {
+    const UserFamily* u = user_family(family, d);
+    return u ? u->fn[rng == PCB_RNG_REFERENCE_HASH ? 6 : 7] : nullptr;
+  }
+  return kSample[family](d, rng);
+}
+static const void* invoke_kernel_ptr(int family, int d) {
+  if (family >= PCB_N_FAMILIES) { const UserFamily* u = user_family(family, d); return u ? u->fn[4] : nullptr; }
+  return kInvoke[family](d);
+}
+static const void* qmc_kernel_ptr(int family, int d) {
+  if (family >= PCB_N_FAMILIES) { const UserFamily* u = user_family(family, d); return u ? u->fn[5] : nullptr; }
+  return kQmc[family](d);
+}
 
 pcb_status validate_integrand(pcb_ctx* ctx, const pcb_integrand* f) {
   if (!f) return fail(ctx, PCB_INVALID, "integrand is NULL");
-  if (f->family < 0 || f->family >= PCB_N_FAMILIES) return fail(ctx, PCB_INVALID, "unknown integrand family %d", f->family);
   if (f->d < 1 || f->d > PCB_MAX_DIM) return fail(ctx, PCB_INVALID, "dimension %d outside [1, %d]", f->d, PCB_MAX_DIM);
+  if (f->family >= PCB_USER_FAMILY_BASE && f->family < PCB_USER_FAMILY_BASE + PCB_MAX_USER_FAMILIES) {
+    if (!user_family(f->family, f->d))
+      return fail(ctx, PCB_INVALID, "run-time family %d is not loaded for dimension %d (pcb_user_family_load)", f->family, f->d);
+    return PCB_OK;
+  }
+  if (f->family < 0 || f->family >= PCB_N_FAMILIES) return fail(ctx, PCB_INVALID, "unknown integrand family %d", f->family);
   return PCB_OK;
 }
 
@@ -71,6 +121,45 @@ __global__ void uniforms_kernel(unsigned long long seed, int kind, long long n, 
 using namespace pcb;
 
 extern "C" {
+
+pcb_status pcb_user_family_load(pcb_ctx* ctx, int32_t family, int32_t d, const void* cubin, uint64_t bytes,
+                                const pcb_user_kernel_names* names) {
+  const int slot = family - PCB_USER_FAMILY_BASE;
+  if (slot < 0 || slot >= PCB_MAX_USER_FAMILIES)
+    return fail(ctx, PCB_INVALID, "run-time family id %d outside [%d, %d)", family, PCB_USER_FAMILY_BASE, PCB_USER_FAMILY_BASE + PCB_MAX_USER_FAMILIES);
+  if (d < 1 || d > PCB_MAX_DIM || !cubin || bytes == 0 || !names) return fail(ctx, PCB_INVALID, "user_family_load: bad arguments");
+  if (ctx) PCB_CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cudaLibrary_t lib = nullptr;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin, nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) return fail(ctx, PCB_CUDA, "user_family_load: the image does not load (%s)", cudaGetErrorString(e));
+  const char* wanted[8] = {names->eval, names->eval_wide, names->lanes, names->points,
+                           names->invoke, names->qmc, names->sample_hash, names->sample_generic};
+  UserFamily u;
+  u.d = d;
+  u.lib = lib;
+  for (int k = 0; k < 8; ++k) {
+    cudaKernel_t kern = nullptr;
+    e = wanted[k] ? cudaLibraryGetKernel(&kern, lib, wanted[k]) : cudaErrorInvalidValue;
+    if (e != cudaSuccess) {
+      cudaLibraryUnload(lib);
+      (void)cudaGetLastError();
+      return fail(ctx, PCB_INVALID, "user_family_load: kernel %s not found in the image (%s)", wanted[k] ? wanted[k] : "(null)", cudaGetErrorString(e));
+    }
+    u.fn[k] = (const void*)kern;
+  }
+  if (g_user[slot].lib) cudaLibraryUnload(g_user[slot].lib);
+  g_user[slot] = u;
+  return PCB_OK;
+}
+
+pcb_status pcb_user_family_unload(pcb_ctx* ctx, int32_t family) {
+  const int slot = family - PCB_USER_FAMILY_BASE;
+  if (slot < 0 || slot >= PCB_MAX_USER_FAMILIES) return fail(ctx, PCB_INVALID, "run-time family id %d out of range", family);
+  if (g_user[slot].lib) cudaLibraryUnload(g_user[slot].lib);
+  g_user[slot] = UserFamily{};
+  return PCB_OK;
+}
+
 
 pcb_status pcb_ctx_create(int device_ordinal, pcb_ctx** out) {
   if (!out) return PCB_INVALID;
@@ -260,7 +349,7 @@ pcb_status pcb_bench_invoke(pcb_ctx* ctx, const pcb_integrand* f, int64_t n, con
   pcb_status st = PCB_OK;
   for (int r = 0; r < repetitions && st == PCB_OK; ++r) {
     cudaEventRecord(e0, ctx->stream);
-    cudaError_t err = cudaLaunchKernel(kInvoke[f->family](f->d), dim3(blocks), dim3(threads), args, 0, ctx->stream);
+    cudaError_t err = cudaLaunchKernel(invoke_kernel_ptr(f->family, f->d), dim3(blocks), dim3(threads), args, 0, ctx->stream);
     cudaEventRecord(e1, ctx->stream);
     ctx->launches++;
     if (err == cudaSuccess) err = cudaEventSynchronize(e1);
@@ -331,7 +420,7 @@ pcb_status pcb_qmc_shift_sums(pcb_ctx* ctx, const pcb_integrand* f, int32_t log2
   const unsigned* dirs_c = dirs_dev;
   const double* shifts_c = shifts_dev;
   void* args[] = {&fv, &lg, &dirs_c, &shifts_c, &partial};
-  PCB_CUDA_TRY(ctx, cudaLaunchKernel(kQmc[f->family](d), dim3(blocks, (unsigned)n_shifts), dim3(256), args, 0, ctx->stream));
+  PCB_CUDA_TRY(ctx, cudaLaunchKernel(qmc_kernel_ptr(f->family, d), dim3(blocks, (unsigned)n_shifts), dim3(256), args, 0, ctx->stream));
   ctx->launches++;
   for (int s = 0; s < n_shifts; ++s) PCB_TRY(tree_sum_dev(ctx, partial + (size_t)s * blocks, blocks, sums_dev + s));
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync(sums, sums_dev, (size_t)n_shifts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -64,6 +64,18 @@ const void* PCB_CAT(lanes_kernel_fam, PCB_FAM)(int d, size_t* smem, int* threads
   return nullptr;
 }
 
+#if PCB_FAM == 0
+// dynamic shared memory of the generic lane kernel for a run-time dimension (run-time families, ctx.cu)
+size_t generic_lanes_smem(int d) {
+  switch (d) {
+#define X(D) case D: return GenericLaneLayout<D>::smem_bytes();
+    PCB_DIMS(X)
+#undef X
+  }
+  return 0;
+}
+#endif
+
 const void* PCB_CAT(points_kernel_fam, PCB_FAM)(int d) {
   switch (d) {
 #define X(D) case D: return (const void*)&eval_points_kernel<PCB_FAM, D>;

@@ -185,3 +185,16 @@ def test_bench_refuses_to_claim_gpus_it_does_not_have():
     proc = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"], capture_output=True,
                           text=True, timeout=300, env=env)
     assert proc.returncode != 0 and "refusing to report n_gpus=4" in proc.stderr
+
+
+def test_run_time_family_image_builds_and_carries_every_kernel():
+    """userfn.build_image cross-compiles here (no GPU needed): the cubin must hold the eight kernels whose mangled
+    names userfn._kernel_names predicts, and a source error must surface as ValueError with the compiler's log."""
+    from paper_2302_05730_b200 import userfn
+
+    image = userfn.build_image(9, 4, "double u = x - 0.3; return u * u;", "return exp(-param[0] * acc);", "numpy_sum")
+    for key, name in userfn._kernel_names(9, 4).items():
+        assert name.encode() in image, key
+    with pytest.raises(ValueError, match="does not compile"):
+        userfn.build_image(9, 4, "return no_such_symbol;", "return acc;", "sum")
+    assert userfn.USER_FAMILY_BASE == 8 and userfn.MAX_USER_FAMILIES == 8      # include/parcube_b200.h
