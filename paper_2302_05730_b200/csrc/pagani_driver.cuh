@@ -27,7 +27,32 @@ constexpr int kTreeSpan = kTreeBlock * 4;       // elements per CTA: one aligned
 // each odd level is the same as zero-padding the input to a power of two.
 __global__ void __launch_bounds__(kTreeBlock) tree_level_kernel(const double* __restrict__ in, long long n,
                                                                 double* __restrict__ out) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   __shared__ double s[kTreeBlock / 32];
+  const long long base = (long long)blockIdx.x * kTreeSpan + 4LL * threadIdx.x;
+  double a0 = base + 0 < n ? in[base + 0] : 0.0;
+  double a1 = base + 1 < n ? in[base + 1] : 0.0;
+  double a2 = base + 2 < n ? in[base + 2] : 0.0;
+  double a3 = base + 3 < n ? in[base + 3] : 0.0;
+  double v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) v = v + __shfl_xor_sync(PCB_FULL_MASK, v, m);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    out[blockIdx.x] = t;
+  }
+}
+
+// The same level for TWO arrays of equal length in one launch (blockIdx.y selects the array): the refinement always
+// sums integrals and errors together, and a launch boundary costs more than a level of a short list.
+__global__ void __launch_bounds__(kTreeBlock) tree_level2_kernel(const double* __restrict__ in0, const double* __restrict__ in1,
+                                                                 long long n, double* __restrict__ out0, double* __restrict__ out1) {
+  pdl_wait();
+  __shared__ double s[kTreeBlock / 32];
+  const double* __restrict__ in = blockIdx.y ? in1 : in0;
+  double* __restrict__ out = blockIdx.y ? out1 : out0;
   const long long base = (long long)blockIdx.x * kTreeSpan + 4LL * threadIdx.x;
   double a0 = base + 0 < n ? in[base + 0] : 0.0;
   double a1 = base + 1 < n ? in[base + 1] : 0.0;
@@ -46,6 +71,7 @@ __global__ void __launch_bounds__(kTreeBlock) tree_level_kernel(const double* __
 
 // max over a double array (only needed for the "force progress" fallback, pagani.py:364-365)
 __global__ void max_kernel(const double* __restrict__ in, long long n, double* __restrict__ out) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   __shared__ double s[32];
   double v = -1.0;  // error estimates are non-negative
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
@@ -81,6 +107,7 @@ struct ClassifyArgs {
 
 // split_mask and per-CTA counts
 __global__ void __launch_bounds__(kScanBlock) classify_kernel(const __grid_constant__ ClassifyArgs a) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   __shared__ unsigned int s_cnt[32];
   const long long r = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   bool split = false;
@@ -110,6 +137,7 @@ __global__ void __launch_bounds__(kScanBlock) classify_kernel(const __grid_const
 __global__ void __launch_bounds__(1024) scan_counts_kernel(const unsigned int* __restrict__ counts, int nb,
                                                            unsigned long long* __restrict__ offsets,
                                                            unsigned long long* __restrict__ total) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   __shared__ unsigned long long s_warp[32];
   __shared__ unsigned long long s_carry;
   if (threadIdx.x == 0) s_carry = 0;
@@ -157,13 +185,29 @@ struct SplitArgs {
   double* out_lengths;
   double* retired_i;     // compacted estimates of the regions that are not split, parent order
   double* retired_e;
+  unsigned long long* rearm_bad = nullptr;   // non-finite flag of the evaluation that follows (set to ~0 here), or NULL
 };
+
+// Hand `count` scalar slots to the host through pinned memory: values first, then the sequence word the host polls.
+// Replaces a device->host copy plus a stream synchronisation per read (two per iteration of the general refine path).
+__global__ void publish_scalars_kernel(const unsigned long long* __restrict__ scalars, int first, int count,
+                                       volatile unsigned long long* pinned, volatile unsigned long long* seq_word, unsigned long long seq) {
+  pdl_wait();
+  if (threadIdx.x < count) pinned[first + threadIdx.x] = scalars[first + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *seq_word = seq;
+  }
+}
 
 // stable compaction + bisection (pagani.py:282-297, 371-377)
 __global__ void __launch_bounds__(kScanBlock) split_kernel(const __grid_constant__ SplitArgs a) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   __shared__ unsigned int s_warp[32];
   const long long r = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (a.rearm_bad && r == 0) *a.rearm_bad = ~0ULL;   // the host has read the previous evaluation's flag before it launched this kernel
   const bool split = r < a.n && a.flags[r];
   const unsigned int ballot = __ballot_sync(PCB_FULL_MASK, split);
   if (lane == 0) s_warp[w] = __popc(ballot);
@@ -203,6 +247,7 @@ __global__ void __launch_bounds__(kScanBlock) split_kernel(const __grid_constant
 
 // lexicographic uniform tiling, axis 0 slowest: left = idx * (1/g), length = 1/g (core.py:265-268)
 __global__ void tiling_kernel(int d, int g, long long first, long long n, long long ld, double h, double* lefts, double* lengths) {
+  pdl_wait();   // may be launched with programmatic serialisation behind its producer (a no-op otherwise)
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
     long long rem = first + r;  // global tile index
     for (int j = d - 1; j >= 0; --j) {

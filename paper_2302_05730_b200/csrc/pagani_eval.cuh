@@ -215,6 +215,7 @@ struct CornerCombine {
 // the G partials (zero leaves beyond the last virtual thread that owns a point: x + 0.0 == x).
 template <int FAM, int D, bool WIDE = false>
 __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_kernel(const __grid_constant__ EvalArgs args) {
+  pdl_wait();   // region list and flags come from the kernels before it in the stream (programmatic serialisation)
   using F = Family<FAM>;
   constexpr int kStore = 4 * D + 1;            // f(centre), f(+-l2 e_j), f(+-l3 e_j): split-axis inputs
   constexpr int kCorner0 = 2 * D * D + 2 * D + 1;  // first corner point

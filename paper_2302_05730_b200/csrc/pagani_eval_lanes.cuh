@@ -128,6 +128,7 @@ constexpr int lanes_min_blocks() {
 template <int FAM, int D>
 __global__ void __launch_bounds__((PCB_LANES_HALVES_REAL > 1 || MultFamily<FAM>::cplx) ? 64 : 32, lanes_min_blocks<FAM, D>())
 pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
+  pdl_wait();   // region list and flags come from the kernels before it in the stream (programmatic serialisation)
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;
@@ -636,6 +637,7 @@ __host__ __device__ constexpr int generic_lane_chains() {
 }
 template <int FAM, int D>
 __global__ void __launch_bounds__(32, generic_lane_chains<FAM, D>() == 8 ? 1 : PCB_LANES_GENERIC_MINB) pagani_eval_lanes_generic_kernel(const __grid_constant__ EvalArgs args) {
+  pdl_wait();   // region list and flags come from the kernels before it in the stream (programmatic serialisation)
   using F = Family<FAM>;
   using L = GenericLaneLayout<D>;
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -109,6 +109,7 @@ struct MultLayout {
 
 template <int FAM, int D>
 __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const __grid_constant__ EvalArgs args) {
+  pdl_wait();   // region list and flags come from the kernels before it in the stream (programmatic serialisation)
   using F = Family<FAM>;
   using MF = MultFamily<FAM>;
   using V = MVal<MF::cplx>;

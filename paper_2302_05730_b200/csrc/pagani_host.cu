@@ -12,11 +12,15 @@
 
 namespace pcb {
 
+// Every kernel of this file waits for its producers at pdl_wait(), so all of them are launched with programmatic
+// stream serialisation: back-to-back kernels of an iteration (evaluate -> tree levels -> classify -> scan, split ->
+// tree levels -> evaluate) overlap launch latency with the tail of their predecessor (0.8 us per boundary instead
+// of 2.5-3.5 us; ~15 boundaries per iteration of the general path).
 template <class... Args>
 static cudaError_t launch(pcb_ctx* ctx, const void* fn, dim3 grid, dim3 block, size_t smem, Args... a) {
   void* args[] = {(void*)&a...};
   ctx->launches++;
-  return cudaLaunchKernel(fn, grid, block, args, smem, ctx->stream);
+  return launch_pdl(fn, grid, block, args, smem, ctx->stream);
 }
 
 static pcb_status validate_rule(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg) {
@@ -101,9 +105,9 @@ static pcb_status preload_refine_kernels(pcb_ctx* ctx, const pcb_integrand* f, c
   int lanes_threads = 32;
   const void* lanes_fn = cfg->group_size == 64 ? eval_lanes_kernel(f->family, f->d, &lanes_smem, &lanes_threads) : nullptr;
   const void* fns[] = {cfg->group_size > 64 ? eval_wide_kernel(f->family, f->d) : eval_kernel(f->family, f->d), lanes_fn,
-                       (const void*)&tiling_kernel, (const void*)&tree_level_kernel, (const void*)&short_iteration_kernel,
+                       (const void*)&tiling_kernel, (const void*)&tree_level_kernel, (const void*)&tree_level2_kernel, (const void*)&short_iteration_kernel,
                        (const void*)&classify_kernel, (const void*)&scan_counts_kernel, (const void*)&max_kernel,
-                       (const void*)&split_kernel};
+                       (const void*)&split_kernel, (const void*)&publish_scalars_kernel};
   for (const void* fn : fns) {
     if (!fn || !ctx->preloaded.insert(fn).second) continue;
     cudaFuncAttributes attr;
@@ -119,6 +123,31 @@ static pcb_status preload_refine_kernels(pcb_ctx* ctx, const pcb_integrand* f, c
   return PCB_OK;
 }
 
+// engine.tree_sum of two arrays of the same length, level by level in shared launches (same bits as two tree_sum_dev)
+static pcb_status tree_sum2_dev(pcb_ctx* ctx, const double* in0, const double* in1, long long n, double* out0, double* out1) {
+  if (n <= 0) {
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(out0, 0, sizeof(double), ctx->stream));
+    PCB_CUDA_TRY(ctx, cudaMemsetAsync(out1, 0, sizeof(double), ctx->stream));
+    return PCB_OK;
+  }
+  int which = 0;
+  while (true) {
+    const long long nb = (n + kTreeSpan - 1) / kTreeSpan;
+    double *dst0 = out0, *dst1 = out1;
+    if (nb > 1) {   // the two arrays' block sums share one ping-pong buffer, second half for the second array
+      PCB_CUDA_TRY(ctx, ctx->tree[which].ensure((size_t)2 * nb * sizeof(double)));
+      dst0 = ctx->tree[which].as<double>();
+      dst1 = dst0 + nb;
+    }
+    PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&tree_level2_kernel, dim3((unsigned)nb, 2), dim3(kTreeBlock), 0, in0, in1, n, dst0, dst1));
+    if (nb == 1) return PCB_OK;
+    in0 = dst0;
+    in1 = dst1;
+    n = nb;
+    which ^= 1;
+  }
+}
+
 pcb_status tree_sum_dev(pcb_ctx* ctx, const double* in, long long n, double* out) {
   if (n <= 0) {
     PCB_CUDA_TRY(ctx, cudaMemsetAsync(out, 0, sizeof(double), ctx->stream));
@@ -132,9 +161,7 @@ pcb_status tree_sum_dev(pcb_ctx* ctx, const double* in, long long n, double* out
       PCB_CUDA_TRY(ctx, ctx->tree[which].ensure((size_t)nb * sizeof(double)));
       dst = ctx->tree[which].as<double>();
     }
-    tree_level_kernel<<<(unsigned)nb, kTreeBlock, 0, ctx->stream>>>(in, n, dst);
-    ctx->launches++;
-    PCB_CUDA_TRY(ctx, cudaGetLastError());
+    PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&tree_level_kernel, dim3((unsigned)nb), dim3(kTreeBlock), 0, in, n, dst));
     if (nb == 1) return PCB_OK;
     in = dst;
     n = nb;
@@ -195,6 +222,32 @@ static pcb_status read_scalars(pcb_ctx* ctx, int first, int count) {
   PCB_CUDA_TRY(ctx, cudaMemcpyAsync((double*)ctx->pinned + first, ctx->scalars.as<double>() + first, count * sizeof(double),
                                     cudaMemcpyDeviceToHost, ctx->stream));
   PCB_CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return PCB_OK;
+}
+
+// The same read for the refinement loop: a one-warp kernel writes the slots and then a sequence word into pinned
+// memory and the host polls the word -- no copy engine, no stream synchronisation (measured on lists of 5e4..3e6
+// regions: see DESIGN 4.2).  The stream is queried now and then so that a failed launch surfaces instead of hanging.
+static pcb_status publish_scalars(pcb_ctx* ctx, int first, int count) {
+  if (!ctx->pg_record) {
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 256));
+    std::memset(ctx->pg_record, 0, 256);
+  }
+  volatile unsigned long long* seq_word = reinterpret_cast<volatile unsigned long long*>(static_cast<char*>(ctx->pg_record) + 128);
+  const unsigned long long seq = ++ctx->pg_seq;
+  PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&publish_scalars_kernel, dim3(1), dim3(32), 0,
+                           (const unsigned long long*)ctx->scalars.as<unsigned long long>(), first, count,
+                           (volatile unsigned long long*)ctx->pinned, seq_word, seq));
+  for (unsigned spin = 0; *seq_word != seq; ++spin) {
+    if ((spin & 0xfff) == 0xfff) {
+      cudaError_t e = cudaStreamQuery(ctx->stream);
+      if (e != cudaErrorNotReady && *seq_word != seq) {
+        (void)cudaGetLastError();
+        return fail(ctx, PCB_CUDA, "pagani_refine: the device did not publish its scalars (%s)", cudaGetErrorString(e));
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   return PCB_OK;
 }
 
@@ -303,6 +356,9 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   n = (long long)exact;
 
   PCB_TRY(preload_refine_kernels(ctx, f, cfg));
+  // scalars travel through pinned memory (publish_scalars); PCB_PAGANI_PUBLISH=0: copy + synchronise (A/B runs)
+  static const bool use_publish = [] { const char* e = std::getenv("PCB_PAGANI_PUBLISH"); return !(e && std::atoi(e) == 0); }();
+  auto fetch = use_publish ? publish_scalars : read_scalars;
   cudaEvent_t ev0, ev1;
   PCB_CUDA_TRY(ctx, cudaEventCreate(&ev0));
   PCB_CUDA_TRY(ctx, cudaEventCreate(&ev1));
@@ -316,9 +372,8 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   long long ld = round_up(n, 32);
   PCB_CUDA_TRY(ctx, ctx->lefts[cur].ensure((size_t)ld * d * sizeof(double)));
   PCB_CUDA_TRY(ctx, ctx->lengths[cur].ensure((size_t)ld * d * sizeof(double)));
-  tiling_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, ctx->stream>>>(
-      d, (int)g, 0LL, n, ld, 1.0 / (double)g, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>());
-  ctx->launches++;
+  PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&tiling_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, 4096)), dim3(256), 0,
+                           d, (int)g, 0LL, n, ld, 1.0 / (double)g, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>()));
 
   double* sc = ctx->scalars.as<double>();
   unsigned long long* sc_u = ctx->scalars.as<unsigned long long>();
@@ -345,16 +400,16 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   // short lists (<= 1024 regions) run the whole iteration in one CTA and hand one record back through pinned memory
   bool use_short = true;
   if (const char* env = std::getenv("PCB_PAGANI_SHORT")) use_short = std::atoi(env) != 0;
-  if (use_short && !ctx->pg_record) {
-    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 128));
-    std::memset(ctx->pg_record, 0, 128);
+  if (!ctx->pg_record) {   // bytes [0, 128): the short-iteration record, [128, 256): the sequence word of publish_scalars
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 256));
+    std::memset(ctx->pg_record, 0, 256);
   }
   ShortIterRecord* srec = static_cast<ShortIterRecord*>(ctx->pg_record);
 
   for (int it = 0; it <= cfg->max_iterations; ++it) {
     if (use_short && n >= 1 && n <= 1024) {
       if (have_retired) {  // fold the general path's pending retirements first
-        PCB_TRY(read_scalars(ctx, 0, 8));
+        PCB_TRY(fetch(ctx, 0, 8));
         fin_i += host[S_RET_I];
         fin_e += host[S_RET_E];
         have_retired = false;
@@ -431,9 +486,8 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       PCB_TRY(evaluate(n, ld, false));
       continue;
     }
-    PCB_TRY(tree_sum_dev(ctx, ctx->est_i.as<double>(), n, sc + S_SUM_I));
-    PCB_TRY(tree_sum_dev(ctx, ctx->est_e.as<double>(), n, sc + S_SUM_E));
-    PCB_TRY(read_scalars(ctx, 0, 8));
+    PCB_TRY(tree_sum2_dev(ctx, ctx->est_i.as<double>(), ctx->est_e.as<double>(), n, sc + S_SUM_I, sc + S_SUM_E));
+    PCB_TRY(fetch(ctx, 0, 8));
     if (host_u[S_BAD] != ~0ULL)
       return fetch_nonfinite_pagani(ctx, f, rule, ld, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(), host_u[S_BAD], bad);
     if (have_retired) {  // fin += tree_sum(act[~mask]) of the previous iteration (pagani.py:371-372)
@@ -483,18 +537,17 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     ca.block_counts = ctx->counts.as<unsigned int>();
     long long n_split = 0;
     for (int pass = 0; pass < 2; ++pass) {
-      classify_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(ca);
-      scan_counts_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->counts.as<unsigned int>(), (int)nblk,
-                                                      ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT);
-      ctx->launches += 2;
-      PCB_TRY(read_scalars(ctx, S_NSPLIT, 1));
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&classify_kernel, dim3((unsigned)nblk), dim3(kScanBlock), 0, ca));
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&scan_counts_kernel, dim3(1), dim3(1024), 0, (const unsigned int*)ctx->counts.as<unsigned int>(),
+                               (int)nblk, ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT));
+      PCB_TRY(fetch(ctx, S_NSPLIT, 1));
       n_split = (long long)host_u[S_NSPLIT];
       if (n_split > 0 || pass == 1) break;
       // nothing exceeds its budget: force progress on the worst regions, ties included (pagani.py:364-365)
       PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc + S_EMAX, 0, sizeof(double), ctx->stream));
-      max_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 1024), 256, 0, ctx->stream>>>(ctx->est_e.as<double>(), n, sc + S_EMAX);
-      ctx->launches++;
-      PCB_TRY(read_scalars(ctx, S_EMAX, 1));
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&max_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, 1024)), dim3(256), 0,
+                               (const double*)ctx->est_e.as<double>(), n, sc + S_EMAX));
+      PCB_TRY(fetch(ctx, S_EMAX, 1));
       ca.mode = 1;
       ca.emax = host[S_EMAX];
     }
@@ -520,18 +573,16 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     sa.out_lengths = ctx->lengths[nxt].as<double>();
     sa.retired_i = ctx->ret_i.as<double>();
     sa.retired_e = ctx->ret_e.as<double>();
-    split_kernel<<<(unsigned)nblk, kScanBlock, 0, ctx->stream>>>(sa);
-    ctx->launches++;
-    PCB_CUDA_TRY(ctx, cudaGetLastError());
-    PCB_TRY(tree_sum_dev(ctx, ctx->ret_i.as<double>(), n_ret, sc + S_RET_I));
-    PCB_TRY(tree_sum_dev(ctx, ctx->ret_e.as<double>(), n_ret, sc + S_RET_E));
+    sa.rearm_bad = sc_u + S_BAD;   // instead of a memset between the kernels (it would end their programmatic overlap)
+    PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&split_kernel, dim3((unsigned)nblk), dim3(kScanBlock), 0, sa));
+    PCB_TRY(tree_sum2_dev(ctx, ctx->ret_i.as<double>(), ctx->ret_e.as<double>(), n_ret, sc + S_RET_I, sc + S_RET_E));
     have_retired = true;  // read back together with the next iteration's sums
     fin_count += n_ret;
     processed += n_child;
     n = n_child;
     ld = ld_out;
     cur = nxt;
-    PCB_TRY(evaluate(n, ld));
+    PCB_TRY(evaluate(n, ld, false));
   }
 
   cudaEventRecord(ev1, ctx->stream);
