@@ -103,6 +103,12 @@ struct ClassifyArgs {
   const double* errors;
   unsigned char* flags;
   unsigned int* block_counts;  // per 1024-region CTA
+  // Budget taken on the device (mode 0, `scalars` != NULL): the host's own expressions on the scalars it is about to
+  // read -- fin = fin_i [+ scalars[slot_ret_i]], estimate = fin + scalars[slot_sum_i] -- so that the classification can
+  // be enqueued BEFORE the host has seen the sums and one round trip per iteration carries sums and split count.
+  const double* scalars = nullptr;
+  double fin_i = 0.0, rel_tol = 0.0, abs_tol = 0.0;
+  int have_retired = 0, slot_sum_i = 0, slot_ret_i = 0;
 };
 
 // split_mask and per-CTA counts
@@ -111,12 +117,18 @@ __global__ void __launch_bounds__(kScanBlock) classify_kernel(const __grid_const
   __shared__ unsigned int s_cnt[32];
   const long long r = (long long)blockIdx.x * kScanBlock + threadIdx.x;
   bool split = false;
+  double budget = a.budget;
+  if (a.scalars) {
+    double fin = a.fin_i;
+    if (a.have_retired) fin = fin + a.scalars[a.slot_ret_i];
+    budget = split_budget(a.rel_tol, a.abs_tol, fin + a.scalars[a.slot_sum_i]);
+  }
   if (r < a.n) {
     const double e = a.errors[r];
     if (a.mode == 0) {
       double vol = a.lengths[r];
       for (int j = 1; j < a.d; ++j) vol = vol * a.lengths[j * a.ld + r];  // np.prod, left to right
-      split = e > a.budget * vol;
+      split = e > budget * vol;
     } else {
       split = e >= a.emax;
     }

@@ -487,6 +487,27 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       continue;
     }
     PCB_TRY(tree_sum2_dev(ctx, ctx->est_i.as<double>(), ctx->est_e.as<double>(), n, sc + S_SUM_I, sc + S_SUM_E));
+    // classification (pagani.py:361-365), enqueued before the host has seen the sums: the kernel takes its budget from
+    // the same scalars with the host's own expressions, so one round trip returns sums AND split count (the
+    // classification of the last iteration is the only work that is ever wasted)
+    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
+    ClassifyArgs ca;
+    const bool speculate = it < cfg->max_iterations && n > 0;
+    if (speculate) {
+      PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)n));
+      PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));
+      PCB_CUDA_TRY(ctx, ctx->offsets.ensure((size_t)nblk * sizeof(unsigned long long)));
+      ca.n = n; ca.ld = ld; ca.d = d; ca.mode = 0; ca.budget = 0.0; ca.emax = 0.0;
+      ca.lengths = ctx->lengths[cur].as<double>();
+      ca.errors = ctx->est_e.as<double>();
+      ca.flags = ctx->flags.as<unsigned char>();
+      ca.block_counts = ctx->counts.as<unsigned int>();
+      ca.scalars = sc; ca.fin_i = fin_i; ca.rel_tol = cfg->rel_tol; ca.abs_tol = cfg->abs_tol;
+      ca.have_retired = have_retired ? 1 : 0; ca.slot_sum_i = S_SUM_I; ca.slot_ret_i = S_RET_I;
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&classify_kernel, dim3((unsigned)nblk), dim3(kScanBlock), 0, ca));
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&scan_counts_kernel, dim3(1), dim3(1024), 0, (const unsigned int*)ctx->counts.as<unsigned int>(),
+                               (int)nblk, ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT));
+    }
     PCB_TRY(fetch(ctx, 0, 8));
     if (host_u[S_BAD] != ~0ULL)
       return fetch_nonfinite_pagani(ctx, f, rule, ld, ctx->lefts[cur].as<double>(), ctx->lengths[cur].as<double>(), host_u[S_BAD], bad);
@@ -523,26 +544,8 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
     if (it == cfg->max_iterations) { reason = PCB_STOP_MAX_ITER; break; }
     if (n == 0) { reason = PCB_STOP_NO_ACTIVE; break; }
 
-    // classification (pagani.py:361-365)
-    const double budget = split_budget(cfg->rel_tol, cfg->abs_tol, estimate);
-    const long long nblk = (n + kScanBlock - 1) / kScanBlock;
-    PCB_CUDA_TRY(ctx, ctx->flags.ensure((size_t)n));
-    PCB_CUDA_TRY(ctx, ctx->counts.ensure((size_t)nblk * sizeof(unsigned int)));
-    PCB_CUDA_TRY(ctx, ctx->offsets.ensure((size_t)nblk * sizeof(unsigned long long)));
-    ClassifyArgs ca;
-    ca.n = n; ca.ld = ld; ca.d = d; ca.mode = 0; ca.budget = budget; ca.emax = 0.0;
-    ca.lengths = ctx->lengths[cur].as<double>();
-    ca.errors = ctx->est_e.as<double>();
-    ca.flags = ctx->flags.as<unsigned char>();
-    ca.block_counts = ctx->counts.as<unsigned int>();
-    long long n_split = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&classify_kernel, dim3((unsigned)nblk), dim3(kScanBlock), 0, ca));
-      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&scan_counts_kernel, dim3(1), dim3(1024), 0, (const unsigned int*)ctx->counts.as<unsigned int>(),
-                               (int)nblk, ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT));
-      PCB_TRY(fetch(ctx, S_NSPLIT, 1));
-      n_split = (long long)host_u[S_NSPLIT];
-      if (n_split > 0 || pass == 1) break;
+    long long n_split = (long long)host_u[S_NSPLIT];
+    if (n_split == 0) {
       // nothing exceeds its budget: force progress on the worst regions, ties included (pagani.py:364-365)
       PCB_CUDA_TRY(ctx, cudaMemsetAsync(sc + S_EMAX, 0, sizeof(double), ctx->stream));
       PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&max_kernel, dim3((unsigned)std::min<long long>((n + 255) / 256, 1024)), dim3(256), 0,
@@ -550,6 +553,12 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       PCB_TRY(fetch(ctx, S_EMAX, 1));
       ca.mode = 1;
       ca.emax = host[S_EMAX];
+      ca.scalars = nullptr;
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&classify_kernel, dim3((unsigned)nblk), dim3(kScanBlock), 0, ca));
+      PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&scan_counts_kernel, dim3(1), dim3(1024), 0, (const unsigned int*)ctx->counts.as<unsigned int>(),
+                               (int)nblk, ctx->offsets.as<unsigned long long>(), sc_u + S_NSPLIT));
+      PCB_TRY(fetch(ctx, S_NSPLIT, 1));
+      n_split = (long long)host_u[S_NSPLIT];
     }
     if (processed + 2 * n_split > cfg->region_cap) { reason = PCB_STOP_REGION_CAP; break; }
 
