@@ -129,8 +129,13 @@ struct DevBuf {
     };
     // geometric growth (a list that doubles per iteration maps ~2 new ranges per step); big steps take the
     // context's pre-created 64-MiB chunks first
+    // A mapping step costs ~0.25 ms whatever its size (cuMemCreate + cuMemMap + cuMemSetAccess, measured), and a
+    // refinement that outgrows ten buffers by a few MiB per iteration paid more for them than for its kernels:
+    // the first step is at least 8 MiB, small buffers double, large ones (>= 256 MiB) grow by half.
     size_t want = bytes - cap;
-    if (want < cap / 2) want = cap / 2;
+    if (cap == 0 && want < ((size_t)8 << 20)) want = (size_t)8 << 20;
+    const size_t geometric = cap < ((size_t)256 << 20) ? cap : cap / 2;
+    if (want < geometric) want = geometric;
     want = (want + gran - 1) / gran * gran;
     while (cache && want >= ChunkCache::kChunk && !cache->free_chunks.empty() && cap < bytes + ChunkCache::kChunk) {
       CUmemGenericAllocationHandle h = cache->free_chunks.back();

@@ -26,14 +26,17 @@ cap vsample_config4 vsample 1 26873856 warp-sample vsample f3 8 1e9
 cap pagani_lanes_f1_d8 pagani_eval 2 390625 region eval f1 8 5
 cap pagani_lanes_f4_d8 pagani_eval 2 390625 region eval f4 8 5
 cap pagani_lanes_f2_d8 pagani_eval 2 390625 region eval f2 8 5
-cap pagani_warp_f3_d8 pagani_eval 2 390625 region eval f3 8 5
+cap pagani_lanes_f3_d8 pagani_eval 2 390625 region eval f3 8 5
 cap pagani_warp_f4_d5_small pagani_eval 2 1024 region eval f4 5 4
 cap pagani_warp_f1_d8_small pagani_eval 2 6561 region eval f1 8 3
 # the final bench lines (own arm with the secondary workloads, reference arm) and the config-5 sweep
 python bench.py > profiles/${R}_bench_config2.json 2> gpurun_out/bench_final.err
 python bench.py --impl reference > profiles/${R}_bench_config2_reference.json 2>> gpurun_out/bench_final.err
 python scripts/sweep.py --out profiles/${R}_sweep_config5 > gpurun_out/sweep.log 2>&1
-for fam in f1 f2 f3 f4 f5 f6; do python scripts/eval_bench.py $fam 8 5; done > profiles/${R}_eval_bench.txt 2>&1
+for fam in f1 f2 f3 f4 f5 f6; do python scripts/eval_bench.py $fam 8 6; done > profiles/${R}_eval_bench.txt 2>&1
+python scripts/refine_bench.py > profiles/${R}_refine_bench.txt 2>&1
+{ echo "# PCB_NO_PDL=1 PCB_PAGANI_PUBLISH=0: plain launches, scalars by copy + synchronise"; PCB_NO_PDL=1 PCB_PAGANI_PUBLISH=0 python scripts/refine_bench.py; } >> profiles/${R}_refine_bench.txt 2>&1
+timeout 120 scripts/micro/atom > profiles/${R}_micro_shared_atomics.txt 2>&1
 python scripts/cold_call.py > profiles/${R}_cold_call.txt 2>&1
 ls -la profiles/
 # device timeline of one config-2 run (%globaltimer stamps per kernel and phase; PCB_TIMELINE=1)
