@@ -226,6 +226,30 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
       }
       vol = (j == 0) ? len : vol * len;   // np.prod, left to right
       V cg[2];
+      if constexpr (MF::unit && PCB_F1_SHARED_TRIG) {
+        // linear phase: centre factor and one rotation per offset (unit_rotation, pagani_eval_mult.cuh); half 0 builds
+        // the pair candidates (rho = the rotation itself), half 1 the corner factors -- two sincos each
+        double x0 = left + len * rule.offsets[0];
+        if (args.f.bounded) x0 = args.f.low[j] + args.f.width[j] * x0;
+        const V e0 = MF::factor(j, x0, args.f);
+        if (kHalves == 1 || half == 0) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            double x = left + len * rule.offsets[c];   // quadrature.py:301-302: mul, then add
+            if (args.f.bounded) x = args.f.low[j] + args.f.width[j] * x;
+            term[(5 * j + c) * 32] = F::term(j, x, args.f);
+          }
+          cen_s[j * 32] = e0;
+          const V r3 = unit_rotation<MF>(j, len, rule.offsets[3], rule.offsets[0], args.f);
+          tab[(L::kP34 + 2 * j) * 32] = r3;
+          tab[(L::kP34 + 2 * j + 1) * 32] = mconj(r3);
+        }
+        if (kHalves == 1 || half == 1) {
+          const V r5 = unit_rotation<MF>(j, len, rule.offsets[5], rule.offsets[0], args.f);
+          cg[0] = mmul(e0, r5);
+          cg[1] = mmul(e0, mconj(r5));
+        }
+      } else {
 #pragma unroll
       for (int c = 0; c < 7; ++c) {
         if (kHalves > 1 && (c >= 5) != (half == 1)) continue;
@@ -237,6 +261,7 @@ pagani_eval_lanes_kernel(const __grid_constant__ EvalArgs args) {
         if (c == 0) cen_s[j * 32] = v;
         else if (c < 5) tab[(L::kP34 + 2 * j + (c - 3)) * 32] = MF::unit ? mmul(mconj(cen_s[j * 32]), v) : v;
         else cg[c - 5] = v;
+      }
       }
       if (kHalves > 1 && half == 0) continue;
       // corner group tables: Grp[g][combo] = phi[3g][.] * phi[3g+1][.] * phi[3g+2][.], left to right

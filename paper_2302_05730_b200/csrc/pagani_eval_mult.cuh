@@ -42,6 +42,10 @@ __device__ __forceinline__ MVal<true> mmul(MVal<true> a, MVal<true> b) {
   return MVal<true>{__fma_rn(a.re, b.re, -(a.im * b.im)), __fma_rn(a.re, b.im, a.im * b.re)};
 }
 // conjugate: the inverse of a unit-modulus factor
+__device__ __forceinline__ MVal<false> mshfl(MVal<false> a, int src) { return MVal<false>{__shfl_sync(PCB_FULL_MASK, a.re, src)}; }
+__device__ __forceinline__ MVal<true> mshfl(MVal<true> a, int src) {
+  return MVal<true>{__shfl_sync(PCB_FULL_MASK, a.re, src), __shfl_sync(PCB_FULL_MASK, a.im, src)};
+}
 __device__ __forceinline__ MVal<false> mconj(MVal<false> a) { return a; }
 __device__ __forceinline__ MVal<true> mconj(MVal<true> a) { return MVal<true>{a.re, -a.im}; }
 __device__ __forceinline__ MVal<false> mone(MVal<false>) { return MVal<false>{1.0}; }
@@ -107,6 +111,23 @@ struct MultLayout {
   static constexpr int kSize = kGrp + 8 * kGroups;
 };
 
+// Unit-modulus families whose phase is LINEAR in x (f1: phi_j(x) = exp(i (j+1) x)) need no transcendental per abscissa:
+// the rule's abscissae are centre +- delta_k, so phi(centre +- delta) = phi(centre) * R(+-delta) with R(-delta) =
+// conj(R(delta)): three sincos per axis and region (centre, the pair offset, the corner offset) instead of five, and the
+// pair candidates' rho = conj(phi(centre)) * phi(centre +- delta) IS R(+-delta) -- no product at all.  The factors move
+// by the rounding of one argument (as they do between any two ways of writing the sum); the lane kernel and the warp
+// kernel build them with the same operations, so they keep agreeing bit for bit.  PCB_F1_SHARED_TRIG=0: one sincos per
+// abscissa (round 1).
+#ifndef PCB_F1_SHARED_TRIG
+#define PCB_F1_SHARED_TRIG 1
+#endif
+template <class MF>
+__device__ __forceinline__ auto unit_rotation(int j, double len, double off_c, double off_0, const pcb_integrand& f) {
+  double dx = len * (off_c - off_0);
+  if (f.bounded) dx = f.width[j] * dx;
+  return MF::factor(j, dx, f);
+}
+
 template <int FAM, int D>
 __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const __grid_constant__ EvalArgs args) {
   pdl_wait();   // region list and flags come from the kernels before it in the stream (programmatic serialisation)
@@ -166,16 +187,34 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const
 #pragma unroll
     for (int e0 = 0; e0 < 8 * D; e0 += 32) {
       const int e = e0 + lane, j = e >> 3, c = e & 7;
-      if (e < 8 * D) {
-        V v = mone(V{});
-        if (c < 7) {
-          double x = geo[j] + geo[D + j] * s_off[c];
-          if (args.f.bounded) x = args.f.low[j] + args.f.width[j] * x;
+      const bool mine = e < 8 * D;
+      V v = mone(V{});
+      if (mine && c < 7) {
+        double x = geo[j] + geo[D + j] * s_off[c];
+        if (args.f.bounded) x = args.f.low[j] + args.f.width[j] * x;
+        if constexpr (MF::unit && PCB_F1_SHARED_TRIG) {
+          // centre factor (c = 0) or the rotation of the offset pair c belongs to (the operations of unit_rotation();
+          // one call site for the whole warp); completed below
+          double arg = x;
+          if (c >= 3) {
+            arg = geo[D + j] * (s_off[c < 5 ? 3 : 5] - s_off[0]);
+            if (args.f.bounded) arg = args.f.width[j] * arg;
+          }
+          if (c == 0 || c >= 3) v = MF::factor(j, arg, args.f);
+        } else {
           v = MF::factor(j, x, args.f);
-          term[e] = F::term(j, x, args.f);
         }
-        tab[e] = v;   // slot c = 7 of every axis holds 1
+        term[e] = F::term(j, x, args.f);
       }
+      if constexpr (MF::unit && PCB_F1_SHARED_TRIG) {
+        // lane 8 (j mod 4) of this round holds the centre factor of the axis: rho(-delta) = conj(rho(delta)),
+        // phi(centre +- delta) = phi(centre) * rho(+-delta) -- as in the lane kernel, operand for operand
+        const V e0 = mshfl(v, lane & ~7);
+        if (c == 4) v = mconj(v);
+        else if (c == 5) v = mmul(e0, v);
+        else if (c == 6) v = mmul(e0, mconj(v));
+      }
+      if (mine) tab[e] = v;   // slot c = 7 of every axis holds 1
     }
     double vol = geo[D];
 #pragma unroll
@@ -209,7 +248,7 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const
     __syncwarp();
     // ---- 2b. unit-modulus factors: rho[j][c] = conj(phi[j][0]) * phi[j][c] for the pair candidates c = 3, 4 (in place)
     if constexpr (MF::unit) {
-      if (lane < 2 * D) {
+      if (!PCB_F1_SHARED_TRIG && lane < 2 * D) {   // with shared rotations the slots already hold rho
         const int j = lane >> 1, c = 3 + (lane & 1);
         tab[j * 8 + c] = mmul(mconj(tab[j * 8]), tab[j * 8 + c]);
       }

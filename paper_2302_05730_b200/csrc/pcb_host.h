@@ -62,7 +62,7 @@ struct Vmm {
 
 // physical chunks created ahead of time (pcb_ctx_reserve) and handed to the buffers that grow
 struct ChunkCache {
-  static constexpr size_t kChunk = (size_t)64 << 20;
+  static constexpr size_t kChunk = (size_t)64 << 20;   // measured: 256-MiB chunks map several times slower per byte (page-table setup), smaller ones cost ~0.3 ms each
   std::vector<CUmemGenericAllocationHandle> free_chunks;   // each kChunk bytes
 };
 
@@ -131,10 +131,13 @@ struct DevBuf {
     // context's pre-created 64-MiB chunks first
     // A mapping step costs ~0.25 ms whatever its size (cuMemCreate + cuMemMap + cuMemSetAccess, measured), and a
     // refinement that outgrows ten buffers by a few MiB per iteration paid more for them than for its kernels:
-    // the first step is at least 8 MiB, small buffers double, large ones (>= 256 MiB) grow by half.
+    // the first step is at least 8 MiB and a step at least doubles the buffer, up to 64 MiB of slack.  No more than
+    // that: region lists double per iteration anyway, so a large buffer needs one step per iteration whatever the
+    // policy, and creating physical memory is NOT flat in size for gigabytes (mapping 2x ahead made the first run of a
+    // process to 6e7 regions 200 ms slower).
     size_t want = bytes - cap;
     if (cap == 0 && want < ((size_t)8 << 20)) want = (size_t)8 << 20;
-    const size_t geometric = cap < ((size_t)256 << 20) ? cap : cap / 2;
+    const size_t geometric = cap < ((size_t)64 << 20) ? cap : (size_t)64 << 20;
     if (want < geometric) want = geometric;
     want = (want + gran - 1) / gran * gran;
     while (cache && want >= ChunkCache::kChunk && !cache->free_chunks.empty() && cap < bytes + ChunkCache::kChunk) {

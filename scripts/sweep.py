@@ -13,6 +13,7 @@ from paper_2302_05730_b200 import _native
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--out", default="gpurun_out/sweep")
+ap.add_argument("--reserve-gib", type=float, default=40.0)
 args = ap.parse_args()
 fams = ["f1", "f2", "f3", "f4", "f5", "f6"]
 dims = [5, 6, 7, 8]
@@ -20,6 +21,11 @@ tols = [1e-3, 1e-6] if args.quick else [1e-3, 1e-4, 1e-5, 1e-6, 1e-7, 1e-8]
 F = {d: 2**d + 2 * d * d + 2 * d + 1 for d in dims}
 rows = []
 ctx = _native.context(0)
+# one reservation for the whole sweep (pcb_ctx_reserve: physical chunks created once, buffers then grow by mapping
+# them): without it the first run that reaches ~6e7 regions pays 100-200 ms for creating its memory inside its clock
+t0 = time.perf_counter()
+reserved = ctx.reserve(int(args.reserve_gib * 2**30)) if args.reserve_gib > 0 else 0
+print(f"reserved {reserved / 2**30:.1f} GiB in {time.perf_counter() - t0:.2f} s", flush=True)
 for fam in fams:
     for d in dims:
         f = pb.get_integrand(fam, d)
@@ -27,7 +33,8 @@ for fam in fams:
         # warm-up: the first launch of a kernel pays CUDA's lazy module loading (tens of ms for the large evaluate
         # kernels); it is not part of a time-to-epsrel
         spec, orbit = f.device_spec(), pb.rules.orbit_form(pb.build_rule(d))
-        _native.pagani_refine(spec, orbit, pb.PaganiConfig(rel_tol=1e-2 if fam != "f1" else 1e-5, max_iterations=12))
+        # (a run to a 40000-region cap walks the short-list kernel, the general path and the lane kernel once)
+        _native.pagani_refine(spec, orbit, pb.PaganiConfig(rel_tol=1e-13, region_cap=40000))
         _native.mcubes_run(spec, pb.make_plan(10**8, d), 500, 1, 0, _native.RNG_REFERENCE_HASH, True, 1.5, True, 0.0,
                            keep_contributions=False)
         for tol in tols:
