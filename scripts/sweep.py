@@ -13,7 +13,7 @@ from paper_2302_05730_b200 import _native
 ap = argparse.ArgumentParser()
 ap.add_argument("--quick", action="store_true")
 ap.add_argument("--out", default="gpurun_out/sweep")
-ap.add_argument("--reserve-gib", type=float, default=40.0)
+ap.add_argument("--reserve-gib", type=float, default=0.0)
 args = ap.parse_args()
 fams = ["f1", "f2", "f3", "f4", "f5", "f6"]
 dims = [5, 6, 7, 8]
