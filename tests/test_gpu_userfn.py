@@ -113,3 +113,56 @@ def test_source_errors_and_slot_reuse():
     for k, f in enumerate(fams, start=1):
         assert f.eval_many(pts)[0] == k * 0.25 + k * 0.5
     assert fams[0].eval_many(pts)[0] == 0.75
+
+
+def test_bounds_wrapper_pagani_against_oracle():
+    d = 3
+    f, fn = _bump(d)
+    low, high = np.array([-0.5, 0.0, 0.1]), np.array([1.0, 2.0, 0.9])
+    wrapped = pb.scale_to_bounds(f, pb.IntegrationBounds(low, high))
+    rule = pb.build_rule(d)
+    lefts, lengths = random_boxes(d, 1500, 8)
+    bounds = (low, high - low, float(np.prod(high - low)))
+    want_i, want_e, _ = po.pagani_evaluate(fn, lefts, lengths, rule_dict(rule), bounds=bounds)
+    got = pb.pagani_kernel(wrapped, pb.RegionList(lefts, lengths), rule)
+    assert np.all(np.abs(got.integrals - want_i) <= 1e-12 * np.abs(want_i))
+    want = po.pagani_refine(fn, d, rule_dict(rule), rel_tol=1e-5, bounds=bounds)
+    res = pb.refine(wrapped, pb.PaganiConfig(rel_tol=1e-5), rule=rule)
+    assert (res.iterations, res.regions_processed, res.converged) == (want["iterations"], want["regions_processed"], want["converged"])
+    assert abs(res.estimate - want["estimate"]) <= 1e-10 * abs(want["estimate"])
+
+
+def test_non_finite_report_of_a_run_time_family():
+    """1 / (x_0 - 1/2) is infinite at the centre abscissa of a region centred on 1/2: same report as a built-in family."""
+    f = pb.compile_integrand(3, term="return j == 0 ? 1.0 / (x - 0.5) : x;", name="pole")
+    lefts = np.array([[0.0, 0.0, 0.0], [0.25, 0.25, 0.25], [0.0, 0.25, 0.25]])
+    lengths = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5], [1.0, 0.5, 0.5]])
+    with pytest.raises(pb.GroupTaskError) as info:
+        pb.pagani_kernel(f, pb.RegionList(np.tile(lefts, (400, 1)), np.tile(lengths, (400, 1))), pb.build_rule(3))
+    cause = info.value.cause
+    assert isinstance(cause, pb.NonFiniteEvaluationError)
+    assert cause.region_index == 1 and np.array_equal(cause.point, [0.5, 0.5, 0.5]) and np.isinf(cause.value)
+
+
+def test_sharded_refine_with_a_run_time_family():
+    """Two emulated ranks on one device (one library context per rank): same history as the single-device refinement."""
+    from paper_2302_05730_b200 import _native, rules, sharded
+    from test_gpu_sharded import run_ranks
+
+    d = 3
+    f, _ = _bump(d)
+    cfg = pb.PaganiConfig(rel_tol=1e-6)
+    want = pb.refine(f, cfg)
+    orbit = rules.orbit_form(pb.build_rule(d))
+
+    def rank_body(rank, comm):
+        ctx = _native.Context(0)
+        try:
+            shard = _native.PaganiShard(f.device_spec(), orbit, cfg, ctx=ctx)
+            return sharded.pagani_refine_sharded(f, cfg, comm, shard=shard)
+        finally:
+            ctx.close()
+
+    for res in run_ranks(2, rank_body):
+        assert res.history == want.history
+        assert (res.iterations, res.regions_processed, res.converged) == (want.iterations, want.regions_processed, want.converged)
