@@ -43,6 +43,9 @@ struct UserFamily {
   const void* fn[8] = {};   // order of pcb_user_kernel_names
 };
 static UserFamily g_user[PCB_MAX_USER_FAMILIES];
+// bumped by every load / unload: a context drops its per-kernel caches (granted shared memory, preloaded code) when it
+// sees a new value -- a reloaded slot may hand out a kernel handle with the address of one that was unloaded
+static unsigned long long g_user_generation = 0;
 static const UserFamily* user_family(int family, int d) {
   const int slot = family - PCB_USER_FAMILY_BASE;
   if (slot < 0 || slot >= PCB_MAX_USER_FAMILIES || !g_user[slot].lib || g_user[slot].d != d) return nullptr;
@@ -91,6 +94,11 @@ pcb_status validate_integrand(pcb_ctx* ctx, const pcb_integrand* f) {
   if (!f) return fail(ctx, PCB_INVALID, "integrand is NULL");
   if (f->d < 1 || f->d > PCB_MAX_DIM) return fail(ctx, PCB_INVALID, "dimension %d outside [1, %d]", f->d, PCB_MAX_DIM);
   if (f->family >= PCB_USER_FAMILY_BASE && f->family < PCB_USER_FAMILY_BASE + PCB_MAX_USER_FAMILIES) {
+    if (ctx && ctx->user_generation != g_user_generation) {
+      ctx->smem_attr.clear();
+      ctx->preloaded.clear();
+      ctx->user_generation = g_user_generation;
+    }
     if (!user_family(f->family, f->d))
       return fail(ctx, PCB_INVALID, "run-time family %d is not loaded for dimension %d (pcb_user_family_load)", f->family, f->d);
     return PCB_OK;
@@ -149,6 +157,7 @@ pcb_status pcb_user_family_load(pcb_ctx* ctx, int32_t family, int32_t d, const v
   }
   if (g_user[slot].lib) cudaLibraryUnload(g_user[slot].lib);
   g_user[slot] = u;
+  ++g_user_generation;
   return PCB_OK;
 }
 
@@ -157,6 +166,7 @@ pcb_status pcb_user_family_unload(pcb_ctx* ctx, int32_t family) {
   if (slot < 0 || slot >= PCB_MAX_USER_FAMILIES) return fail(ctx, PCB_INVALID, "run-time family id %d out of range", family);
   if (g_user[slot].lib) cudaLibraryUnload(g_user[slot].lib);
   g_user[slot] = UserFamily{};
+  ++g_user_generation;
   return PCB_OK;
 }
 

@@ -175,6 +175,7 @@ struct pcb_ctx {
   size_t total_mem = 0;
   std::map<const void*, size_t> smem_attr;  // dynamic shared memory already granted per kernel
   std::set<const void*> preloaded;          // kernels whose code is known to be loaded (lazy module loading)
+  unsigned long long user_generation = 0;   // run-time family registry state these two caches were filled under (ctx.cu)
   cudaStream_t stream = nullptr;
   std::string err;
   volatile int abort_requested = 0;   // pcb_ctx_abort(), polled by the drivers after every progress callback

@@ -113,6 +113,13 @@ def test_source_errors_and_slot_reuse():
     for k, f in enumerate(fams, start=1):
         assert f.eval_many(pts)[0] == k * 0.25 + k * 0.5
     assert fams[0].eval_many(pts)[0] == 0.75
+    # kernels that need a shared-memory grant, on recycled slots: integral of k (x + y) over the unit square = k
+    plan, grid, rule = pb.make_plan(20000, 2), pb.init_grid(2), pb.build_rule(2)
+    for k in (10, 1, 9, 2):
+        r = pb.mcubes_kernel(fams[k - 1], plan, grid, seed=k)
+        assert abs(r.integral - k) <= 5 * r.variance**0.5
+        est = pb.pagani_kernel(fams[k - 1], pb.uniform_split(2, 120), rule)      # 14400 regions: the lane kernel
+        assert abs(pb.tree_sum(est.integrals) - k) <= 1e-12 * k
 
 
 def test_bounds_wrapper_pagani_against_oracle():
