@@ -333,6 +333,12 @@ struct ShortIterArgs {
   unsigned long long* bad;     // device flag of the evaluate kernel
   ShortIterRecord* record;
   unsigned long long seq;
+  // device-resident chain (ShortState, pcb_device.cuh): the kernel always leaves the next iteration's inputs in
+  // `state`; with from_state it also TAKES n, ld_in, fin_i, fin_e and processed from there (the host enqueued it before
+  // it knew them) and returns at once when the chain has stopped
+  ShortState* state = nullptr;
+  int from_state = 0;
+  int short_max = 1024;        // longest list the chain continues with
 };
 
 // adjacent-pair tree over 1024 values, one per thread (zeros beyond the data); every thread gets the sum
@@ -448,12 +454,23 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
   __shared__ double s_ret_i[1024], s_ret_e[1024];
   __shared__ double s_emax;
   const int r = threadIdx.x, lane = r & 31, w = r >> 5;
-  const bool have = r < a.n;
   pdl_wait();   // launched behind the evaluate kernel with programmatic serialisation: its results are visible from here
+  int n = a.n;
+  long long ld_in = a.ld_in, processed = a.processed;
+  double fin_i0 = a.fin_i, fin_e0 = a.fin_e;
+  if (a.from_state) {
+    if (a.state->status != 0) return;   // CTA-uniform: the chain stopped before this iteration
+    n = (int)a.state->n;
+    ld_in = a.state->ld;
+    processed = a.state->processed;
+    fin_i0 = a.state->fin_i;
+    fin_e0 = a.state->fin_e;
+  }
+  const bool have = r < n;
   const double my_i = have ? a.integrals[r] : 0.0, my_e = have ? a.errors[r] : 0.0;
   const double sum_i = tree1024(my_i, s_warp);
   const double sum_e = tree1024(my_e, s_warp);
-  const double estimate = a.fin_i + sum_i, errorest = a.fin_e + sum_e;
+  const double estimate = fin_i0 + sum_i, errorest = fin_e0 + sum_e;
   const unsigned long long bad = *a.bad;
   __syncthreads();   // every thread holds the flag before thread 0 may re-arm it below: `action` is CTA-uniform
   int action = 0;
@@ -461,14 +478,14 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
   else if (errorest <= tolerance_target(a.rel_tol, a.abs_tol, estimate)) action = 1;
   else if (a.iteration == a.max_iterations) action = 2;
   long long n_split = 0;
-  double fin_i = a.fin_i, fin_e = a.fin_e;
+  double fin_i = fin_i0, fin_e = fin_e0;
   if (action == 0) {
     // classification (pagani.py:361-365)
     const double budget = split_budget(a.rel_tol, a.abs_tol, estimate);
     bool split = false;
     if (have) {
       double vol = a.lengths[r];
-      for (int j = 1; j < a.d; ++j) vol = vol * a.lengths[j * a.ld_in + r];  // np.prod, left to right
+      for (int j = 1; j < a.d; ++j) vol = vol * a.lengths[j * ld_in + r];  // np.prod, left to right
       split = my_e > budget * vol;
     }
     unsigned total = __syncthreads_count(split);
@@ -489,7 +506,7 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
       total = __syncthreads_count(split);
     }
     n_split = total;
-    if (a.processed + 2 * n_split > a.region_cap) {
+    if (processed + 2 * n_split > a.region_cap) {
       action = 3;
     } else {
       // stable ranks: exclusive scan of the split flags
@@ -515,8 +532,8 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
           const int axis = a.axes[r];
           const unsigned c = 2u * rank;
           for (int j = 0; j < a.d; ++j) {
-            const double left = a.lefts[j * a.ld_in + r];
-            double len = a.lengths[j * a.ld_in + r];
+            const double left = a.lefts[j * ld_in + r];
+            double len = a.lengths[j * ld_in + r];
             double upper = left;
             if (j == axis) {
               len = len * 0.5;        // half = length * 0.5
@@ -535,12 +552,21 @@ __global__ void __launch_bounds__(1024) short_iteration_kernel(const __grid_cons
       // fin += tree_sum(act[~mask]) (pagani.py:371-372)
       const double ret_i = tree1024(s_ret_i[r], s_warp);
       const double ret_e = tree1024(s_ret_e[r], s_warp);
-      fin_i = a.fin_i + ret_i;
-      fin_e = a.fin_e + ret_e;
+      fin_i = fin_i0 + ret_i;
+      fin_e = fin_e0 + ret_e;
     }
   }
   if (r == 0) {
     *a.bad = ~0ULL;   // re-arm for the next evaluation
+    if (a.state) {    // every thread read the old state before the barriers above
+      ShortState* st = a.state;
+      st->n = 2 * n_split;
+      st->ld = (2 * n_split + 31) / 32 * 32;
+      st->fin_i = fin_i;
+      st->fin_e = fin_e;
+      st->processed = processed + 2 * n_split;
+      st->status = action != 0 ? action : (2 * n_split > a.short_max ? 5 : 0);
+    }
     ShortIterRecord* rec = a.record;
     rec->estimate = estimate;
     rec->errorest = errorest;

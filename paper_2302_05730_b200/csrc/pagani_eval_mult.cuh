@@ -169,19 +169,25 @@ __global__ void __launch_bounds__(kEvalWarps * 32) pagani_eval_mult_kernel(const
   double* term = s_term[wib];
   const char* term_b = reinterpret_cast<const char*>(term);
   double* store = s_store[wib];
-  const long long ld = args.ld, stride = (long long)gridDim.x * kEvalWarps;
+  long long n_regions = args.n, ld = args.ld;
+  if (args.state) {   // launched before the host knew the list: length and stride come from the previous iteration kernel
+    if (args.state->status != 0) return;
+    n_regions = args.state->n;
+    ld = args.state->ld;
+  }
+  const long long stride = (long long)gridDim.x * kEvalWarps;
   long long r = (long long)blockIdx.x * kEvalWarps + wib;
   int buf = 0;
-  if (r < args.n && lane < 2 * D)
+  if (r < n_regions && lane < 2 * D)
     s_geo[wib][0][lane] = (lane < D) ? args.lefts[lane * ld + r] : args.lengths[(lane - D) * ld + r];
   __syncwarp();
 
-  for (; r < args.n; r += stride, buf ^= 1) {
+  for (; r < n_regions; r += stride, buf ^= 1) {
     const double* geo = s_geo[wib][buf];
     // prefetch the next region's geometry (consumed at the bottom of the loop)
     const long long rn = r + stride;
     double next_geo = 0.0;
-    if (rn < args.n && lane < 2 * D) next_geo = (lane < D) ? args.lefts[lane * ld + rn] : args.lengths[(lane - D) * ld + rn];
+    if (rn < n_regions && lane < 2 * D) next_geo = (lane < D) ? args.lefts[lane * ld + rn] : args.lengths[(lane - D) * ld + rn];
 
     // ---- 1. per-axis tables at the 7 distinct abscissae (quadrature.py:301-302: mul, then add)
 #pragma unroll

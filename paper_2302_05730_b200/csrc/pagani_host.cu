@@ -44,8 +44,11 @@ static int eval_grid(pcb_ctx* ctx, const void* fn, long long n) {
 // launch the evaluate kernel on SoA device buffers; `bad_dev` must already hold ~0
 static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rule* rule, const pcb_pagani_config* cfg,
                                   long long n, long long ld, const double* lefts, const double* lengths, double* I, double* E,
-                                  int32_t* K, unsigned long long* bad_dev) {
+                                  int32_t* K, unsigned long long* bad_dev, const ShortState* state = nullptr) {
+  // state != NULL: a speculative launch for a list of at most n regions whose length and stride the kernel takes from
+  // the device (warp-per-region kernels only)
   EvalArgs a;
+  a.state = state;
   a.f = *f;
   a.rule = *rule;
   a.n = n;
@@ -75,7 +78,7 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   // the lane kernels hard-wire which rule alternates its corner weights with the bit count (kParityRule)
   bool parity_ok = true;
   for (int k = 0; k < 5; ++k) parity_ok = parity_ok && ((rule->corner_parity[k] != 0) == (k == kParityRule));
-  if (lanes_fn && parity_ok && lanes_smem <= lanes_cap && n >= lanes_min) {
+  if (!state && lanes_fn && parity_ok && lanes_smem <= lanes_cap && n >= lanes_min) {
     size_t& have = ctx->smem_attr[lanes_fn];
     if (have < lanes_smem) {
       PCB_CUDA_TRY(ctx, cudaFuncSetAttribute(lanes_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lanes_smem));
@@ -90,7 +93,7 @@ static pcb_status evaluate_launch(pcb_ctx* ctx, const pcb_integrand* f, const pc
   }
   // widths above 64 take the exact-order kernel in its block-walking form (pagani.py:175-192 for any G)
   const void* fn = cfg->group_size > 64 ? eval_wide_kernel(f->family, f->d) : eval_kernel(f->family, f->d);
-  ProfileSpan span(ctx, 0, (double)n);
+  ProfileSpan span(ctx, 0, state ? 0.0 : (double)n);
   PCB_CUDA_TRY(ctx, launch(ctx, fn, dim3(eval_grid(ctx, fn, n)), dim3(kEvalWarps * 32), 0, a));
   return PCB_OK;
 }
@@ -230,10 +233,10 @@ static pcb_status read_scalars(pcb_ctx* ctx, int first, int count) {
 // regions: see DESIGN 4.2).  The stream is queried now and then so that a failed launch surfaces instead of hanging.
 static pcb_status publish_scalars(pcb_ctx* ctx, int first, int count) {
   if (!ctx->pg_record) {
-    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 256));
-    std::memset(ctx->pg_record, 0, 256);
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 512));
+    std::memset(ctx->pg_record, 0, 512);
   }
-  volatile unsigned long long* seq_word = reinterpret_cast<volatile unsigned long long*>(static_cast<char*>(ctx->pg_record) + 128);
+  volatile unsigned long long* seq_word = reinterpret_cast<volatile unsigned long long*>(static_cast<char*>(ctx->pg_record) + 256);
   const unsigned long long seq = ++ctx->pg_seq;
   PCB_CUDA_TRY(ctx, launch(ctx, (const void*)&publish_scalars_kernel, dim3(1), dim3(32), 0,
                            (const unsigned long long*)ctx->scalars.as<unsigned long long>(), first, count,
@@ -400,11 +403,23 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   // short lists (<= 1024 regions) run the whole iteration in one CTA and hand one record back through pinned memory
   bool use_short = true;
   if (const char* env = std::getenv("PCB_PAGANI_SHORT")) use_short = std::atoi(env) != 0;
-  if (!ctx->pg_record) {   // bytes [0, 128): the short-iteration record, [128, 256): the sequence word of publish_scalars
-    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 256));
-    std::memset(ctx->pg_record, 0, 256);
+  if (!ctx->pg_record) {   // bytes [0, 256): a ring of four short-iteration records, [256, 512): the sequence word of publish_scalars
+    PCB_CUDA_TRY(ctx, cudaMallocHost(&ctx->pg_record, 512));
+    std::memset(ctx->pg_record, 0, 512);
   }
-  ShortIterRecord* srec = static_cast<ShortIterRecord*>(ctx->pg_record);
+  static_assert(sizeof(ShortIterRecord) == 64, "four records fit the ring");
+  ShortIterRecord* srec_ring = static_cast<ShortIterRecord*>(ctx->pg_record);
+  // The short-list chain is device-resident (ShortState): while it lasts the host enqueues the evaluate kernel and the
+  // iteration kernel of iteration it+1 -- which take the list length, the running totals and the stop decision from
+  // the device -- BEFORE it polls the record of iteration it, so the device never idles on the round trip.
+  // PCB_PAGANI_SPECULATE=0: one iteration at a time (A/B runs).  Not with the lane kernels forced onto short lists.
+  bool speculate_short = true;
+  if (const char* env = std::getenv("PCB_PAGANI_SPECULATE")) speculate_short = std::atoi(env) != 0;
+  if (const char* env = std::getenv("PCB_PAGANI_LANES_MIN")) speculate_short = speculate_short && std::atoll(env) > 1024;
+  ShortState* state_dev = reinterpret_cast<ShortState*>(sc + 8);   // slots 8..13 of the scalar block (zeroed above)
+  static_assert(sizeof(ShortState) <= 8 * sizeof(double), "the state fits the upper half of the scalar block");
+  int short_enqueued_upto = -1;   // newest iteration whose iteration kernel is already in the stream
+  const unsigned long long run_token = ++ctx->pg_seq;   // record sequence words: (token << 20) | (iteration + 1)
 
   for (int it = 0; it <= cfg->max_iterations; ++it) {
     if (use_short && n >= 1 && n <= 1024) {
@@ -415,35 +430,58 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
         have_retired = false;
       }
       const int nxt = cur ^ 1;
-      const long long ld_cap = round_up(2 * n, 32);
-      PCB_CUDA_TRY(ctx, ctx->lefts[nxt].ensure((size_t)ld_cap * d * sizeof(double)));
-      PCB_CUDA_TRY(ctx, ctx->lengths[nxt].ensure((size_t)ld_cap * d * sizeof(double)));
-      ShortIterArgs sa;
-      sa.n = (int)n; sa.d = d; sa.ld_in = ld; sa.ld_out_unused = 0;
-      sa.lefts = ctx->lefts[cur].as<double>();
-      sa.lengths = ctx->lengths[cur].as<double>();
-      sa.integrals = ctx->est_i.as<double>();
-      sa.errors = ctx->est_e.as<double>();
-      sa.axes = ctx->est_k.as<int32_t>();
-      sa.out_lefts = ctx->lefts[nxt].as<double>();
-      sa.out_lengths = ctx->lengths[nxt].as<double>();
-      sa.fin_i = fin_i; sa.fin_e = fin_e;
-      sa.processed = processed; sa.region_cap = cfg->region_cap;
-      sa.rel_tol = cfg->rel_tol;
-      sa.abs_tol = cfg->abs_tol;
-      sa.iteration = it; sa.max_iterations = cfg->max_iterations;
-      sa.bad = sc_u + S_BAD;
-      sa.record = srec;
-      sa.seq = ++ctx->pg_seq;
-      {  // dependent launch: resident behind the evaluate kernel, waits for its results (pdl_wait)
-        void* args[] = {&sa};
+      // both list buffers hold the children of a full short list (2048 regions), the estimate arrays a full short list
+      const long long ld_cap = 2048;
+      for (int b2 = 0; b2 < 2; ++b2) {
+        PCB_CUDA_TRY(ctx, ctx->lefts[b2].ensure((size_t)ld_cap * d * sizeof(double)));
+        PCB_CUDA_TRY(ctx, ctx->lengths[b2].ensure((size_t)ld_cap * d * sizeof(double)));
+      }
+      PCB_CUDA_TRY(ctx, ctx->est_i.ensure((size_t)1024 * sizeof(double)));
+      PCB_CUDA_TRY(ctx, ctx->est_e.ensure((size_t)1024 * sizeof(double)));
+      PCB_CUDA_TRY(ctx, ctx->est_k.ensure((size_t)1024 * sizeof(int32_t)));
+      // iteration kernel of iteration k reading list buffer `in`; from_state: inputs from the device state
+      auto launch_short = [&](int k, int in, bool from_state) -> pcb_status {
+        ShortIterArgs sa;
+        sa.n = (int)n; sa.d = d; sa.ld_in = ld; sa.ld_out_unused = 0;
+        sa.lefts = ctx->lefts[in].as<double>();
+        sa.lengths = ctx->lengths[in].as<double>();
+        sa.integrals = ctx->est_i.as<double>();
+        sa.errors = ctx->est_e.as<double>();
+        sa.axes = ctx->est_k.as<int32_t>();
+        sa.out_lefts = ctx->lefts[in ^ 1].as<double>();
+        sa.out_lengths = ctx->lengths[in ^ 1].as<double>();
+        sa.fin_i = fin_i; sa.fin_e = fin_e;
+        sa.processed = processed; sa.region_cap = cfg->region_cap;
+        sa.rel_tol = cfg->rel_tol;
+        sa.abs_tol = cfg->abs_tol;
+        sa.iteration = k; sa.max_iterations = cfg->max_iterations;
+        sa.bad = sc_u + S_BAD;
+        sa.record = srec_ring + (k & 3);
+        sa.seq = ((unsigned long long)run_token << 20) | (unsigned long long)(k + 1);
+        sa.state = state_dev;
+        sa.from_state = from_state ? 1 : 0;
+        sa.short_max = 1024;
+        void* args[] = {&sa};   // dependent launch: resident behind the evaluate kernel, waits for its results (pdl_wait)
         PCB_CUDA_TRY(ctx, launch_pdl((const void*)&short_iteration_kernel, dim3(1), dim3(1024), args, 0, ctx->stream));
         ctx->launches++;
+        short_enqueued_upto = k;
+        return PCB_OK;
+      };
+      if (short_enqueued_upto < it) PCB_TRY(launch_short(it, cur, false));
+      bool next_enqueued = short_enqueued_upto > it;
+      if (speculate_short && !next_enqueued && it < cfg->max_iterations) {
+        // iteration it+1 on the state iteration it leaves behind: evaluate the children (list buffer nxt), then iterate
+        PCB_TRY(evaluate_launch(ctx, f, rule, cfg, 1024, 0, ctx->lefts[nxt].as<double>(), ctx->lengths[nxt].as<double>(),
+                                ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), sc_u + S_BAD, state_dev));
+        PCB_TRY(launch_short(it + 1, nxt, true));
+        next_enqueued = true;
       }
-      for (unsigned spin = 0; srec->seq != sa.seq; ++spin) {
+      const ShortIterRecord* srec = srec_ring + (it & 3);
+      const unsigned long long want_seq = ((unsigned long long)run_token << 20) | (unsigned long long)(it + 1);
+      for (unsigned spin = 0; srec->seq != want_seq; ++spin) {
         if ((spin & 0xfff) == 0xfff) {
           cudaError_t e = cudaStreamQuery(ctx->stream);
-          if (e != cudaErrorNotReady && srec->seq != sa.seq) {
+          if (e != cudaErrorNotReady && srec->seq != want_seq) {
             (void)cudaGetLastError();
             return fail(ctx, PCB_CUDA, "pagani_refine: short iteration did not publish its record (%s)", cudaGetErrorString(e));
           }
@@ -483,7 +521,9 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       n = 2 * n_split;
       ld = round_up(n, 32);
       cur = nxt;
-      PCB_TRY(evaluate(n, ld, false));
+      // the chain goes on by itself while the list stays short; a longer list ended it on the device (status 5: the
+      // kernels enqueued ahead return at once) and is evaluated from here
+      if (!(next_enqueued && n >= 1 && n <= 1024)) PCB_TRY(evaluate(n, ld, false));
       continue;
     }
     PCB_TRY(tree_sum2_dev(ctx, ctx->est_i.as<double>(), ctx->est_e.as<double>(), n, sc + S_SUM_I, sc + S_SUM_E));
