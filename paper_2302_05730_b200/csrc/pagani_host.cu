@@ -359,6 +359,20 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
   n = (long long)exact;
 
   PCB_TRY(preload_refine_kernels(ctx, f, cfg));
+  // no list of this run is longer than the region cap: bounds for the buffers that scale with the list
+  // (DevBuf::hint_max), withdrawn when the run ends -- the sharded entry points size the same buffers per rank
+  struct HintGuard {
+    pcb_ctx* c;
+    void set(size_t list_bytes, size_t scalar_bytes) const {
+      for (int b2 = 0; b2 < 2; ++b2) c->lefts[b2].hint_max = c->lengths[b2].hint_max = list_bytes;
+      c->est_i.hint_max = c->est_e.hint_max = c->ret_i.hint_max = c->ret_e.hint_max = scalar_bytes;
+    }
+    ~HintGuard() { set(0, 0); }
+  } hint_guard{ctx};
+  {
+    const size_t cap_regions = (size_t)round_up(cfg->region_cap, 32);
+    hint_guard.set(cap_regions * d * sizeof(double), cap_regions * sizeof(double));
+  }
   // scalars travel through pinned memory (publish_scalars); PCB_PAGANI_PUBLISH=0: copy + synchronise (A/B runs)
   static const bool use_publish = [] { const char* e = std::getenv("PCB_PAGANI_PUBLISH"); return !(e && std::atoi(e) == 0); }();
   auto fetch = use_publish ? publish_scalars : read_scalars;

@@ -72,6 +72,12 @@ struct DevBuf {
   const int* device = nullptr;        // the owning context's device ordinal
   ChunkCache* cache = nullptr;        // the owning context's pre-created chunks
   size_t va = 0;
+  // Upper bound of what this buffer can ever be asked for in the current run (0: unknown).  Once a request passes
+  // kHintFrom the buffer grows straight to the bound: a list that has reached half a gigabyte is on its way to the region
+  // cap, and ONE large mapping step per buffer and process is cheaper -- and less erratic -- than one per iteration
+  // (steps of gigabytes occasionally stall for 50-150 ms, profiles/r2_sweep_config5.md).
+  size_t hint_max = 0;
+  static constexpr size_t kHintFrom = (size_t)512 << 20;
   struct Mapped { CUmemGenericAllocationHandle h; size_t bytes; };
   std::vector<Mapped> chunks;
   static constexpr size_t kVirtual = (size_t)1 << 37;   // 128 GiB of address space per buffer
@@ -139,6 +145,7 @@ struct DevBuf {
     if (cap == 0 && want < ((size_t)8 << 20)) want = (size_t)8 << 20;
     const size_t geometric = cap < ((size_t)64 << 20) ? cap : (size_t)64 << 20;
     if (want < geometric) want = geometric;
+    if (hint_max > bytes && bytes >= kHintFrom && want < hint_max - cap) want = hint_max - cap;
     want = (want + gran - 1) / gran * gran;
     while (cache && want >= ChunkCache::kChunk && !cache->free_chunks.empty() && cap < bytes + ChunkCache::kChunk) {
       CUmemGenericAllocationHandle h = cache->free_chunks.back();
