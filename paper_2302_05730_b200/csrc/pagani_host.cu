@@ -483,10 +483,12 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       };
       if (short_enqueued_upto < it) PCB_TRY(launch_short(it, cur, false));
       bool next_enqueued = short_enqueued_upto > it;
+      long spec_span = -1;
       if (speculate_short && !next_enqueued && it < cfg->max_iterations) {
         // iteration it+1 on the state iteration it leaves behind: evaluate the children (list buffer nxt), then iterate
         PCB_TRY(evaluate_launch(ctx, f, rule, cfg, 1024, 0, ctx->lefts[nxt].as<double>(), ctx->lengths[nxt].as<double>(),
                                 ctx->est_i.as<double>(), ctx->est_e.as<double>(), ctx->est_k.as<int32_t>(), sc_u + S_BAD, state_dev));
+        spec_span = ctx->profiling ? (long)ctx->spans[0].size() - 1 : -1;   // its region count is filled in below
         PCB_TRY(launch_short(it + 1, nxt, true));
         next_enqueued = true;
       }
@@ -537,7 +539,9 @@ pcb_status pcb_pagani_refine(pcb_ctx* ctx, const pcb_integrand* f, const pcb_rul
       cur = nxt;
       // the chain goes on by itself while the list stays short; a longer list ended it on the device (status 5: the
       // kernels enqueued ahead return at once) and is evaluated from here
-      if (!(next_enqueued && n >= 1 && n <= 1024)) PCB_TRY(evaluate(n, ld, false));
+      const bool chained = next_enqueued && n >= 1 && n <= 1024;
+      if (spec_span >= 0 && chained) ctx->spans[0][spec_span].units = (double)n;   // profiling: what the speculative launch evaluated
+      if (!chained) PCB_TRY(evaluate(n, ld, false));
       continue;
     }
     PCB_TRY(tree_sum2_dev(ctx, ctx->est_i.as<double>(), ctx->est_e.as<double>(), n, sc + S_SUM_I, sc + S_SUM_E));
