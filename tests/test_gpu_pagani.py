@@ -459,3 +459,36 @@ def test_progress_exception_stops_the_run_at_once():
     assert seen == [0, 1, 2]
     res = pb.refine(pb.get_integrand("f4", 5), pb.PaganiConfig(rel_tol=1e-3))
     assert (res.iterations, res.regions_processed) == (10, 3328)
+
+
+_REFINE_SNIPPET = r"""
+import json
+import paper_2302_05730_b200 as pb
+out = []
+for fam, d, kw in [("f4", 5, dict(rel_tol=1e-5)), ("f2", 5, dict(rel_tol=1e-3)), ("f1", 6, dict(rel_tol=1e-3)),
+                   ("f3", 5, dict(rel_tol=1e-6, region_cap=100000)), ("f5", 4, dict(rel_tol=1e-5, initial_regions=16)),
+                   ("f4", 5, dict(rel_tol=1e-3, group_size=96)), ("f6", 3, dict(rel_tol=1e-9, max_iterations=9))]:
+    r = pb.refine(pb.get_integrand(fam, d), pb.PaganiConfig(**kw))
+    out.append([r.estimate, r.errorest, r.iterations, int(r.regions_processed), r.reason, [list(h) for h in r.history]])
+print(json.dumps(out))
+"""
+
+
+def test_refine_launch_modes_agree_bit_for_bit():
+    """How the refinement is driven is scheduling only: programmatic launches (PCB_NO_PDL=1: plain), scalars through
+    pinned memory (PCB_PAGANI_PUBLISH=0: copy + synchronise) and the device-resident short-list chain
+    (PCB_PAGANI_SPECULATE=0: one iteration at a time) give the same histories, bit for bit."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for extra in ({}, {"PCB_NO_PDL": "1"}, {"PCB_PAGANI_PUBLISH": "0"}, {"PCB_PAGANI_SPECULATE": "0"},
+                  {"PCB_NO_PDL": "1", "PCB_PAGANI_PUBLISH": "0", "PCB_PAGANI_SPECULATE": "0"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        res = subprocess.run([sys.executable, "-c", _REFINE_SNIPPET], env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr[-2000:]
+        outs.append(json.loads(res.stdout.strip().splitlines()[-1]))
+    assert all(o == outs[0] for o in outs[1:])
