@@ -401,8 +401,16 @@ def _pagani_refine_device(f, cfg, comm, shard, progress, force_collectives):
     abs_tol = getattr(cfg, "abs_tol", 0.0)
     stream = None
 
+    stream_ctx = {}
+
     def on_stream():
-        return torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", dev)))
+        # the library's stream as torch's current one; the wrapper object is built once per stream handle
+        ext = stream_ctx.get(stream)
+        if ext is None:
+            ext = stream_ctx[stream] = torch.cuda.ExternalStream(stream, device=torch.device("cuda", dev))
+        return torch.cuda.stream(ext)
+
+    counts_host = torch.empty((world, 2), dtype=torch.float64).pin_memory()   # (split count, max error) of every rank
 
     try:
         shard.init(g, first, last - first)
@@ -455,7 +463,9 @@ def _pagani_refine_device(f, cfg, comm, shard, progress, force_collectives):
                     gt = _device_tensor(gatheredb, dev)
                     if collect:
                         comm.all_gather_into(gt, _device_tensor(rowb, dev))
-                    vals = gt.cpu().numpy().reshape(world, 2)
+                    counts_host.copy_(gt.view(world, 2), non_blocking=True)     # pinned target: no staging allocation
+                    torch.cuda.current_stream().synchronize()
+                    vals = counts_host.numpy()
                 return [int(round(v)) for v in vals[:, 0]], float(vals[:, 1].max())
 
             split_counts, emax = classify(0, 0.0)
